@@ -1,0 +1,220 @@
+/* b200-tencache C-ABI — the thin boundary between host code (C++ decision
+ * engine, Python mirror, or any FFI) and the B200 data plane.
+ *
+ * The reference has no C ABI (its interface is C++: IPolicy, engine.hpp:52-74,
+ * and the free functions of scheduler.hpp:73-111); SURVEY.md §8(b) fixes what
+ * this layer must export. Each entry below cites the reference interface it
+ * replaces or serves. All functions return 0 on success or a TC_E* code; the
+ * message of the last failure on the calling thread is tc_last_error().
+ * Exceptions never cross this boundary. There is no CPU fallback: a data-plane
+ * call on a machine without a B200 fails with TC_ECUDA.
+ */
+#ifndef TENCACHE_C_H_
+#define TENCACHE_C_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* ---- status codes: one per reference exception type ---- */
+enum {
+  TC_OK = 0,
+  TC_EINTERNAL = 1,   /* std::logic_error incl. SchedulerError (scheduler.cpp:10-13) */
+  TC_ECONFIG = 2,     /* ConfigError (types.hpp:30-33) */
+  TC_EOOM = 3,        /* OomError (types.hpp:35-38) */
+  TC_ETRACE = 4,      /* TraceError (trace.hpp:58-61) */
+  TC_EPOOL = 5,       /* PoolError (bufpool.hpp:18-21) */
+  TC_EARG = 6,        /* std::invalid_argument / domain_error / bad handle */
+  TC_ECUDA = 7,       /* CUDA runtime failure (no reference counterpart) */
+  TC_EIO = 8,         /* NVMe tier file I/O failure (no reference counterpart) */
+  TC_ENCCL = 9        /* NCCL failure (no reference counterpart) */
+};
+
+const char* tc_last_error(void);
+const char* tc_version(void);
+
+/* =================== decision engine (reference C++ API, host) ========== */
+/* One TransferRequest (scheduler.hpp:20-33). flags: 1 via_cpu_staging,
+ * 2 instant, 4 src_retains, 8 dst_has_copy, 16 blocking. Tiers 0 gpu 1 cpu
+ * 2 nvme; kind 0 prefetch 1 evict 2 restore. */
+typedef struct {
+  uint32_t tensor_id;
+  uint8_t src, dst, kind, flags;
+  uint64_t size_bytes;
+} tc_request;
+
+typedef struct tc_policy tc_policy;
+
+/* make_policy(trace, machine, config) + IPolicy::init (engine.hpp:62,73;
+ * policies.cpp:33-93). machine_path "" = default_machine() (machine.cpp:24-40);
+ * cfg_json keys: policy, thresholds_us, restore_overlap, batch_scale,
+ * zero_lookahead_k, seed (engine.hpp:19-27). info = InitInfo
+ * {gpu, cpu, nvme resident bytes, fp16_in_nvme_count} (engine.hpp:54-59). */
+int tc_policy_create(const char* trace_path, const char* machine_path, const char* cfg_json, tc_policy** out,
+                     uint64_t info[4]);
+void tc_policy_destroy(tc_policy* p);
+
+/* IPolicy hooks (engine.hpp:63-70): hook 0 on_step_begin(step), 1
+ * on_step_end(step), 2 on_param_restore_point, 3 on_iteration_end,
+ * 4 reset_iteration. Writes min(n, cap) requests; *n = total. */
+int tc_policy_call(tc_policy* p, int hook, uint32_t step, tc_request* out, size_t cap, size_t* n);
+
+/* Pool views for buffer-assignment parity and the executor (bufpool.hpp:41-95):
+ * which 0 gpu, 1 cpu (parameter cache), 2 cpu_opt. occupant per buffer id,
+ * 0 = free, negative = GPU-designated. layout = (offset, size) per buffer id. */
+int tc_policy_pool(const tc_policy* p, int which, int64_t* occupant, size_t cap, size_t* n);
+int tc_policy_layout(const tc_policy* p, int which, uint64_t* offset_size, size_t cap, size_t* n);
+/* Logical buffer id currently holding `tensor` in pool `which`, or -1. */
+int64_t tc_policy_buffer_of(const tc_policy* p, int which, uint32_t tensor);
+/* Number of steps / iterations of the trace and the index of the first
+ * optimizer step (== steps when none): the engine call order of engine.cpp:363-431. */
+int tc_policy_shape(const tc_policy* p, uint32_t* steps, uint32_t* iterations, uint32_t* first_opt_step);
+
+/* run() (engine.hpp:78, engine.cpp:572-576): model-clock run; SimReport JSON
+ * (exact rationals as "num/den") to report_path, event log JSONL to
+ * events_path ("" = none). reference_guard != 0 applies run_reference's
+ * 64-tensor guard (engine.hpp:81-83). */
+int tc_run(const char* trace_path, const char* machine_path, const char* cfg_json, const char* report_path,
+           const char* events_path, int reference_guard);
+/* The policy call sequence of one run with pool contents after every call,
+ * as JSON (same schema as the oracle's golden streams). */
+int tc_decisions(const char* trace_path, const char* machine_path, const char* cfg_json, const char* out_path,
+                 int with_pools);
+/* synthesize_transformer_trace + save_trace (trace.hpp:76-87). */
+int tc_synthesize(uint32_t layers, uint32_t tensors_per_layer, const uint64_t* sizes, int nsizes,
+                  double compute_us_per_byte, uint64_t seed, uint32_t iterations, double opt_us_per_byte,
+                  int optimizer_steps, const char* out_path);
+int tc_trace_roundtrip(const char* in_path, const char* out_path);
+/* transfer_time_us (machine.cpp:101-111) as an exact "num/den" string. */
+int tc_transfer_time(const char* machine_path, int src, int dst, uint64_t bytes, char* out, size_t out_len);
+/* Wall-clock cost of the host decision path: init and one iteration of
+ * policy calls (ns), averaged over `iterations`. */
+int tc_time_decisions(const char* trace_path, const char* machine_path, const char* cfg_json, int iterations,
+                      double* ns_per_iteration, double* init_ns);
+int tc_time_run(const char* trace_path, const char* machine_path, const char* cfg_json, int repeats,
+                double* ns_per_run);
+
+/* ========================= data plane: sm_100a kernels ================== */
+/* All pointers are device pointers unless stated; `stream` is a cudaStream_t
+ * (NULL = legacy default). Kernels are asynchronous. */
+
+/* A fragment: `bytes` at src_base+src_off -> dst_base+dst_off. */
+typedef struct {
+  uint64_t src_off;
+  uint64_t dst_off;
+  uint64_t bytes;
+} tc_segment;
+
+/* pack / unpack of fragmented tensors into one pooled chunk:
+ * one launch for the whole fragment list; `segs` is a DEVICE array. pack and
+ * unpack are the same gather/scatter with roles swapped; both entry points
+ * exist so call sites read like the reference's vocabulary. */
+int tc_pack(const void* src_base, void* chunk, const tc_segment* segs, uint32_t n, void* stream);
+int tc_unpack(const void* chunk, void* dst_base, const tc_segment* segs, uint32_t n, void* stream);
+
+/* bf16 <-> fp32 casts (RNE, NaN -> quiet NaN; torch .to() semantics). */
+int tc_cast_bf16_to_f32(const void* in, float* out, uint64_t n, void* stream);
+int tc_cast_f32_to_bf16(const float* in, void* out, uint64_t n, void* stream);
+
+/* Fused AdamW on one optimizer-state chunk (the offloaded optimizer step the
+ * reference models as a timed no-op; trace.hpp:72-74 sizes it at
+ * 6x the bf16 parameter bytes). state = [p32 | m | v], n elements each,
+ * fp32; grad = bf16; param_out = bf16 copy of the updated p32 (may be NULL).
+ * lr/b1/b2/eps/wd/step as torch.optim.AdamW; grad_scale multiplies g. */
+int tc_adamw(float* state, const void* grad, void* param_out, uint64_t n, double lr, double beta1, double beta2,
+             double eps, double weight_decay, int64_t step, float grad_scale, void* stream);
+/* Same update with p32/m/v at independent addresses. */
+int tc_adamw_split(float* p32, float* m, float* v, const void* grad, void* param_out, uint64_t n, double lr,
+                   double beta1, double beta2, double eps, double weight_decay, int64_t step, float grad_scale,
+                   void* stream);
+/* The 8 fp32 scalars the update uses, for parity tests. */
+int tc_adamw_scalars(double lr, double beta1, double beta2, double eps, double weight_decay, int64_t step,
+                     float out[8]);
+
+/* Checksum of `bytes` (multiple of 4) at `data`: sum of u32 word * (2i+1)
+ * mod 2^64, accumulated into *out (device u64). The forward/backward
+ * stand-in reads every migrated byte through this. */
+int tc_checksum(const void* data, uint64_t bytes, uint64_t* out, void* stream);
+/* Busy the compute stream for `us` microseconds on `ctas` CTAs (the layer
+ * compute stand-in; trace compute_us, trace.hpp:38). */
+int tc_spin(double us, int ctas, void* stream);
+
+/* ====================== migration executor (real mode) ================= */
+/* A per-GPU engine: pinned host pools and an HBM pool carved exactly like the
+ * policy's BufferPools (bufpool.cpp:47-66), dedicated H2D/D2H streams,
+ * per-slot events, and an NVMe tier staged through pinned bounce buffers.
+ * It replays the policy's TransferRequests (scheduler.hpp:20-33) as
+ * copy-engine work ordered against a compute stream. */
+typedef struct tc_engine tc_engine;
+
+typedef struct {
+  int device;              /* CUDA device ordinal */
+  const char* nvme_dir;    /* directory for the NVMe tier file ("" = none) */
+  int gpu_spare_slots;     /* extra HBM slots per class for restore cycles */
+  int host_spare_slots;    /* extra pinned slots per class */
+  int opt_stage_slots;     /* HBM staging buffers for the optimizer pipeline */
+  int direct_io;           /* O_DIRECT for the NVMe tier */
+  uint64_t grad_bytes_per_param_byte; /* gradient bytes per bf16 param byte (1) */
+} tc_engine_options;
+
+int tc_engine_create(const char* trace_path, const char* machine_path, const char* cfg_json,
+                     const tc_engine_options* opts, tc_engine** out);
+void tc_engine_destroy(tc_engine* e);
+
+/* Fill every tensor's home copy with deterministic data (seeded), zero the
+ * optimizer moments, and put the engine at the start of an iteration. */
+int tc_engine_seed(tc_engine* e, uint64_t seed);
+
+/* Host-side copies of a tensor, wherever it currently lives (for tests and the
+ * end-to-end API): read into / write from a HOST buffer of its size. */
+int tc_engine_read_tensor(tc_engine* e, uint32_t tensor, void* host_dst, uint64_t bytes);
+int tc_engine_write_tensor(tc_engine* e, uint32_t tensor, const void* host_src, uint64_t bytes);
+/* Device pointer of the tensor's current GPU slot (NULL if not GPU-resident). */
+void* tc_engine_gpu_ptr(tc_engine* e, uint32_t tensor);
+/* Gradient buffer (bf16, on GPU) of a parameter tensor. */
+void* tc_engine_grad_ptr(tc_engine* e, uint32_t tensor);
+
+typedef struct {
+  double lr, beta1, beta2, eps, weight_decay;
+  float grad_scale;
+  int compute_mode;    /* 0: checksum only, 1: checksum + spin for compute_us*batch_scale */
+  int spin_ctas;
+} tc_step_options;
+
+/* One training iteration: every trace step in order, policy decisions at the
+ * engine's fixed call points (engine.cpp:363-431), transfers on the copy
+ * streams, the fwd/bwd stand-in and the fused AdamW on the compute stream.
+ * Asynchronous w.r.t. the host only where CUDA allows; returns after
+ * enqueueing (call tc_engine_sync to wait). */
+int tc_engine_iteration(tc_engine* e, const tc_step_options* so, void* compute_stream);
+int tc_engine_sync(tc_engine* e);
+
+/* Counters of the last iteration(s) since the previous reset_stats. */
+typedef struct {
+  uint64_t h2d_bytes, d2h_bytes;         /* cache-decision bytes over PCIe (category i) */
+  uint64_t opt_h2d_bytes, opt_d2h_bytes; /* optimizer round trip (category ii) */
+  uint64_t writeback_bytes;              /* updated-param write-back (category iii) */
+  uint64_t nvme_read_bytes, nvme_write_bytes; /* category iv */
+  uint64_t param_accesses, param_hits;   /* engine_internal.hpp:98-102 definition */
+  uint64_t ontime_accesses;              /* prefetched accesses already landed */
+  uint64_t requests, kernel_launches, copies;
+  double h2d_busy_ms, d2h_busy_ms;       /* copy-engine busy time (event pairs) */
+  double stall_ms;                       /* compute stream waiting on copies */
+  double adam_ms;                        /* fused AdamW kernel time */
+  uint64_t adam_elems;
+} tc_engine_stats;
+
+int tc_engine_stats_get(tc_engine* e, tc_engine_stats* out);
+int tc_engine_stats_reset(tc_engine* e);
+/* checksum the fwd/bwd stand-in computed for each parameter access of the
+ * last iteration (device -> host copy), in access order. */
+int tc_engine_access_checksums(tc_engine* e, uint64_t* out, size_t cap, size_t* n);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* TENCACHE_C_H_ */

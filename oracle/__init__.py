@@ -1,0 +1,5 @@
+"""ORACLE TEST INFRASTRUCTURE — not product code.
+
+Only tests/, __graft_entry__.smoke() and bench.py's cpu_baseline /
+``--impl reference`` legs may import this package.
+"""
