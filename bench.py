@@ -1,0 +1,417 @@
+#!/usr/bin/env python
+"""Benchmark of the 10Cache migration path on B200 (BASELINE.json metric:
+"step time & migrated GB/s per GPU vs PCIe roofline; GPU cache hit rate").
+
+One step = one training iteration of the chunk trace through the engine:
+TenCache decisions at every hook, cache migrations on the H2D/D2H copy
+engines, the forward/backward stand-in (checksum of every accessed chunk +
+the trace's compute time as a calibrated spin) and the fused AdamW over every
+optimizer-state chunk streamed from pinned host memory.
+
+value  = cache-decision migrated GB/s (whole job) = sum of the policy's
+         non-instant TransferRequest bytes per step / step time. The numerator
+         is bit-identical to the reference's transfer_bytes (same decisions),
+         so the ratio to the reference arm is the true step-time ratio.
+Also reported: ms_per_step, PCIe GB/s per direction over all categories
+(decisions + optimizer round trip + write-back) vs the measured PCIe peak,
+hidden-migration fraction, exact hit rate, on-time rate, and the dominant
+kernel's HBM roofline.
+
+--impl reference runs the reference's own CPU path: the reference IPolicy
+(oracle/_ref, the unmodified reference compiled here) makes the decisions,
+each migration is a host memcpy between tier buffers, the stand-in checksums
+on the CPU, the trace compute time elapses, and AdamW runs on the host cores
+(oracle/numerics.c, OpenMP) — the paper's CPU-Adam architecture.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import tempfile
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "step time & migrated GB/s per GPU vs PCIe roofline; GPU cache hit rate"
+ADAM_BYTES_PER_ELEM = 28  # read p32,m,v (12) + g bf16 (2); write p32,m,v (12) + p bf16 (2)
+
+
+def peaks():
+    try:
+        return json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
+    except Exception:
+        return {"hbm_gbs": 6650.0, "_fallback": True}
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons during the timed region."""
+
+    def __init__(self, gpu=0):
+        self.gpu = gpu
+        self.rows = []
+        self.proc = None
+
+    def __enter__(self):
+        q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+             "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+             "clocks_event_reasons.sw_power_cap")
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={q}",
+                                          "--format=csv,noheader,nounits", "-lms", "200"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.rows.append([x.strip() for x in line.split(",")])
+
+    def __exit__(self, *a):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        if not self.rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        sm = sorted(float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit())
+        mx = max((float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()), default=None)
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in self.rows for i in range(4) if len(r) > 4 + i and r[4 + i] == "Active"})
+        return {"sm_mhz": sm[len(sm) // 2] if sm else None, "sm_max_mhz": mx, "reasons": reasons,
+                "samples": len(self.rows)}
+
+
+def build_c2(workdir, tokens, tflops, iters=1):
+    from paper_2511_14124_b200 import traces as T
+    info = T.config_c2(workdir, iterations=iters, tokens=tokens, effective_tflops=tflops)
+    return info
+
+
+def decision_bytes_per_iter(trace, machine, cfg):
+    """Cache-decision bytes of one iteration from the product's model clock
+    (bit-identical to the reference's transfer_bytes)."""
+    from paper_2511_14124_b200 import policy as P
+    rep = P.run(trace, machine, cfg)
+    tb = rep["transfer_bytes"]
+    h2d = tb.get("cpu->gpu", 0)
+    d2h = tb.get("gpu->cpu", 0)
+    total = sum(tb.values())
+    return total, h2d, d2h, rep
+
+
+# ----------------------------------------------------------------- ours
+def run_ours(args):
+    import torch
+    from paper_2511_14124_b200.engine import Engine
+
+    torch.cuda.set_device(0)
+    wd = tempfile.mkdtemp(dir="/dev/shm" if os.path.isdir("/dev/shm") else None)
+    info = build_c2(wd, args.tokens, args.tflops)
+    cfg = {"policy": "tencache"}
+    dec_bytes, dec_h2d, dec_d2h, rep = decision_bytes_per_iter(info["trace"], info["machine"], cfg)
+    t0 = time.perf_counter()
+    eng = Engine(info["trace"], info["machine"], cfg, nvme_dir=wd)
+    eng.seed(0)
+    setup_s = time.perf_counter() - t0
+    stream = torch.cuda.current_stream()
+    mode = 1 if args.compute == "spin" else 0
+    step_kw = dict(lr=1e-4, compute_mode=mode, spin_ctas=1, stream=stream.cuda_stream)
+    for _ in range(args.warmup):
+        eng.iteration(**step_kw)
+    eng.reset_stats()
+    torch.cuda.synchronize()
+    s_ev, e_ev = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler() as clk:
+        s_ev.record(stream)
+        for _ in range(args.steps):
+            eng.iteration(**step_kw)
+        e_ev.record(stream)
+        torch.cuda.synchronize()
+    ms = s_ev.elapsed_time(e_ev) / args.steps
+    st = eng.stats(reset=True)
+    K = args.steps
+
+    # e2e through the public API with host buffers: per step the input batch
+    # (token ids, pinned host) goes H2D and the step's result (per-access
+    # checksums) comes back D2H; wall clock on the host.
+    B, S = 8, args.tokens // 8
+    tokens_h = torch.randint(0, 50272, (B, S), dtype=torch.int32).pin_memory()
+    tokens_d = torch.empty_like(tokens_h, device="cuda")
+    e2e_steps = max(2, K // 2)
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    for _ in range(e2e_steps):
+        tokens_d.copy_(tokens_h, non_blocking=True)
+        eng.iteration(**step_kw)
+        cks = eng.access_checksums()
+    torch.cuda.synchronize()
+    e2e_ms = (time.perf_counter() - t0) * 1e3 / e2e_steps
+    eng.reset_stats()
+
+    pk = peaks()
+    hbm = pk.get("hbm_gbs", 6650.0)
+    launches_per_iter = info["params"]
+    elems_per_launch = st["adam_elems"] / max(1, K * launches_per_iter)
+    avg_launch_ms = st["adam_ms"] / max(1, K * launches_per_iter)
+    achieved = ADAM_BYTES_PER_ELEM * elems_per_launch / (avg_launch_ms * 1e-3) / 1e9 if avg_launch_ms else 0.0
+    traffic = None
+    tf = os.path.join(ROOT, "profiles", "adamw_dram_bytes.json")
+    if os.path.exists(tf):
+        try:
+            traffic = json.load(open(tf)).get("dram_bytes_per_launch")
+        except Exception:
+            traffic = None
+    pcie_peak = {"h2d": args.pcie_h2d, "d2h": args.pcie_d2h}
+    h2d_all = (st["h2d_bytes"] + st["opt_h2d_bytes"]) / K
+    d2h_all = (st["d2h_bytes"] + st["opt_d2h_bytes"] + st["writeback_bytes"]) / K
+    h2d_gbs_busy = h2d_all * K / (st["h2d_busy_ms"] * 1e-3) / 1e9 if st["h2d_busy_ms"] else 0
+    d2h_gbs_busy = d2h_all * K / (st["d2h_busy_ms"] * 1e-3) / 1e9 if st["d2h_busy_ms"] else 0
+    copy_busy = st["h2d_busy_ms"] + st["d2h_busy_ms"]
+    hidden = 1.0 - st["stall_ms"] / copy_busy if copy_busy else None
+    prefetched = st["param_accesses"] - st["param_hits"]
+    value = dec_bytes / (ms * 1e-3) / 1e9
+
+    line = {
+        "metric": METRIC, "value": round(value, 4), "unit": "GB/s", "n_gpus": 1, "steps": K, "warmup": args.warmup,
+        "ms_per_step": round(ms, 3), "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+        "dtype": "bf16/fp32", "data": "synthetic (seeded N(0,0.02) params, N(0,1e-3) grads; chunk trace)",
+        "config": {"workload": "C2: OPT-1.3B offloaded training step, 1xB200, GPU->pinned-CPU tier, "
+                               "size-class buffer reuse (BASELINE.json configs[1])",
+                   "model": "opt-1.3b", "chunks": info["params"], "chunk_bytes": info["chunk_bytes"],
+                   "gpu_param_chunks": info["gpu_chunks"], "policy": "tencache",
+                   "tokens_per_step": args.tokens, "compute": args.compute,
+                   "compute_model_tflops": args.tflops, "l2": "inputs larger than L2 (>15 GB streamed per step)",
+                   "parallelism": "single GPU"},
+        "hit_rate": {"exact": rep["hit_rate"], "hits": st["param_hits"] // K, "accesses": st["param_accesses"] // K,
+                     "model_clock_hits": rep["param_hits"]},
+        "ontime_rate": round(st["ontime_accesses"] / prefetched, 4) if prefetched else 1.0,
+        "migrated_bytes_per_step": {"decisions": dec_bytes, "decisions_h2d": dec_h2d, "decisions_d2h": dec_d2h,
+                                    "optimizer_h2d": st["opt_h2d_bytes"] // K, "optimizer_d2h": st["opt_d2h_bytes"] // K,
+                                    "param_writeback": st["writeback_bytes"] // K,
+                                    "nvme_read": st["nvme_read_bytes"] // K, "nvme_write": st["nvme_write_bytes"] // K},
+        "pcie": {"h2d_GBps_step": round(h2d_all / (ms * 1e-3) / 1e9, 2),
+                 "d2h_GBps_step": round(d2h_all / (ms * 1e-3) / 1e9, 2),
+                 "h2d_GBps_busy": round(h2d_gbs_busy, 2), "d2h_GBps_busy": round(d2h_gbs_busy, 2),
+                 "h2d_frac": round(h2d_all / (ms * 1e-3) / 1e9 / pcie_peak["h2d"], 4),
+                 "d2h_frac": round(d2h_all / (ms * 1e-3) / 1e9 / pcie_peak["d2h"], 4),
+                 "peak_GBps": pcie_peak, "peak_source": "measured on this pool (256 MiB pinned cudaMemcpyAsync)"},
+        "migration_hidden_frac": round(hidden, 4) if hidden is not None else None,
+        "stall_ms_per_step": round(st["stall_ms"] / K, 3),
+        "roofline": {"kernel": "fused AdamW (adamw_kernel<2>)", "bound": "hbm", "achieved": round(achieved, 1),
+                     "peak": hbm, "unit": "GB/s", "frac": round(achieved / hbm, 4), "traffic": traffic,
+                     "algorithmic_bytes_per_launch": int(ADAM_BYTES_PER_ELEM * elems_per_launch),
+                     "avg_launch_us": round(avg_launch_ms * 1e3, 2),
+                     "peak_source": "MEASURED_PEAKS.json hbm_gbs (burst copy)"},
+        "e2e": {"value": round(dec_bytes / (e2e_ms * 1e-3) / 1e9, 4), "unit": "GB/s", "ms_per_step": round(e2e_ms, 3),
+                "h2d_bytes_per_step": int(tokens_h.numel() * 4), "d2h_bytes_per_step": int(len(cks) * 8),
+                "path": "Engine.iteration (ctypes C-ABI tc_engine_iteration), host wall clock"},
+        "gpu_launches": int(st["kernel_launches"]),
+        "setup_s": round(setup_s, 2),
+    }
+    del eng
+    if not args.no_cpu_baseline:
+        line["cpu_baseline"] = cpu_baseline(info, cfg, dec_bytes)
+    line["clocks"] = clk.summary()
+    return line
+
+
+# ---------------------------------------------------- reference CPU path
+class HostTiers:
+    """Tier buffers for the CPU reference arm: per (tier, size) slot arrays
+    with FIFO free lists; tensors move by memcpy (all host threads)."""
+
+    def __init__(self, np, ref, trace_tensors, initial, counts):
+        self.np, self.ref = np, ref
+        self.slots = {}
+        self.free = {}
+        for (tier, size), n in counts.items():
+            self.slots[(tier, size)] = [np.empty(size, np.uint8) for _ in range(n)]
+            self.free[(tier, size)] = list(range(n))
+        self.loc = {}
+        self.size = {t: s for t, s in trace_tensors.items()}
+        for tid, tier in initial.items():
+            self.loc[tid] = (tier, self.take(tier, self.size[tid]))
+
+    def take(self, tier, size):
+        return self.free[(tier, size)].pop(0)
+
+    def buf(self, tid):
+        tier, s = self.loc[tid]
+        return self.slots[(tier, self.size[tid])][s]
+
+    def move(self, tid, dst, copy=True):
+        tier, s = self.loc[tid]
+        size = self.size[tid]
+        ns = self.take(dst, size)
+        if copy:
+            self.ref.memcpy(self.slots[(dst, size)][ns], self.slots[(tier, size)][s], size)
+        self.free[(tier, size)].append(s)
+        self.loc[tid] = (dst, ns)
+
+
+def run_reference_arm(args):
+    import numpy as np
+    from oracle import ref
+
+    wd = tempfile.mkdtemp(dir="/dev/shm" if os.path.isdir("/dev/shm") else None)
+    info = build_c2(wd, args.tokens, args.tflops)
+    cfg = {"policy": "tencache"}
+    S, n = info["chunk_bytes"], info["params"]
+    rp = ref.Replay(info["trace"], info["machine"], cfg)
+    dec = ref.decisions(info["trace"], info["machine"], cfg, with_pools=False)
+    place = dec["init"]["placement"]
+    initial = {int(k): v for k, v in place["params"].items()}
+    initial.update({int(k): v for k, v in place["opt"].items()})
+    sizes = {i: S for i in range(1, n + 1)}
+    sizes.update({n + i: 6 * S for i in range(1, n + 1)})
+    g = info["gpu_chunks"]
+    counts = {(0, S): g + 1, (1, S): n - g + 2, (2, S): 8, (1, 6 * S): n + 2, (2, 6 * S): 2}
+    tiers = HostTiers(np, ref, sizes, initial, counts)
+    rng = np.random.default_rng(0)
+    blk = (rng.standard_normal(S // 2) * 0.02).astype(np.float32)
+    for i in range(1, n + 1):
+        tiers.buf(i)[:] = 0
+        st = tiers.buf(n + i).view(np.float32)
+        st[: S // 2] = blk
+        st[S // 2:] = 0
+    grads = (rng.standard_normal(S // 2) * 1e-3).astype(np.float32).view(np.uint32) >> 16
+    grads = grads.astype(np.uint16)
+    steps = []
+    import json as _j
+    for line in open(info["trace"]):
+        r = _j.loads(line)
+        if "s" in r:
+            steps.append(r["s"])
+    first_opt = next(i for i, s in enumerate(steps) if s["phase"] == "o")
+    threads = ref.threads()
+
+    def one_iteration(t):
+        restored = False
+        cks = 0
+        for i, s in enumerate(steps):
+            if i == first_opt and not restored:
+                restored = True
+                apply(rp.call("R"))
+            apply(rp.call("B", i))
+            if s["phase"] != "o":
+                for tid in s["ids"]:
+                    cks ^= ref.checksum(tiers.buf(tid))
+                time.sleep(s["us"] * 1e-6)  # the layer compute the GPU would do
+            else:
+                sid, pid = s["ids"]
+                st = tiers.buf(sid).view(np.float32)
+                k = S // 2
+                ref.adamw(st[:k], st[k:2 * k], st[2 * k:], grads, 1e-4, 0.9, 0.999, 1e-8, 0.01, t,
+                          want_bf16=False)
+                ref.num().tcnum_cast_f32_to_bf16(ref._p(st[:k]), ref._p(tiers.buf(pid)), k)
+            apply(rp.call("E", i))
+        if not restored:
+            apply(rp.call("R"))
+        apply(rp.call("I"))
+        rp.call("Z")
+        return cks
+
+    def apply(reqs):
+        for r in reqs:
+            tid, src, dst, size, kind, flags = (int(x) for x in r)
+            tiers.move(tid, dst, copy=not (flags & 2))  # instant = bookkeeping only
+
+    for t in range(1, args.warmup + 1):
+        one_iteration(t)
+    t0 = time.perf_counter()
+    for t in range(args.warmup + 1, args.warmup + args.steps + 1):
+        one_iteration(t)
+    ms = (time.perf_counter() - t0) * 1e3 / args.steps
+    dec_bytes, _, _, rep = decision_bytes_per_iter(info["trace"], info["machine"], cfg)
+    v = dec_bytes / (ms * 1e-3) / 1e9
+    return {"metric": METRIC, "value": round(v, 4), "unit": "GB/s", "n_gpus": 1, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": round(ms, 3), "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "fp32", "impl": "reference",
+            "data": "synthetic", "config": {"workload": "C2: OPT-1.3B offloaded training step (CPU reference path)",
+                                           "model": "opt-1.3b", "chunks": n, "chunk_bytes": S, "policy": "tencache"},
+            "hit_rate": {"exact": rep["hit_rate"]},
+            "cpu_baseline": {"value": round(v, 4), "unit": "GB/s", "cores": threads, "kind": "reference",
+                             "sample": f"{args.steps} full C2 iterations: reference IPolicy decisions "
+                                       "(oracle/_ref), host memcpy migrations, CPU checksums, trace compute "
+                                       "time, OpenMP AdamW (oracle/numerics.c)"},
+            "e2e": {"value": round(v, 4), "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+
+
+def cpu_baseline(info, cfg, dec_bytes):
+    """Bounded sample of the reference CPU path on this host: one iteration of
+    reference decisions (oracle/_ref IPolicy) + AdamW on 4 state chunks (port,
+    all threads) + memcpy of the decision bytes, scaled to a full step."""
+    import numpy as np
+    from oracle import ref
+    S, n = info["chunk_bytes"], info["params"]
+    ns_iter, _ = ref.time_decisions(info["trace"], info["machine"], cfg, iterations=2)
+    k = S // 2
+    st = np.zeros(3 * k, np.float32)
+    g = np.zeros(k, np.uint16)
+    reps = 4
+    t0 = time.perf_counter()
+    for t in range(1, reps + 1):
+        ref.adamw(st[:k], st[k:2 * k], st[2 * k:], g, 1e-4, 0.9, 0.999, 1e-8, 0.01, t)
+    adam_s = (time.perf_counter() - t0) / reps
+    a = np.empty(S, np.uint8)
+    b = np.empty(S, np.uint8)
+    t0 = time.perf_counter()
+    for _ in range(4):
+        ref.memcpy(b, a, S)
+    cp_s = (time.perf_counter() - t0) / 4
+    compute_s = 0.0
+    for line in open(info["trace"]):
+        r = json.loads(line)
+        if "s" in r and r["s"]["phase"] != "o":
+            compute_s += r["s"]["us"] * 1e-6
+    step_s = ns_iter * 1e-9 + adam_s * n + cp_s * dec_bytes / S + compute_s
+    return {"value": round(dec_bytes / step_s / 1e9, 4), "unit": "GB/s", "cores": ref.threads(),
+            "kind": "reference", "ms_per_step": round(step_s * 1e3, 2),
+            "sample": f"reference IPolicy decisions for 2 C2 iterations ({ns_iter / 1e6:.2f} ms/iter) + "
+                      f"AdamW on {reps} state chunks ({adam_s * 1e3:.1f} ms each) + 4 x {S} B memcpy, "
+                      f"scaled to {n} chunks, plus the trace compute time"}
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--compute", default="spin", choices=["spin", "none"])
+    ap.add_argument("--tokens", type=int, default=16384)
+    ap.add_argument("--tflops", type=float, default=700.0)
+    ap.add_argument("--pcie-h2d", type=float, default=55.3)
+    ap.add_argument("--pcie-d2h", type=float, default=57.0)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    if args.impl == "reference":
+        if rank != 0:
+            return
+        print(json.dumps(run_reference_arm(args)))
+        return
+    if world > 1:
+        from paper_2511_14124_b200 import zero3
+        line = zero3.bench_rank(args)
+        if rank == 0 and line:
+            print(json.dumps(line))
+        return
+    print(json.dumps(run_ours(args)))
+
+
+if __name__ == "__main__":
+    main()

@@ -101,19 +101,25 @@ int tc_time_run(const char* trace_path, const char* machine_path, const char* cf
 /* All pointers are device pointers unless stated; `stream` is a cudaStream_t
  * (NULL = legacy default). Kernels are asynchronous. */
 
-/* A fragment: `bytes` at src_base+src_off -> dst_base+dst_off. */
+/* A fragment: `bytes` at src_base+src_off <-> dst_base+dst_off. */
 typedef struct {
   uint64_t src_off;
   uint64_t dst_off;
   uint64_t bytes;
 } tc_segment;
 
-/* pack / unpack of fragmented tensors into one pooled chunk:
- * one launch for the whole fragment list; `segs` is a DEVICE array. pack and
- * unpack are the same gather/scatter with roles swapped; both entry points
- * exist so call sites read like the reference's vocabulary. */
-int tc_pack(const void* src_base, void* chunk, const tc_segment* segs, uint32_t n, void* stream);
-int tc_unpack(const void* chunk, void* dst_base, const tc_segment* segs, uint32_t n, void* stream);
+/* pack / unpack of fragmented tensors into one pooled chunk.
+ * A plan uploads the fragment list (host array) once to HBM with each
+ * fragment's position in the concatenated stream; pack then moves every
+ * fragment src_base+src_off -> dst_base+dst_off in ONE launch, and unpack is
+ * the inverse (src_base+dst_off -> dst_base+src_off). Fragments must not
+ * overlap at the destination. */
+typedef struct tc_pack_plan tc_pack_plan;
+int tc_pack_plan_create(const tc_segment* host_segs, uint32_t n, tc_pack_plan** out);
+void tc_pack_plan_destroy(tc_pack_plan* plan);
+uint64_t tc_pack_plan_bytes(const tc_pack_plan* plan);
+int tc_pack(const tc_pack_plan* plan, const void* src_base, void* dst_base, void* stream);
+int tc_unpack(const tc_pack_plan* plan, const void* src_base, void* dst_base, void* stream);
 
 /* bf16 <-> fp32 casts (RNE, NaN -> quiet NaN; torch .to() semantics). */
 int tc_cast_bf16_to_f32(const void* in, float* out, uint64_t n, void* stream);
@@ -172,6 +178,8 @@ int tc_engine_seed(tc_engine* e, uint64_t seed);
  * end-to-end API): read into / write from a HOST buffer of its size. */
 int tc_engine_read_tensor(tc_engine* e, uint32_t tensor, void* host_dst, uint64_t bytes);
 int tc_engine_write_tensor(tc_engine* e, uint32_t tensor, const void* host_src, uint64_t bytes);
+/* Host copy of a parameter's bf16 gradient (HBM). */
+int tc_engine_read_grad(tc_engine* e, uint32_t tensor, void* host_dst, uint64_t bytes);
 /* Device pointer of the tensor's current GPU slot (NULL if not GPU-resident). */
 void* tc_engine_gpu_ptr(tc_engine* e, uint32_t tensor);
 /* Gradient buffer (bf16, on GPU) of a parameter tensor. */

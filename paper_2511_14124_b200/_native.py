@@ -103,8 +103,11 @@ _SIGS = {
                            C.POINTER(C.c_double)], C.c_int),
     "tc_time_run": ([C.c_char_p, C.c_char_p, C.c_char_p, C.c_int, C.POINTER(C.c_double)], C.c_int),
     # data plane
-    "tc_pack": ([C.c_void_p, C.c_void_p, C.c_void_p, C.c_uint32, C.c_void_p], C.c_int),
-    "tc_unpack": ([C.c_void_p, C.c_void_p, C.c_void_p, C.c_uint32, C.c_void_p], C.c_int),
+    "tc_pack_plan_create": ([C.c_void_p, C.c_uint32, C.POINTER(C.c_void_p)], C.c_int),
+    "tc_pack_plan_destroy": ([C.c_void_p], None),
+    "tc_pack_plan_bytes": ([C.c_void_p], C.c_uint64),
+    "tc_pack": ([C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p], C.c_int),
+    "tc_unpack": ([C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p], C.c_int),
     "tc_cast_bf16_to_f32": ([C.c_void_p, C.c_void_p, C.c_uint64, C.c_void_p], C.c_int),
     "tc_cast_f32_to_bf16": ([C.c_void_p, C.c_void_p, C.c_uint64, C.c_void_p], C.c_int),
     "tc_adamw": ([C.c_void_p, C.c_void_p, C.c_void_p, C.c_uint64, C.c_double, C.c_double, C.c_double, C.c_double,
@@ -121,6 +124,7 @@ _SIGS = {
     "tc_engine_seed": ([C.c_void_p, C.c_uint64], C.c_int),
     "tc_engine_read_tensor": ([C.c_void_p, C.c_uint32, C.c_void_p, C.c_uint64], C.c_int),
     "tc_engine_write_tensor": ([C.c_void_p, C.c_uint32, C.c_void_p, C.c_uint64], C.c_int),
+    "tc_engine_read_grad": ([C.c_void_p, C.c_uint32, C.c_void_p, C.c_uint64], C.c_int),
     "tc_engine_gpu_ptr": ([C.c_void_p, C.c_uint32], C.c_void_p),
     "tc_engine_grad_ptr": ([C.c_void_p, C.c_uint32], C.c_void_p),
     "tc_engine_iteration": ([C.c_void_p, C.POINTER(tc_step_options), C.c_void_p], C.c_int),

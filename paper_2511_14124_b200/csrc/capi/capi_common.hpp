@@ -11,6 +11,8 @@
 namespace tcb {
 
 int set_error(int code, const std::string& msg);
+tencache::RunConfig parse_run_config(const char* cfg_json);
+tencache::MachineConfig machine_from(const char* path);
 
 // Runtime failures of the data plane (CUDA / NCCL / file I/O).
 struct DeviceError : std::runtime_error {

@@ -1,0 +1,897 @@
+// Per-GPU migration executor (see executor.hpp for the physical layout).
+#include "executor.hpp"
+
+#include <fcntl.h>
+#include <unistd.h>
+
+#include <algorithm>
+#include <cstdlib>
+#include <cstring>
+
+namespace tcb {
+
+using namespace tencache;
+
+void cuda_check(cudaError_t e, const char* what) {
+  if (e != cudaSuccess) throw DeviceError(TC_ECUDA, std::string(what) + ": " + cudaGetErrorString(e));
+}
+
+// ------------------------------------------------------------ EventArena
+EventArena::~EventArena() {
+  for (auto* v : {&free_, &free_timed_, &used_, &used_timed_})
+    for (cudaEvent_t e : *v) cudaEventDestroy(e);
+}
+
+cudaEvent_t EventArena::get(bool timing) {
+  auto& fr = timing ? free_timed_ : free_;
+  auto& us = timing ? used_timed_ : used_;
+  cudaEvent_t e;
+  if (fr.empty()) {
+    TCB_CK(cudaEventCreateWithFlags(&e, timing ? cudaEventDefault : cudaEventDisableTiming));
+  } else {
+    e = fr.back();
+    fr.pop_back();
+  }
+  us.push_back(e);
+  return e;
+}
+
+void EventArena::recycle() {
+  free_.insert(free_.end(), used_.begin(), used_.end());
+  free_timed_.insert(free_timed_.end(), used_timed_.begin(), used_timed_.end());
+  used_.clear();
+  used_timed_.clear();
+}
+
+// -------------------------------------------------------------- SlotPool
+void SlotPool::allocate(bool device, int dev) {
+  device_ = device;
+  bytes_ = 0;
+  for (const auto& [size, n] : want_) bytes_ += size * n;
+  if (bytes_ == 0) return;
+  if (device)
+    TCB_CK(cudaMalloc(&base_, bytes_));
+  else
+    TCB_CK(cudaHostAlloc(reinterpret_cast<void**>(&base_), bytes_, cudaHostAllocPortable));
+  std::uint64_t off = 0;
+  for (const auto& [size, n] : want_) {  // carved like BufferPool::build: ascending class, then index
+    SlotClass& c = classes_[size];
+    c.size = size;
+    c.slots.resize(n);
+    for (std::uint32_t i = 0; i < n; ++i) {
+      c.slots[i].ptr = base_ + off;
+      off += size;
+      c.free_fifo.push_back(i);
+    }
+  }
+}
+
+void SlotPool::release_memory() {
+  if (base_ == nullptr) return;
+  if (device_)
+    cudaFree(base_);
+  else
+    cudaFreeHost(base_);
+  base_ = nullptr;
+}
+
+SlotClass& SlotPool::cls(std::uint64_t size) {
+  auto it = classes_.find(size);
+  if (it == classes_.end()) throw DeviceError(TC_EINTERNAL, "no physical slot class of " + std::to_string(size) + " bytes");
+  return it->second;
+}
+
+bool SlotPool::has_free(std::uint64_t size) const {
+  auto it = classes_.find(size);
+  return it != classes_.end() && !it->second.free_fifo.empty();
+}
+
+// -------------------------------------------------------------- Executor
+namespace {
+
+constexpr std::uint64_t kAlign = 4096;
+std::uint64_t round_up(std::uint64_t x, std::uint64_t a) { return (x + a - 1) / a * a; }
+
+}  // namespace
+
+
+Executor::Executor(const std::string& trace_path, const std::string& machine_path, const std::string& cfg_json,
+                   const tc_engine_options& opts)
+    : opts_(opts) {
+  device_ = opts.device;
+  TCB_CK(cudaSetDevice(device_));
+  trace_ = load_trace(trace_path);
+  machine_ = machine_from(machine_path.c_str());
+  cfg_ = parse_run_config(cfg_json.c_str());
+  if (cfg_.policy != PolicyKind::TenCache && cfg_.policy != PolicyKind::TenCachePlusOpt)
+    throw ConfigError("the CUDA executor runs the TenCache policies (tencache, tencache+opt)");
+  policy_ = make_policy(trace_, machine_, cfg_);
+  policy_->init();
+  const SchedulerState& st = *policy_->scheduler_state();
+
+  // tensor table
+  recs_.reserve(trace_.tensors.size());
+  for (const auto& t : trace_.tensors) {
+    index_[t.id] = static_cast<std::int32_t>(recs_.size());
+    TensorRec r;
+    r.id = t.id;
+    r.bytes = t.size_bytes;
+    r.is_state = t.kind == TensorKind::OptStateFP32;
+    recs_.push_back(r);
+  }
+  for (const auto& [sid, pid] : trace_.optimizer_pairs()) {
+    if (pid == 0) continue;
+    TensorRec& s = rec(sid);
+    TensorRec& p = rec(pid);
+    if (s.bytes != 6 * p.bytes || p.bytes % 16 != 0)
+      throw ConfigError("optimizer state " + std::to_string(sid) + " must be 6x its bf16 parameter (16-byte multiple)");
+    s.partner = index_.at(pid);
+    p.partner = index_.at(sid);
+  }
+
+  // physical pools: logical counts from the policy's pools + spares
+  const int gspare = std::max(opts.gpu_spare_slots, 1), hspare = std::max(opts.host_spare_slots, 1);
+  std::map<std::uint64_t, std::uint32_t> gcount, hcount, ocount;
+  for (const Chunk& c : st.gpu_pool.chunks()) ++gcount[c.size];
+  for (const Chunk& c : st.cpu_pool.chunks()) ++hcount[c.size];
+  for (const Chunk& c : st.cpu_opt_pool.chunks()) ++ocount[c.size];
+  std::map<std::uint64_t, bool> pclass, sclass;
+  for (const auto& r : recs_) (r.is_state ? sclass : pclass)[r.bytes] = true;
+  for (const auto& [size, _] : pclass) {
+    gpu_.plan(size, gcount[size] + gspare);
+    host_param_.plan(size, hcount[size] + hspare);
+  }
+  for (const auto& [size, _] : sclass) host_opt_.plan(size, ocount[size] + hspare + 1);  // +1 transient
+  gpu_.allocate(true, device_);
+  host_param_.allocate(false, device_);
+  host_opt_.allocate(false, device_);
+
+  // NVMe tier: one sparse file, a 4 KiB-aligned extent per tensor
+  std::uint64_t off = 0;
+  bool all_aligned = true;
+  for (auto& r : recs_) {
+    r.nvme_off = off;
+    off += round_up(r.bytes, kAlign);
+    all_aligned = all_aligned && r.bytes % kAlign == 0;
+  }
+  std::string dir = opts.nvme_dir && *opts.nvme_dir ? opts.nvme_dir : "";
+  if (dir.empty()) dir = std::getenv("TMPDIR") ? std::getenv("TMPDIR") : "/tmp";
+  nvme_path_ = dir + "/tencache_nvme_XXXXXX";
+  std::vector<char> tmpl(nvme_path_.begin(), nvme_path_.end());
+  tmpl.push_back(0);
+  nvme_fd_ = mkstemp(tmpl.data());
+  if (nvme_fd_ < 0) throw DeviceError(TC_EIO, "cannot create NVMe tier file in " + dir);
+  nvme_path_ = tmpl.data();
+  unlink(nvme_path_.c_str());
+  if (opts.direct_io && all_aligned) {
+    int fl = fcntl(nvme_fd_, F_GETFL);
+    fcntl(nvme_fd_, F_SETFL, fl | O_DIRECT);
+  }
+  if (ftruncate(nvme_fd_, static_cast<off_t>(off)) != 0) throw DeviceError(TC_EIO, "ftruncate NVMe tier file");
+
+  for (const auto& [size, _] : pclass) {
+    void* p = nullptr;
+    TCB_CK(cudaHostAlloc(&p, size, cudaHostAllocPortable));
+    bounce_[size] = static_cast<std::uint8_t*>(p);
+    bounce_sync_[size] = SlotSync{};
+  }
+  std::uint64_t max_state = 0;
+  for (const auto& [size, _] : sclass) max_state = std::max(max_state, size);
+  for (const auto& [size, _] : pclass) max_state = std::max(max_state, 6 * size);  // seed scratch
+  stage_bytes_ = max_state;
+  const int nstage = std::max(opts.opt_stage_slots, 2);
+  for (int i = 0; i < nstage; ++i) {
+    void* p = nullptr;
+    TCB_CK(cudaMalloc(&p, stage_bytes_));
+    stage_.push_back(static_cast<std::uint8_t*>(p));
+    stage_sync_.emplace_back();
+  }
+  for (const auto& [size, _] : pclass) {
+    for (int i = 0; i < 2; ++i) {
+      void* p = nullptr;
+      TCB_CK(cudaMalloc(&p, size));
+      pout_scratch_[size].push_back(static_cast<std::uint8_t*>(p));
+      pout_sync_[size].emplace_back();
+    }
+    pout_next_[size] = 0;
+  }
+  std::uint64_t gbytes = 0;
+  for (const auto& r : recs_)
+    if (!r.is_state) gbytes += r.bytes;
+  if (gbytes) TCB_CK(cudaMalloc(&grads_, gbytes));
+  gbytes = 0;
+  for (auto& r : recs_)
+    if (!r.is_state) {
+      r.grad = grads_ + gbytes;
+      gbytes += r.bytes;
+    }
+  for (const auto& s : trace_.steps)
+    if (s.phase != Phase::OptimizerUpdate) n_accesses_ += s.tensor_ids.size();
+  TCB_CK(cudaMalloc(&d_checksums_, std::max<std::size_t>(n_accesses_, 1) * sizeof(std::uint64_t)));
+  h_checksums_.assign(n_accesses_, 0);
+  TCB_CK(cudaStreamCreateWithFlags(&h2d_, cudaStreamNonBlocking));
+  TCB_CK(cudaStreamCreateWithFlags(&d2h_, cudaStreamNonBlocking));
+
+  // initial physical placement = the policy's placement
+  for (auto& r : recs_) {
+    const Tier t = st.final_loc(r.id);
+    if (t == Tier::Gpu) {
+      r.tier = PTier::Gpu;
+      r.slot = take_slot(PTier::Gpu, r.bytes, index_of(r.id));
+    } else if (t == Tier::Cpu) {
+      r.tier = host_tier(r);
+      r.slot = take_slot(r.tier, r.bytes, index_of(r.id));
+    } else {
+      r.tier = PTier::Nvme;
+    }
+    r.nvme_valid = t == Tier::Nvme;
+  }
+}
+
+Executor::~Executor() {
+  cudaSetDevice(device_);
+  if (h2d_) cudaStreamSynchronize(h2d_);
+  if (d2h_) cudaStreamSynchronize(d2h_);
+  cudaDeviceSynchronize();
+  gpu_.release_memory();
+  host_param_.release_memory();
+  host_opt_.release_memory();
+  for (auto& [s, p] : bounce_) cudaFreeHost(p);
+  for (auto* p : stage_) cudaFree(p);
+  for (auto& [s, v] : pout_scratch_)
+    for (auto* p : v) cudaFree(p);
+  if (grads_) cudaFree(grads_);
+  if (d_checksums_) cudaFree(d_checksums_);
+  if (h2d_) cudaStreamDestroy(h2d_);
+  if (d2h_) cudaStreamDestroy(d2h_);
+  if (compute_owned_) cudaStreamDestroy(compute_owned_);
+  if (nvme_fd_ >= 0) close(nvme_fd_);
+}
+
+std::int32_t Executor::index_of(TensorId id) const {
+  auto it = index_.find(id);
+  if (it == index_.end()) throw TraceError("unknown tensor id " + std::to_string(id));
+  return it->second;
+}
+
+TensorRec& Executor::rec(TensorId id) { return recs_[static_cast<std::size_t>(index_of(id))]; }
+
+SlotPool& Executor::pool(PTier t) {
+  switch (t) {
+    case PTier::Gpu: return gpu_;
+    case PTier::HostParam: return host_param_;
+    case PTier::HostOpt: return host_opt_;
+    default: throw DeviceError(TC_EINTERNAL, "NVMe has no slot pool");
+  }
+}
+
+Slot& Executor::slot_of(const TensorRec& r) { return pool(r.tier).cls(r.bytes).slots.at(r.slot); }
+std::uint8_t* Executor::where(const TensorRec& r) { return slot_of(r).ptr; }
+
+std::uint32_t Executor::take_slot(PTier t, std::uint64_t size, std::int32_t occupant) {
+  SlotClass& c = pool(t).cls(size);
+  if (c.free_fifo.empty()) throw DeviceError(TC_EINTERNAL, "physical slot pool exhausted (class " + std::to_string(size) + ")");
+  const std::uint32_t s = c.free_fifo.front();
+  c.free_fifo.pop_front();
+  c.slots[s].occupant = occupant;
+  return s;
+}
+
+void Executor::free_slot(PTier t, std::uint64_t size, std::uint32_t s) {
+  SlotClass& c = pool(t).cls(size);
+  c.slots[s].occupant = -1;
+  c.free_fifo.push_back(s);
+}
+
+void Executor::wait_for_read(cudaStream_t s, const SlotSync& y) {
+  if (y.writer) TCB_CK(cudaStreamWaitEvent(s, y.writer, 0));
+}
+
+void Executor::wait_for_write(cudaStream_t s, const SlotSync& y) {
+  if (y.writer) TCB_CK(cudaStreamWaitEvent(s, y.writer, 0));
+  for (cudaEvent_t e : y.readers) TCB_CK(cudaStreamWaitEvent(s, e, 0));
+}
+
+void Executor::host_wait_all(const SlotSync& y) {
+  if (y.writer) TCB_CK(cudaEventSynchronize(y.writer));
+  for (cudaEvent_t e : y.readers) TCB_CK(cudaEventSynchronize(e));
+}
+
+cudaEvent_t Executor::copy(cudaStream_t s, void* dst, const void* src, std::uint64_t n, bool h2d) {
+  Copy c;
+  c.start = events_.get(true);
+  c.end = events_.get(true);
+  c.h2d = h2d;
+  c.bytes = n;
+  TCB_CK(cudaEventRecord(c.start, s));
+  TCB_CK(cudaMemcpyAsync(dst, src, n, h2d ? cudaMemcpyHostToDevice : cudaMemcpyDeviceToHost, s));
+  TCB_CK(cudaEventRecord(c.end, s));
+  copies_.push_back(c);
+  ++stats_.copies;
+  return c.end;
+}
+
+void Executor::nvme_read(const TensorRec& r, void* dst) {
+  std::uint64_t done = 0;
+  auto* p = static_cast<std::uint8_t*>(dst);
+  while (done < r.bytes) {
+    const ssize_t k = pread(nvme_fd_, p + done, r.bytes - done, static_cast<off_t>(r.nvme_off + done));
+    if (k <= 0) throw DeviceError(TC_EIO, "NVMe tier read failed for tensor " + std::to_string(r.id));
+    done += static_cast<std::uint64_t>(k);
+  }
+  stats_.nvme_read_bytes += r.bytes;
+}
+
+void Executor::nvme_write(TensorRec& r, const void* src) {
+  std::uint64_t done = 0;
+  const auto* p = static_cast<const std::uint8_t*>(src);
+  while (done < r.bytes) {
+    const ssize_t k = pwrite(nvme_fd_, p + done, r.bytes - done, static_cast<off_t>(r.nvme_off + done));
+    if (k <= 0) throw DeviceError(TC_EIO, "NVMe tier write failed for tensor " + std::to_string(r.id));
+    done += static_cast<std::uint64_t>(k);
+  }
+  r.nvme_valid = true;
+  stats_.nvme_write_bytes += r.bytes;
+}
+
+// An "instant" move to NVMe claims a clean replica. After an optimizer update
+// the replica is stale, so the executor writes the current bytes first
+// (SURVEY.md §7 traffic category iii).
+void Executor::ensure_nvme_fresh(TensorRec& r) {
+  if (r.nvme_valid) return;
+  if (r.tier == PTier::Gpu) {
+    Slot& g = slot_of(r);
+    std::uint8_t* b = bounce_.at(r.bytes);
+    host_wait_all(bounce_sync_[r.bytes]);
+    wait_for_read(d2h_, g.sync);
+    cudaEvent_t e = copy(d2h_, b, g.ptr, r.bytes, false);
+    g.sync.readers.push_back(e);
+    TCB_CK(cudaEventSynchronize(e));
+    bounce_sync_[r.bytes] = SlotSync{};
+    nvme_write(r, b);
+  } else {
+    Slot& h = slot_of(r);
+    host_wait_all(h.sync);
+    nvme_write(r, h.ptr);
+  }
+  stats_.writeback_bytes += r.bytes;
+}
+
+bool Executor::dest_available(const Req& r) const {
+  if (r.instant || r.dst == Tier::Nvme) return true;
+  const TensorRec& x = recs_[static_cast<std::size_t>(index_of(r.tensor_id))];
+  if (r.dst == Tier::Gpu) return gpu_.has_free(x.bytes);
+  return (x.is_state ? host_opt_ : host_param_).has_free(x.bytes);
+}
+
+// Requests run in order, except that one whose destination class has no free
+// physical slot yet waits for a later departure from that class (never past
+// an earlier request for the same tensor).
+void Executor::execute(std::vector<Req> reqs) {
+  while (!reqs.empty()) {
+    std::size_t pick = reqs.size();
+    for (std::size_t i = 0; i < reqs.size() && pick == reqs.size(); ++i) {
+      bool blocked = false;
+      for (std::size_t j = 0; j < i && !blocked; ++j) blocked = reqs[j].tensor_id == reqs[i].tensor_id;
+      if (!blocked && dest_available(reqs[i])) pick = i;
+    }
+    if (pick == reqs.size()) throw DeviceError(TC_EINTERNAL, "no physical slot for any pending transfer");
+    apply(reqs[pick]);
+    reqs.erase(reqs.begin() + static_cast<std::ptrdiff_t>(pick));
+  }
+}
+
+void Executor::apply(const Req& r) {
+  TensorRec& x = rec(r.tensor_id);
+  ++stats_.requests;
+  if (!r.instant) ++x.issued_since_access;
+  const bool src_ok = (r.src == Tier::Gpu && x.tier == PTier::Gpu) ||
+                      (r.src == Tier::Cpu && (x.tier == PTier::HostParam || x.tier == PTier::HostOpt)) ||
+                      (r.src == Tier::Nvme && x.tier == PTier::Nvme);
+  if (!src_ok)
+    throw DeviceError(TC_EINTERNAL, "executor/policy desync: tensor " + std::to_string(x.id) + " not in " + to_string(r.src));
+  const std::int32_t xi = index_of(x.id);
+  cudaEvent_t done = nullptr;
+
+  if (r.src == Tier::Gpu && r.dst == Tier::Cpu) {  // evict / restore, D2H
+    Slot& g = slot_of(x);
+    const PTier ht = host_tier(x);
+    const std::uint32_t hs = take_slot(ht, x.bytes, xi);
+    Slot& h = pool(ht).cls(x.bytes).slots[hs];
+    wait_for_read(d2h_, g.sync);
+    wait_for_write(d2h_, h.sync);
+    done = copy(d2h_, h.ptr, g.ptr, x.bytes, false);
+    g.sync.readers.push_back(done);
+    h.sync.writer = done;
+    h.sync.readers.clear();
+    free_slot(PTier::Gpu, x.bytes, x.slot);
+    x.tier = ht;
+    x.slot = hs;
+    stats_.d2h_bytes += x.bytes;
+  } else if (r.src == Tier::Cpu && r.dst == Tier::Gpu) {  // prefetch / restore, H2D
+    if (r.src_retains) throw ConfigError("executor: host-retaining fetches (comparison policies) are not executed");
+    Slot& h = slot_of(x);
+    const std::uint32_t gs = take_slot(PTier::Gpu, x.bytes, xi);
+    Slot& g = gpu_.cls(x.bytes).slots[gs];
+    wait_for_read(h2d_, h.sync);
+    wait_for_write(h2d_, g.sync);
+    done = copy(h2d_, g.ptr, h.ptr, x.bytes, true);
+    h.sync.readers.push_back(done);
+    g.sync.writer = done;
+    g.sync.readers.clear();
+    free_slot(x.tier, x.bytes, x.slot);
+    x.tier = PTier::Gpu;
+    x.slot = gs;
+    x.arrival = done;
+    stats_.h2d_bytes += x.bytes;
+  } else if (r.src == Tier::Nvme && r.dst == Tier::Gpu) {  // staged: NVMe -> bounce -> HBM
+    const std::uint32_t gs = take_slot(PTier::Gpu, x.bytes, xi);
+    Slot& g = gpu_.cls(x.bytes).slots[gs];
+    std::uint8_t* b = bounce_.at(x.bytes);
+    host_wait_all(bounce_sync_[x.bytes]);
+    nvme_read(x, b);
+    wait_for_write(h2d_, g.sync);
+    done = copy(h2d_, g.ptr, b, x.bytes, true);
+    bounce_sync_[x.bytes] = SlotSync{nullptr, {done}};
+    g.sync.writer = done;
+    g.sync.readers.clear();
+    if (!r.src_retains) x.nvme_valid = false;
+    x.tier = PTier::Gpu;
+    x.slot = gs;
+    x.arrival = done;
+    stats_.h2d_bytes += x.bytes;
+  } else if (r.src == Tier::Nvme && r.dst == Tier::Cpu) {  // state (or param) read into host memory
+    const PTier ht = host_tier(x);
+    const std::uint32_t hs = take_slot(ht, x.bytes, xi);
+    Slot& h = pool(ht).cls(x.bytes).slots[hs];
+    host_wait_all(h.sync);
+    nvme_read(x, h.ptr);
+    h.sync = SlotSync{};
+    x.tier = ht;
+    x.slot = hs;
+  } else if (r.src == Tier::Cpu && r.dst == Tier::Nvme) {  // spill / state write-back
+    if (!r.instant || !x.nvme_valid) {
+      Slot& h = slot_of(x);
+      host_wait_all(h.sync);
+      nvme_write(x, h.ptr);
+    }
+    Slot& h = slot_of(x);
+    h.sync = SlotSync{};
+    free_slot(x.tier, x.bytes, x.slot);
+    x.tier = PTier::Nvme;
+  } else if (r.src == Tier::Gpu && r.dst == Tier::Nvme) {  // drop (replica authoritative) or write-back
+    ensure_nvme_fresh(x);
+    free_slot(PTier::Gpu, x.bytes, x.slot);
+    x.tier = PTier::Nvme;
+  } else {
+    throw DeviceError(TC_EINTERNAL, "unsupported transfer direction");
+  }
+  if (r.blocking && done) barriers_.push_back(done);
+}
+
+void Executor::wait_barriers(cudaStream_t cs) {
+  for (cudaEvent_t e : barriers_) TCB_CK(cudaStreamWaitEvent(cs, e, 0));
+  barriers_.clear();
+}
+
+void Executor::param_step(const TraceStep& step, std::size_t, cudaStream_t cs) {
+  cudaEvent_t reach = events_.get(true), go = events_.get(true);
+  TCB_CK(cudaEventRecord(reach, cs));
+  for (TensorId id : step.tensor_ids) {
+    TensorRec& x = rec(id);
+    if (x.tier != PTier::Gpu) throw DeviceError(TC_EINTERNAL, "step tensor " + std::to_string(id) + " not GPU-resident");
+    wait_for_read(cs, slot_of(x).sync);
+  }
+  wait_barriers(cs);
+  TCB_CK(cudaEventRecord(go, cs));
+  stalls_.emplace_back(reach, go);
+  for (TensorId id : step.tensor_ids) {
+    TensorRec& x = rec(id);
+    ++stats_.param_accesses;
+    if (x.issued_since_access == 0)
+      ++stats_.param_hits;
+    else if (x.arrival)
+      ontime_.emplace_back(reach, x.arrival);
+    x.issued_since_access = 0;
+    if (access_cursor_ < n_accesses_) {
+      TCB_CK(launch_checksum(where(x), x.bytes & ~3ull,
+                             reinterpret_cast<unsigned long long*>(d_checksums_ + access_cursor_), cs));
+      ++stats_.kernel_launches;
+      ++access_cursor_;
+    }
+  }
+  if (so_.compute_mode == 1) {
+    const double us = step.compute_us * cfg_.batch_scale;
+    TCB_CK(launch_spin(static_cast<std::uint64_t>(us * 1000.0), so_.spin_ctas, cs));
+    ++stats_.kernel_launches;
+  }
+  cudaEvent_t done = events_.get(false);
+  TCB_CK(cudaEventRecord(done, cs));
+  for (TensorId id : step.tensor_ids) slot_of(rec(id)).sync.readers.push_back(done);
+}
+
+void Executor::optimizer_step(const TraceStep& step, cudaStream_t cs) {
+  TensorRec& s = rec(step.tensor_ids.front());
+  if (!s.is_state || s.partner < 0) throw DeviceError(TC_EINTERNAL, "optimizer step without a paired state");
+  TensorRec& p = recs_[static_cast<std::size_t>(s.partner)];
+  if (s.tier != PTier::HostOpt) throw DeviceError(TC_EINTERNAL, "optimizer state not in host memory at its update");
+  const std::uint64_t n = p.bytes / 2;
+  Slot& h = slot_of(s);
+
+  // H2D: state chunk -> HBM stage (ring slot free once its last D2H is done)
+  const std::size_t b = stage_next_;
+  stage_next_ = (stage_next_ + 1) % stage_.size();
+  std::uint8_t* stg = stage_[b];
+  wait_for_write(h2d_, stage_sync_[b]);
+  wait_for_read(h2d_, h.sync);
+  cudaEvent_t e1 = copy(h2d_, stg, h.ptr, s.bytes, true);
+  h.sync.readers.push_back(e1);
+  stage_sync_[b] = SlotSync{e1, {}};
+  stats_.opt_h2d_bytes += s.bytes;
+
+  // fused AdamW on the compute stream; the bf16 result goes straight into the
+  // parameter's HBM slot when it is resident, else into a scratch buffer.
+  TCB_CK(cudaStreamWaitEvent(cs, e1, 0));
+  wait_barriers(cs);
+  std::uint8_t* pout;
+  SlotSync* psync;
+  const bool on_gpu = p.tier == PTier::Gpu;
+  if (on_gpu) {
+    Slot& g = slot_of(p);
+    pout = g.ptr;
+    psync = &g.sync;
+  } else {
+    std::size_t& k = pout_next_[p.bytes];
+    pout = pout_scratch_[p.bytes][k];
+    psync = &pout_sync_[p.bytes][k];
+    k = (k + 1) % pout_scratch_[p.bytes].size();
+  }
+  wait_for_write(cs, *psync);
+  cudaEvent_t a0 = events_.get(true), a1 = events_.get(true);
+  TCB_CK(cudaEventRecord(a0, cs));
+  auto* st = reinterpret_cast<float*>(stg);
+  const AdamScalars sc = adam_scalars(so_.lr, so_.beta1, so_.beta2, so_.eps, so_.weight_decay, adam_step_);
+  TCB_CK(launch_adamw(st, st + n, st + 2 * n, reinterpret_cast<const std::uint16_t*>(p.grad),
+                      reinterpret_cast<std::uint16_t*>(pout), n, sc, so_.grad_scale, cs));
+  TCB_CK(cudaEventRecord(a1, cs));
+  adam_.emplace_back(a0, a1);
+  ++stats_.kernel_launches;
+  stats_.adam_elems += n;
+  *psync = SlotSync{a1, {}};
+  stage_sync_[b].readers.push_back(a1);
+  p.nvme_valid = false;  // any NVMe replica of the parameter is now stale
+  if (on_gpu) p.arrival = nullptr;
+
+  // D2H: updated state back to its host slot
+  wait_for_read(d2h_, stage_sync_[b]);  // writer e1 (h2d) ...
+  TCB_CK(cudaStreamWaitEvent(d2h_, a1, 0));  // ... and the update
+  cudaEvent_t e3 = copy(d2h_, h.ptr, stg, s.bytes, false);
+  h.sync = SlotSync{e3, {}};
+  stage_sync_[b].readers.push_back(e3);
+  stats_.opt_d2h_bytes += s.bytes;
+
+  if (!on_gpu) {  // updated-parameter write-back to its home tier
+    if (p.tier == PTier::Nvme) {
+      TCB_CK(cudaEventSynchronize(a1));
+      std::uint8_t* bb = bounce_.at(p.bytes);
+      host_wait_all(bounce_sync_[p.bytes]);
+      TCB_CK(cudaMemcpy(bb, pout, p.bytes, cudaMemcpyDeviceToHost));
+      bounce_sync_[p.bytes] = SlotSync{};
+      nvme_write(p, bb);
+    } else {
+      Slot& ph = slot_of(p);
+      wait_for_write(d2h_, ph.sync);
+      cudaEvent_t e4 = copy(d2h_, ph.ptr, pout, p.bytes, false);
+      ph.sync = SlotSync{e4, {}};
+      psync->readers.push_back(e4);
+    }
+    stats_.writeback_bytes += p.bytes;
+  }
+}
+
+void Executor::iteration(const StepOptions& so, cudaStream_t compute) {
+  TCB_CK(cudaSetDevice(device_));
+  if (compute == nullptr) {
+    if (!compute_owned_) TCB_CK(cudaStreamCreateWithFlags(&compute_owned_, cudaStreamNonBlocking));
+    compute = compute_owned_;
+  }
+  compute_ = compute;
+  so_ = so;
+  ++adam_step_;
+  access_cursor_ = 0;
+  TCB_CK(cudaMemsetAsync(d_checksums_, 0, std::max<std::size_t>(n_accesses_, 1) * sizeof(std::uint64_t), compute));
+  std::size_t first_opt = trace_.steps.size();
+  for (std::size_t i = 0; i < trace_.steps.size(); ++i)
+    if (trace_.steps[i].phase == Phase::OptimizerUpdate) {
+      first_opt = i;
+      break;
+    }
+  bool restored = false;
+  for (std::size_t i = 0; i < trace_.steps.size(); ++i) {
+    const TraceStep& step = trace_.steps[i];
+    if (cfg_.restore_overlap && i == first_opt && !restored) {
+      restored = true;
+      execute(policy_->on_param_restore_point());
+    }
+    execute(policy_->on_step_begin(step));
+    if (step.phase == Phase::OptimizerUpdate)
+      optimizer_step(step, compute);
+    else
+      param_step(step, i, compute);
+    execute(policy_->on_step_end(step));
+  }
+  if (!restored) execute(policy_->on_param_restore_point());
+  execute(policy_->on_iteration_end());
+  policy_->reset_iteration();
+  finish_iteration();
+}
+
+void Executor::finish_iteration() {
+  TCB_CK(cudaStreamSynchronize(h2d_));
+  TCB_CK(cudaStreamSynchronize(d2h_));
+  TCB_CK(cudaStreamSynchronize(compute_));
+  float ms = 0;
+  for (const Copy& c : copies_) {
+    TCB_CK(cudaEventElapsedTime(&ms, c.start, c.end));
+    (c.h2d ? stats_.h2d_busy_ms : stats_.d2h_busy_ms) += ms;
+  }
+  for (const auto& [reach, go] : stalls_) {
+    TCB_CK(cudaEventElapsedTime(&ms, reach, go));
+    stats_.stall_ms += ms;
+  }
+  for (const auto& [reach, arrival] : ontime_) {
+    TCB_CK(cudaEventElapsedTime(&ms, reach, arrival));
+    if (ms <= 0.0f) ++stats_.ontime_accesses;
+  }
+  for (const auto& [a0, a1] : adam_) {
+    TCB_CK(cudaEventElapsedTime(&ms, a0, a1));
+    stats_.adam_ms += ms;
+  }
+  TCB_CK(cudaMemcpy(h_checksums_.data(), d_checksums_, n_accesses_ * sizeof(std::uint64_t), cudaMemcpyDeviceToHost));
+  copies_.clear();
+  stalls_.clear();
+  ontime_.clear();
+  adam_.clear();
+  barriers_.clear();
+  // Every recorded event has completed: drop all slot references, recycle.
+  for (SlotPool* p : {&gpu_, &host_param_, &host_opt_})
+    for (auto& [size, c] : p->classes())
+      for (Slot& s : c.slots) s.sync = SlotSync{};
+  for (auto& [k, v] : bounce_sync_) v = SlotSync{};
+  for (auto& v : stage_sync_) v = SlotSync{};
+  for (auto& [k, v] : pout_sync_)
+    for (auto& y : v) y = SlotSync{};
+  for (auto& r : recs_) r.arrival = nullptr;
+  events_.recycle();
+}
+
+void Executor::sync() {
+  TCB_CK(cudaSetDevice(device_));
+  TCB_CK(cudaDeviceSynchronize());
+}
+
+const std::vector<std::uint64_t>& Executor::access_checksums() { return h_checksums_; }
+
+void Executor::seed(std::uint64_t seed) {
+  TCB_CK(cudaSetDevice(device_));
+  sync();
+  std::uint8_t* tmp = stage_[0];  // >= 6x the largest parameter
+  for (auto& p : recs_) {
+    if (p.is_state) continue;
+    const std::uint64_t n = p.bytes / 2;
+    std::uint8_t* dst = p.tier == PTier::Gpu ? where(p) : tmp;
+    TCB_CK(launch_fill_normal_bf16(reinterpret_cast<std::uint16_t*>(dst), n, 0.02f, seed, p.id, nullptr));
+    TCB_CK(launch_fill_normal_bf16(reinterpret_cast<std::uint16_t*>(p.grad), n, 1e-3f, seed + 1, p.id, nullptr));
+    if (p.tier != PTier::Gpu) {
+      TCB_CK(cudaDeviceSynchronize());
+      if (p.tier == PTier::Nvme) {
+        std::uint8_t* b = bounce_.at(p.bytes);
+        TCB_CK(cudaMemcpy(b, tmp, p.bytes, cudaMemcpyDeviceToHost));
+        nvme_write(p, b);
+      } else {
+        TCB_CK(cudaMemcpy(where(p), tmp, p.bytes, cudaMemcpyDeviceToHost));
+      }
+    }
+    if (p.partner >= 0) {  // master copy = the bf16 value, moments zero
+      TensorRec& s = recs_[static_cast<std::size_t>(p.partner)];
+      std::uint8_t* pv = p.tier == PTier::Gpu ? where(p) : tmp;
+      std::uint8_t* sdst = stage_[1];
+      TCB_CK(launch_init_state(reinterpret_cast<const std::uint16_t*>(pv), reinterpret_cast<float*>(sdst), n, nullptr));
+      TCB_CK(cudaDeviceSynchronize());
+      if (s.tier == PTier::Nvme) {
+        std::vector<std::uint8_t> hb(s.bytes);
+        void* pin = nullptr;
+        TCB_CK(cudaMallocHost(&pin, s.bytes));
+        TCB_CK(cudaMemcpy(pin, sdst, s.bytes, cudaMemcpyDeviceToHost));
+        nvme_write(s, pin);
+        cudaFreeHost(pin);
+      } else {
+        TCB_CK(cudaMemcpy(where(s), sdst, s.bytes, cudaMemcpyDeviceToHost));
+      }
+    }
+  }
+  TCB_CK(cudaDeviceSynchronize());
+  adam_step_ = 0;
+  stats_.nvme_write_bytes = 0;
+  for (auto& r : recs_) r.issued_since_access = 0;
+}
+
+void Executor::read_tensor(TensorId id, void* dst, std::uint64_t bytes) {
+  TCB_CK(cudaSetDevice(device_));
+  sync();
+  TensorRec& r = rec(id);
+  if (bytes != r.bytes) throw std::invalid_argument("read_tensor: size mismatch");
+  if (r.tier == PTier::Gpu) {
+    TCB_CK(cudaMemcpy(dst, where(r), bytes, cudaMemcpyDeviceToHost));
+  } else if (r.tier == PTier::Nvme) {
+    std::uint64_t done = 0;
+    auto* p = static_cast<std::uint8_t*>(dst);
+    if (!r.nvme_valid) throw DeviceError(TC_EINTERNAL, "NVMe replica of tensor is stale");
+    std::uint8_t* tmp = nullptr;
+    TCB_CK(cudaMallocHost(reinterpret_cast<void**>(&tmp), bytes));
+    while (done < bytes) {
+      const ssize_t k = pread(nvme_fd_, tmp + done, bytes - done, static_cast<off_t>(r.nvme_off + done));
+      if (k <= 0) {
+        cudaFreeHost(tmp);
+        throw DeviceError(TC_EIO, "read_tensor: NVMe read failed");
+      }
+      done += static_cast<std::uint64_t>(k);
+    }
+    std::memcpy(p, tmp, bytes);
+    cudaFreeHost(tmp);
+  } else {
+    std::memcpy(dst, where(r), bytes);
+  }
+}
+
+void Executor::write_tensor(TensorId id, const void* src, std::uint64_t bytes) {
+  TCB_CK(cudaSetDevice(device_));
+  sync();
+  TensorRec& r = rec(id);
+  if (bytes != r.bytes) throw std::invalid_argument("write_tensor: size mismatch");
+  if (r.tier == PTier::Gpu) {
+    TCB_CK(cudaMemcpy(where(r), src, bytes, cudaMemcpyHostToDevice));
+    r.nvme_valid = false;
+  } else if (r.tier == PTier::Nvme) {
+    std::uint8_t* tmp = nullptr;
+    TCB_CK(cudaMallocHost(reinterpret_cast<void**>(&tmp), bytes));
+    std::memcpy(tmp, src, bytes);
+    nvme_write(r, tmp);
+    cudaFreeHost(tmp);
+  } else {
+    std::memcpy(where(r), src, bytes);
+    r.nvme_valid = false;
+  }
+}
+
+void* Executor::gpu_ptr(TensorId id) {
+  TensorRec& r = rec(id);
+  return r.tier == PTier::Gpu ? where(r) : nullptr;
+}
+
+void* Executor::grad_ptr(TensorId id) { return rec(id).grad; }
+
+}  // namespace tcb
+
+// ------------------------------------------------------------------ C-ABI
+struct tc_engine {
+  std::unique_ptr<tcb::Executor> ex;
+};
+
+using namespace tcb;
+
+extern "C" {
+
+int tc_engine_create(const char* trace_path, const char* machine_path, const char* cfg_json,
+                     const tc_engine_options* opts, tc_engine** out) {
+  TC_GUARD({
+    if (out == nullptr || trace_path == nullptr) return set_error(TC_EARG, "tc_engine_create: null argument");
+    tc_engine_options o{};
+    o.gpu_spare_slots = 1;
+    o.host_spare_slots = 1;
+    o.opt_stage_slots = 3;
+    o.grad_bytes_per_param_byte = 1;
+    if (opts) o = *opts;
+    auto e = std::make_unique<tc_engine>();
+    e->ex = std::make_unique<Executor>(trace_path, machine_path ? machine_path : "", cfg_json ? cfg_json : "", o);
+    *out = e.release();
+    return TC_OK;
+  })
+}
+
+void tc_engine_destroy(tc_engine* e) { delete e; }
+
+int tc_engine_seed(tc_engine* e, uint64_t seed) {
+  TC_GUARD({
+    e->ex->seed(seed);
+    return TC_OK;
+  })
+}
+
+int tc_engine_read_tensor(tc_engine* e, uint32_t tensor, void* host_dst, uint64_t bytes) {
+  TC_GUARD({
+    e->ex->read_tensor(tensor, host_dst, bytes);
+    return TC_OK;
+  })
+}
+
+int tc_engine_write_tensor(tc_engine* e, uint32_t tensor, const void* host_src, uint64_t bytes) {
+  TC_GUARD({
+    e->ex->write_tensor(tensor, host_src, bytes);
+    return TC_OK;
+  })
+}
+
+int tc_engine_read_grad(tc_engine* e, uint32_t tensor, void* host_dst, uint64_t bytes) {
+  TC_GUARD({
+    void* g = e->ex->grad_ptr(tensor);
+    if (g == nullptr) return set_error(TC_EARG, "tensor has no gradient");
+    e->ex->sync();
+    TCB_CK(cudaMemcpy(host_dst, g, bytes, cudaMemcpyDeviceToHost));
+    return TC_OK;
+  })
+}
+
+void* tc_engine_gpu_ptr(tc_engine* e, uint32_t tensor) {
+  try {
+    return e->ex->gpu_ptr(tensor);
+  } catch (...) {
+    return nullptr;
+  }
+}
+
+void* tc_engine_grad_ptr(tc_engine* e, uint32_t tensor) {
+  try {
+    return e->ex->grad_ptr(tensor);
+  } catch (...) {
+    return nullptr;
+  }
+}
+
+int tc_engine_iteration(tc_engine* e, const tc_step_options* so, void* compute_stream) {
+  TC_GUARD({
+    StepOptions o;
+    if (so) {
+      o.lr = so->lr;
+      o.beta1 = so->beta1;
+      o.beta2 = so->beta2;
+      o.eps = so->eps;
+      o.weight_decay = so->weight_decay;
+      o.grad_scale = so->grad_scale;
+      o.compute_mode = so->compute_mode;
+      o.spin_ctas = so->spin_ctas;
+    }
+    e->ex->iteration(o, static_cast<cudaStream_t>(compute_stream));
+    return TC_OK;
+  })
+}
+
+int tc_engine_sync(tc_engine* e) {
+  TC_GUARD({
+    e->ex->sync();
+    return TC_OK;
+  })
+}
+
+int tc_engine_stats_get(tc_engine* e, tc_engine_stats* out) {
+  if (!e || !out) return set_error(TC_EARG, "null argument");
+  *out = e->ex->stats();
+  return TC_OK;
+}
+
+int tc_engine_stats_reset(tc_engine* e) {
+  if (!e) return set_error(TC_EARG, "null argument");
+  e->ex->reset_stats();
+  return TC_OK;
+}
+
+int tc_engine_access_checksums(tc_engine* e, uint64_t* out, size_t cap, size_t* n) {
+  TC_GUARD({
+    const auto& v = e->ex->access_checksums();
+    for (std::size_t i = 0; i < v.size() && i < cap; ++i) out[i] = v[i];
+    if (n) *n = v.size();
+    return TC_OK;
+  })
+}
+
+}  // extern "C"

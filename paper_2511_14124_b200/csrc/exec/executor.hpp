@@ -1,0 +1,206 @@
+// Per-GPU migration executor: replays the TenCache policy's TransferRequests
+// (scheduler.hpp:20-33) as real data movement on a B200.
+//
+// Physical layout (one set per GPU):
+//   * HBM parameter pool   — one cudaMalloc region carved into size classes
+//                            exactly like the policy's GPU BufferPool
+//                            (bufpool.cpp:47-66), plus `spare` slots/class;
+//   * pinned host pools    — parameter cache and optimizer-state cache, each
+//                            one cudaHostAlloc region carved the same way;
+//   * NVMe tier            — one sparse file, a fixed 4 KiB-aligned extent per
+//                            tensor, reached through per-class pinned bounce
+//                            buffers (the staging slot of engine.cpp:214-221);
+//   * HBM optimizer stages — a ring of state-chunk buffers for the
+//                            H2D -> fused AdamW -> D2H pipeline;
+//   * HBM gradients        — one bf16 buffer per parameter (ZeRO-3 keeps the
+//                            reduce-scattered shard on GPU for GPU Adam).
+// Logical buffer ids of the policy stay logical: physical
+// slots are chosen from per-class FIFO free lists, so an evict+prefetch pair
+// lands in slots freed a step earlier and both copy directions run at once.
+// Hazards are tracked per physical slot with CUDA events (last writer + the
+// readers since), never by stream-wide synchronisation.
+#pragma once
+
+#include <cstdint>
+#include <deque>
+#include <map>
+#include <memory>
+#include <string>
+#include <unordered_map>
+#include <vector>
+
+#include <cuda_runtime.h>
+
+#include "capi_common.hpp"
+#include "dataplane.cuh"
+#include "tencache/tencache.hpp"
+#include "tencache_c.h"
+
+namespace tcb {
+
+void cuda_check(cudaError_t e, const char* what);
+#define TCB_CK(x) ::tcb::cuda_check((x), #x)
+
+// Events are recycled only at iteration boundaries (after a full sync), so a
+// slot's recorded event is never re-recorded underneath it.
+class EventArena {
+ public:
+  ~EventArena();
+  cudaEvent_t get(bool timing = false);
+  void recycle();  // caller guarantees every event has completed
+ private:
+  std::vector<cudaEvent_t> free_, free_timed_, used_, used_timed_;
+};
+
+struct SlotSync {
+  cudaEvent_t writer = nullptr;         // last op that wrote the slot
+  std::vector<cudaEvent_t> readers;     // ops that read it since
+};
+
+enum class PTier : std::uint8_t { Gpu, HostParam, HostOpt, Nvme };
+
+struct Slot {
+  std::uint8_t* ptr = nullptr;
+  SlotSync sync;
+  std::int32_t occupant = -1;  // tensor index
+};
+
+struct SlotClass {
+  std::uint64_t size = 0;
+  std::vector<Slot> slots;
+  std::deque<std::uint32_t> free_fifo;
+};
+
+class SlotPool {
+ public:
+  void plan(std::uint64_t size, std::uint32_t count) { want_[size] += count; }
+  void allocate(bool device, int dev);
+  void release_memory();
+  SlotClass& cls(std::uint64_t size);
+  bool has_free(std::uint64_t size) const;
+  std::uint64_t bytes() const { return bytes_; }
+  std::map<std::uint64_t, SlotClass>& classes() { return classes_; }
+
+ private:
+  std::map<std::uint64_t, std::uint32_t> want_;
+  std::map<std::uint64_t, SlotClass> classes_;
+  std::uint8_t* base_ = nullptr;
+  bool device_ = false;
+  std::uint64_t bytes_ = 0;
+};
+
+struct TensorRec {
+  tencache::TensorId id = 0;
+  std::uint64_t bytes = 0;
+  bool is_state = false;
+  std::int32_t partner = -1;       // state <-> param index
+  PTier tier = PTier::Nvme;
+  std::uint32_t slot = 0;          // physical slot index within its class
+  std::uint64_t nvme_off = 0;
+  bool nvme_valid = false;         // NVMe extent holds the current bytes
+  std::uint8_t* grad = nullptr;    // params: bf16 gradient in HBM
+  int issued_since_access = 0;     // P7b hit definition
+  cudaEvent_t arrival = nullptr;   // last H2D into its GPU slot (for on-time)
+};
+
+struct StepOptions {
+  double lr = 1e-4, beta1 = 0.9, beta2 = 0.999, eps = 1e-8, weight_decay = 0.01;
+  float grad_scale = 1.0f;
+  int compute_mode = 0;
+  int spin_ctas = 1;
+};
+
+class Executor {
+ public:
+  Executor(const std::string& trace_path, const std::string& machine_path, const std::string& cfg_json,
+           const tc_engine_options& opts);
+  ~Executor();
+
+  void seed(std::uint64_t seed);
+  void iteration(const StepOptions& so, cudaStream_t compute);
+  void sync();
+  void read_tensor(tencache::TensorId id, void* dst, std::uint64_t bytes);
+  void write_tensor(tencache::TensorId id, const void* src, std::uint64_t bytes);
+  void* gpu_ptr(tencache::TensorId id);
+  void* grad_ptr(tencache::TensorId id);
+  tc_engine_stats stats() const { return stats_; }
+  void reset_stats() { stats_ = tc_engine_stats{}; }
+  const std::vector<std::uint64_t>& access_checksums();
+  const tencache::IPolicy& policy() const { return *policy_; }
+
+ private:
+  using Req = tencache::TransferRequest;
+  struct Copy {
+    cudaEvent_t start = nullptr, end = nullptr;
+    bool h2d = true;
+    std::uint64_t bytes = 0;
+  };
+
+  TensorRec& rec(tencache::TensorId id);
+  std::int32_t index_of(tencache::TensorId id) const;
+  SlotPool& pool(PTier t);
+  PTier host_tier(const TensorRec& r) const { return r.is_state ? PTier::HostOpt : PTier::HostParam; }
+  Slot& slot_of(const TensorRec& r);
+  std::uint8_t* where(const TensorRec& r);
+
+  // request execution
+  void execute(std::vector<Req> reqs);
+  bool dest_available(const Req& r) const;
+  void apply(const Req& r);
+  std::uint32_t take_slot(PTier t, std::uint64_t size, std::int32_t occupant);
+  void free_slot(PTier t, std::uint64_t size, std::uint32_t s);
+  void wait_for_write(cudaStream_t s, const SlotSync& y);
+  void wait_for_read(cudaStream_t s, const SlotSync& y);
+  void host_wait_all(const SlotSync& y);
+  cudaEvent_t copy(cudaStream_t s, void* dst, const void* src, std::uint64_t n, bool h2d);
+  void nvme_read(const TensorRec& r, void* dst);
+  void nvme_write(TensorRec& r, const void* src);
+  void ensure_nvme_fresh(TensorRec& r);
+
+  // compute
+  void param_step(const tencache::TraceStep& step, std::size_t step_idx, cudaStream_t cs);
+  void optimizer_step(const tencache::TraceStep& step, cudaStream_t cs);
+  void wait_barriers(cudaStream_t cs);
+  void finish_iteration();
+
+  tencache::ExecutionTrace trace_;
+  tencache::MachineConfig machine_;
+  tencache::RunConfig cfg_;
+  std::unique_ptr<tencache::IPolicy> policy_;
+  tc_engine_options opts_;
+  int device_ = 0;
+
+  std::vector<TensorRec> recs_;
+  std::unordered_map<tencache::TensorId, std::int32_t> index_;
+  SlotPool gpu_, host_param_, host_opt_;
+  std::map<std::uint64_t, std::uint8_t*> bounce_;  // pinned NVMe staging per class
+  std::map<std::uint64_t, SlotSync> bounce_sync_;
+  std::vector<std::uint8_t*> stage_;              // HBM optimizer ring
+  std::vector<SlotSync> stage_sync_;
+  std::uint64_t stage_bytes_ = 0;
+  std::size_t stage_next_ = 0;
+  std::map<std::uint64_t, std::vector<std::uint8_t*>> pout_scratch_;  // HBM updated-param scratch
+  std::map<std::uint64_t, std::vector<SlotSync>> pout_sync_;
+  std::map<std::uint64_t, std::size_t> pout_next_;
+  std::uint8_t* grads_ = nullptr;
+  std::uint64_t* d_checksums_ = nullptr;
+  std::vector<std::uint64_t> h_checksums_;
+  std::size_t n_accesses_ = 0, access_cursor_ = 0;
+  int nvme_fd_ = -1;
+  std::string nvme_path_;
+
+  cudaStream_t h2d_ = nullptr, d2h_ = nullptr;
+  cudaStream_t compute_ = nullptr;
+  cudaStream_t compute_owned_ = nullptr;
+  EventArena events_;
+  std::vector<cudaEvent_t> barriers_;
+  std::vector<Copy> copies_;
+  std::vector<std::pair<cudaEvent_t, cudaEvent_t>> stalls_;        // (reach, go) on compute
+  std::vector<std::pair<cudaEvent_t, cudaEvent_t>> ontime_;        // (reach, arrival)
+  std::vector<std::pair<cudaEvent_t, cudaEvent_t>> adam_;          // kernel start/end
+  std::int64_t adam_step_ = 0;
+  StepOptions so_;
+  tc_engine_stats stats_{};
+};
+
+}  // namespace tcb

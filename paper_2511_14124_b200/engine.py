@@ -1,0 +1,89 @@
+"""Per-GPU CUDA migration engine (Python mirror of the C-ABI tc_engine_*).
+
+One ``Engine`` per GPU: it owns the TenCache policy for its (shard) trace,
+the pinned host pools, the HBM pool, the NVMe tier file and the copy streams,
+and runs whole training iterations natively (csrc/exec/executor.cpp):
+policy hooks at the reference's fixed call points (engine.cpp:363-431),
+each TransferRequest as copy-engine work, the forward/backward stand-in and
+the fused AdamW on the compute stream.
+"""
+from __future__ import annotations
+
+import ctypes as C
+
+import numpy as np
+
+from . import _native as N
+
+
+class Engine:
+    def __init__(self, trace_path, machine_path="", config=None, device=0, nvme_dir="", gpu_spare_slots=1,
+                 host_spare_slots=1, opt_stage_slots=3, direct_io=False):
+        import json
+        o = N.tc_engine_options(device, N.b(nvme_dir), gpu_spare_slots, host_spare_slots, opt_stage_slots,
+                                1 if direct_io else 0, 1)
+        self._h = C.c_void_p()
+        N.check(N.lib().tc_engine_create(N.b(trace_path), N.b(machine_path), N.b(json.dumps(config or {})),
+                                         C.byref(o), C.byref(self._h)))
+        self.device = device
+
+    # -- data -----------------------------------------------------------
+    def seed(self, seed=0):
+        N.check(N.lib().tc_engine_seed(self._h, seed))
+
+    def read_tensor(self, tensor_id, nbytes, dtype=np.uint8):
+        buf = np.empty(nbytes, np.uint8)
+        N.check(N.lib().tc_engine_read_tensor(self._h, tensor_id, buf.ctypes.data, nbytes))
+        return buf.view(dtype)
+
+    def write_tensor(self, tensor_id, arr):
+        a = np.ascontiguousarray(arr).view(np.uint8)
+        N.check(N.lib().tc_engine_write_tensor(self._h, tensor_id, a.ctypes.data, a.nbytes))
+
+    def read_grad(self, tensor_id, nbytes):
+        buf = np.empty(nbytes, np.uint8)
+        N.check(N.lib().tc_engine_read_grad(self._h, tensor_id, buf.ctypes.data, nbytes))
+        return buf.view(np.uint16)
+
+    def gpu_ptr(self, tensor_id):
+        return N.lib().tc_engine_gpu_ptr(self._h, tensor_id)
+
+    def grad_ptr(self, tensor_id):
+        return N.lib().tc_engine_grad_ptr(self._h, tensor_id)
+
+    # -- execution --------------------------------------------------------
+    def iteration(self, lr=1e-4, beta1=0.9, beta2=0.999, eps=1e-8, weight_decay=0.01, grad_scale=1.0,
+                  compute_mode=0, spin_ctas=1, stream=None):
+        so = N.tc_step_options(lr, beta1, beta2, eps, weight_decay, grad_scale, compute_mode, spin_ctas)
+        N.check(N.lib().tc_engine_iteration(self._h, C.byref(so), C.c_void_p(stream or 0)))
+
+    def sync(self):
+        N.check(N.lib().tc_engine_sync(self._h))
+
+    def stats(self, reset=False):
+        s = N.tc_engine_stats()
+        N.check(N.lib().tc_engine_stats_get(self._h, C.byref(s)))
+        if reset:
+            N.check(N.lib().tc_engine_stats_reset(self._h))
+        return s.as_dict()
+
+    def reset_stats(self):
+        N.check(N.lib().tc_engine_stats_reset(self._h))
+
+    def access_checksums(self):
+        n = C.c_size_t()
+        N.check(N.lib().tc_engine_access_checksums(self._h, None, 0, C.byref(n)))
+        out = (C.c_uint64 * max(n.value, 1))()
+        N.check(N.lib().tc_engine_access_checksums(self._h, out, n.value, C.byref(n)))
+        return np.array(out[: n.value], dtype=np.uint64)
+
+    def close(self):
+        if self._h:
+            N.lib().tc_engine_destroy(self._h)
+            self._h = C.c_void_p()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
