@@ -127,7 +127,7 @@ def run_ours(args):
     setup_s = time.perf_counter() - t0
     stream = torch.cuda.current_stream()
     mode = 1 if args.compute == "spin" else 0
-    step_kw = dict(lr=1e-4, compute_mode=mode, spin_ctas=1, stream=stream.cuda_stream)
+    step_kw = dict(lr=1e-4, compute_mode=mode, spin_ctas=1, stream=stream.cuda_stream, hoist=not args.no_hoist)
     for _ in range(args.warmup):
         eng.iteration(**step_kw)
     eng.reset_stats()
@@ -140,6 +140,7 @@ def run_ours(args):
         e_ev.record(stream)
         torch.cuda.synchronize()
     ms = s_ev.elapsed_time(e_ev) / args.steps
+    phases = eng.phase_ms()
     st = eng.stats(reset=True)
     K = args.steps
 
@@ -209,6 +210,8 @@ def run_ours(args):
                  "peak_GBps": pcie_peak, "peak_source": "measured on this pool (256 MiB pinned cudaMemcpyAsync)"},
         "migration_hidden_frac": round(hidden, 4) if hidden is not None else None,
         "stall_ms_per_step": round(st["stall_ms"] / K, 3),
+        "phase_ms_last_step": {k: round(v, 2) for k, v in zip(("forward", "backward", "optimizer_and_drain"), phases)},
+        "optimizer_hoisted": not args.no_hoist,
         "roofline": {"kernel": "fused AdamW (adamw_kernel<2>)", "bound": "hbm", "achieved": round(achieved, 1),
                      "peak": hbm, "unit": "GB/s", "frac": round(achieved / hbm, 4), "traffic": traffic,
                      "algorithmic_bytes_per_launch": int(ADAM_BYTES_PER_ELEM * elems_per_launch),
@@ -396,6 +399,7 @@ def main():
     ap.add_argument("--pcie-h2d", type=float, default=55.3)
     ap.add_argument("--pcie-d2h", type=float, default=57.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-hoist", action="store_true", help="run optimizer updates in place (after backward)")
     args = ap.parse_args()
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", "1"))

@@ -136,6 +136,10 @@ int tc_adamw(float* state, const void* grad, void* param_out, uint64_t n, double
 int tc_adamw_split(float* p32, float* m, float* v, const void* grad, void* param_out, uint64_t n, double lr,
                    double beta1, double beta2, double eps, double weight_decay, int64_t step, float grad_scale,
                    void* stream);
+/* Select the AdamW kernel implementation (all are bit-identical): 0 register-
+ * unrolled, 1 register-lean one-wave, 2 TMA bulk-copy pipeline (default).
+ * Returns the previous selection. */
+int tc_set_adamw_variant(int variant);
 /* The 8 fp32 scalars the update uses, for parity tests. */
 int tc_adamw_scalars(double lr, double beta1, double beta2, double eps, double weight_decay, int64_t step,
                      float out[8]);
@@ -190,6 +194,7 @@ typedef struct {
   float grad_scale;
   int compute_mode;    /* 0: checksum only, 1: checksum + spin for compute_us*batch_scale */
   int spin_ctas;
+  int flags;           /* bit 0: run optimizer updates in place (no hoisting after the last access) */
 } tc_step_options;
 
 /* One training iteration: every trace step in order, policy decisions at the
@@ -217,6 +222,9 @@ typedef struct {
 
 int tc_engine_stats_get(tc_engine* e, tc_engine_stats* out);
 int tc_engine_stats_reset(tc_engine* e);
+/* Compute-stream phase durations of the last iteration (ms): forward,
+ * backward, optimizer (+ drain of all streams). */
+int tc_engine_phase_ms(tc_engine* e, double* out, size_t cap, size_t* n);
 /* checksum the fwd/bwd stand-in computed for each parameter access of the
  * last iteration (device -> host copy), in access order. */
 int tc_engine_access_checksums(tc_engine* e, uint64_t* out, size_t cap, size_t* n);

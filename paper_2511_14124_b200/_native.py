@@ -65,7 +65,7 @@ class tc_engine_options(C.Structure):
 class tc_step_options(C.Structure):
     _fields_ = [("lr", C.c_double), ("beta1", C.c_double), ("beta2", C.c_double), ("eps", C.c_double),
                 ("weight_decay", C.c_double), ("grad_scale", C.c_float), ("compute_mode", C.c_int),
-                ("spin_ctas", C.c_int)]
+                ("spin_ctas", C.c_int), ("flags", C.c_int)]
 
 
 class tc_engine_stats(C.Structure):
@@ -114,6 +114,7 @@ _SIGS = {
                   C.c_double, C.c_int64, C.c_float, C.c_void_p], C.c_int),
     "tc_adamw_split": ([C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_uint64, C.c_double,
                         C.c_double, C.c_double, C.c_double, C.c_double, C.c_int64, C.c_float, C.c_void_p], C.c_int),
+    "tc_set_adamw_variant": ([C.c_int], C.c_int),
     "tc_adamw_scalars": ([C.c_double] * 5 + [C.c_int64, C.POINTER(C.c_float)], C.c_int),
     "tc_checksum": ([C.c_void_p, C.c_uint64, C.c_void_p, C.c_void_p], C.c_int),
     "tc_spin": ([C.c_double, C.c_int, C.c_void_p], C.c_int),
@@ -131,6 +132,7 @@ _SIGS = {
     "tc_engine_sync": ([C.c_void_p], C.c_int),
     "tc_engine_stats_get": ([C.c_void_p, C.POINTER(tc_engine_stats)], C.c_int),
     "tc_engine_stats_reset": ([C.c_void_p], C.c_int),
+    "tc_engine_phase_ms": ([C.c_void_p, C.POINTER(C.c_double), C.c_size_t, C.POINTER(C.c_size_t)], C.c_int),
     "tc_engine_access_checksums": ([C.c_void_p, C.POINTER(C.c_uint64), C.c_size_t, C.POINTER(C.c_size_t)], C.c_int),
 }
 

@@ -104,6 +104,12 @@ int tc_adamw(float* state, const void* grad, void* param_out, uint64_t n, double
                         step, grad_scale, stream);
 }
 
+int tc_set_adamw_variant(int variant) {
+  const int prev = adamw_variant();
+  set_adamw_variant(variant);
+  return prev;
+}
+
 int tc_adamw_scalars(double lr, double beta1, double beta2, double eps, double weight_decay, int64_t step,
                      float out[8]) {
   const AdamScalars s = adam_scalars(lr, beta1, beta2, eps, weight_decay, step);

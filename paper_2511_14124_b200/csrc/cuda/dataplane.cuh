@@ -34,5 +34,8 @@ cudaError_t launch_fill_normal_bf16(std::uint16_t* out, std::uint64_t n, float s
 cudaError_t launch_init_state(const std::uint16_t* param, float* state, std::uint64_t n, cudaStream_t st);
 
 int num_sms();
+// AdamW kernel variant: 0 register-unrolled, 1 register-lean one wave, 2 TMA bulk pipeline.
+void set_adamw_variant(int v);
+int adamw_variant();
 
 }  // namespace tcb

@@ -211,6 +211,7 @@ Executor::Executor(const std::string& trace_path, const std::string& machine_pat
   h_checksums_.assign(n_accesses_, 0);
   TCB_CK(cudaStreamCreateWithFlags(&h2d_, cudaStreamNonBlocking));
   TCB_CK(cudaStreamCreateWithFlags(&d2h_, cudaStreamNonBlocking));
+  TCB_CK(cudaStreamCreateWithFlags(&opt_, cudaStreamNonBlocking));
 
   // initial physical placement = the policy's placement
   for (auto& r : recs_) {
@@ -244,6 +245,7 @@ Executor::~Executor() {
   if (d_checksums_) cudaFree(d_checksums_);
   if (h2d_) cudaStreamDestroy(h2d_);
   if (d2h_) cudaStreamDestroy(d2h_);
+  if (opt_) cudaStreamDestroy(opt_);
   if (compute_owned_) cudaStreamDestroy(compute_owned_);
   if (nvme_fd_ >= 0) close(nvme_fd_);
 }
@@ -510,15 +512,14 @@ void Executor::param_step(const TraceStep& step, std::size_t, cudaStream_t cs) {
   for (TensorId id : step.tensor_ids) slot_of(rec(id)).sync.readers.push_back(done);
 }
 
-void Executor::optimizer_step(const TraceStep& step, cudaStream_t cs) {
-  TensorRec& s = rec(step.tensor_ids.front());
-  if (!s.is_state || s.partner < 0) throw DeviceError(TC_EINTERNAL, "optimizer step without a paired state");
-  TensorRec& p = recs_[static_cast<std::size_t>(s.partner)];
+// One optimizer update, data side: state chunk H2D into an HBM stage, fused
+// AdamW on the optimizer stream (bf16 result straight into the parameter's
+// HBM slot when resident, else a scratch buffer), updated state D2H back to
+// its pinned slot, and the parameter write-back when it lives off-GPU.
+void Executor::optimizer_work(TensorRec& s, TensorRec& p) {
   if (s.tier != PTier::HostOpt) throw DeviceError(TC_EINTERNAL, "optimizer state not in host memory at its update");
   const std::uint64_t n = p.bytes / 2;
   Slot& h = slot_of(s);
-
-  // H2D: state chunk -> HBM stage (ring slot free once its last D2H is done)
   const std::size_t b = stage_next_;
   stage_next_ = (stage_next_ + 1) % stage_.size();
   std::uint8_t* stg = stage_[b];
@@ -529,10 +530,7 @@ void Executor::optimizer_step(const TraceStep& step, cudaStream_t cs) {
   stage_sync_[b] = SlotSync{e1, {}};
   stats_.opt_h2d_bytes += s.bytes;
 
-  // fused AdamW on the compute stream; the bf16 result goes straight into the
-  // parameter's HBM slot when it is resident, else into a scratch buffer.
-  TCB_CK(cudaStreamWaitEvent(cs, e1, 0));
-  wait_barriers(cs);
+  TCB_CK(cudaStreamWaitEvent(opt_, e1, 0));
   std::uint8_t* pout;
   SlotSync* psync;
   const bool on_gpu = p.tier == PTier::Gpu;
@@ -546,14 +544,14 @@ void Executor::optimizer_step(const TraceStep& step, cudaStream_t cs) {
     psync = &pout_sync_[p.bytes][k];
     k = (k + 1) % pout_scratch_[p.bytes].size();
   }
-  wait_for_write(cs, *psync);
+  wait_for_write(opt_, *psync);
   cudaEvent_t a0 = events_.get(true), a1 = events_.get(true);
-  TCB_CK(cudaEventRecord(a0, cs));
+  TCB_CK(cudaEventRecord(a0, opt_));
   auto* st = reinterpret_cast<float*>(stg);
   const AdamScalars sc = adam_scalars(so_.lr, so_.beta1, so_.beta2, so_.eps, so_.weight_decay, adam_step_);
   TCB_CK(launch_adamw(st, st + n, st + 2 * n, reinterpret_cast<const std::uint16_t*>(p.grad),
-                      reinterpret_cast<std::uint16_t*>(pout), n, sc, so_.grad_scale, cs));
-  TCB_CK(cudaEventRecord(a1, cs));
+                      reinterpret_cast<std::uint16_t*>(pout), n, sc, so_.grad_scale, opt_));
+  TCB_CK(cudaEventRecord(a1, opt_));
   adam_.emplace_back(a0, a1);
   ++stats_.kernel_launches;
   stats_.adam_elems += n;
@@ -562,15 +560,14 @@ void Executor::optimizer_step(const TraceStep& step, cudaStream_t cs) {
   p.nvme_valid = false;  // any NVMe replica of the parameter is now stale
   if (on_gpu) p.arrival = nullptr;
 
-  // D2H: updated state back to its host slot
-  wait_for_read(d2h_, stage_sync_[b]);  // writer e1 (h2d) ...
-  TCB_CK(cudaStreamWaitEvent(d2h_, a1, 0));  // ... and the update
+  wait_for_read(d2h_, stage_sync_[b]);
+  TCB_CK(cudaStreamWaitEvent(d2h_, a1, 0));
   cudaEvent_t e3 = copy(d2h_, h.ptr, stg, s.bytes, false);
   h.sync = SlotSync{e3, {}};
   stage_sync_[b].readers.push_back(e3);
   stats_.opt_d2h_bytes += s.bytes;
 
-  if (!on_gpu) {  // updated-parameter write-back to its home tier
+  if (!on_gpu) {  // updated-parameter write-back to its home tier (category iii)
     if (p.tier == PTier::Nvme) {
       TCB_CK(cudaEventSynchronize(a1));
       std::uint8_t* bb = bounce_.at(p.bytes);
@@ -589,6 +586,78 @@ void Executor::optimizer_step(const TraceStep& step, cudaStream_t cs) {
   }
 }
 
+// The whole iteration's decisions, made up front in the reference's call
+// order (engine.cpp:363-431). Legal because the request stream is a pure
+// function of (trace, capacities, policy) and independent of timing
+// (engine.hpp:49-51); it lets the executor see every future
+// move when it schedules the data work.
+std::vector<Executor::Hook> Executor::decide_iteration() {
+  std::vector<Hook> hooks;
+  std::size_t first_opt = trace_.steps.size();
+  for (std::size_t i = 0; i < trace_.steps.size(); ++i)
+    if (trace_.steps[i].phase == Phase::OptimizerUpdate) {
+      first_opt = i;
+      break;
+    }
+  bool restored = false;
+  for (std::size_t i = 0; i < trace_.steps.size(); ++i) {
+    if (cfg_.restore_overlap && i == first_opt && !restored) {
+      restored = true;
+      hooks.push_back({2, i, policy_->on_param_restore_point()});
+    }
+    hooks.push_back({0, i, policy_->on_step_begin(trace_.steps[i])});
+    hooks.push_back({1, i, policy_->on_step_end(trace_.steps[i])});
+  }
+  if (!restored) hooks.push_back({2, trace_.steps.size(), policy_->on_param_restore_point()});
+  hooks.push_back({3, trace_.steps.size(), policy_->on_iteration_end()});
+  policy_->reset_iteration();
+  return hooks;
+}
+
+// For each step, the optimizer steps whose data work runs right after that
+// step's compute (before its end-hook moves): the parameter's last forward /
+// backward access has happened, its gradient is final, and no decision
+// touches the state until the update's own step. hoist_at[i] lists opt step
+// indexes to run after step i; an opt step not listed runs in place.
+std::vector<std::size_t> Executor::plan_hoisting(const std::vector<Hook>& hooks) {
+  const std::size_t n = trace_.steps.size();
+  std::vector<std::size_t> at(n, n);  // opt step -> host step (n = in place)
+  if (!so_.hoist_optimizer) return at;
+  std::unordered_map<TensorId, std::size_t> last_access;
+  for (std::size_t i = 0; i < n; ++i)
+    if (trace_.steps[i].phase != Phase::OptimizerUpdate)
+      for (TensorId id : trace_.steps[i].tensor_ids) last_access[id] = i;
+  // position of each begin hook, and the hooks touching each tensor
+  std::vector<std::size_t> begin_pos(n, 0), end_pos(n, 0);
+  std::unordered_map<TensorId, std::vector<std::size_t>> touched;
+  for (std::size_t k = 0; k < hooks.size(); ++k) {
+    if (hooks[k].kind == 0) begin_pos[hooks[k].step] = k;
+    if (hooks[k].kind == 1) end_pos[hooks[k].step] = k;
+    for (const Req& r : hooks[k].reqs) touched[r.tensor_id].push_back(k);
+  }
+  // the state's host residency at iteration start = its placement
+  const SchedulerState& st = *policy_->scheduler_state();
+  for (std::size_t j = 0; j < n; ++j) {
+    const TraceStep& os = trace_.steps[j];
+    if (os.phase != Phase::OptimizerUpdate) continue;
+    const TensorId sid = os.tensor_ids.front();
+    const TensorRec& s = rec(sid);
+    if (!s.is_state || s.partner < 0) continue;
+    const TensorId pid = recs_[static_cast<std::size_t>(s.partner)].id;
+    auto la = last_access.find(pid);
+    if (la == last_access.end()) continue;
+    const std::size_t a = la->second;
+    if (st.final_loc(sid) != Tier::Cpu) continue;
+    bool moved = false;  // any decision moving the state before its update's end
+    auto t = touched.find(sid);
+    if (t != touched.end())
+      for (std::size_t k : t->second) moved = moved || k <= end_pos[j];
+    if (moved) continue;
+    at[j] = a;
+  }
+  return at;
+}
+
 void Executor::iteration(const StepOptions& so, cudaStream_t compute) {
   TCB_CK(cudaSetDevice(device_));
   if (compute == nullptr) {
@@ -600,29 +669,53 @@ void Executor::iteration(const StepOptions& so, cudaStream_t compute) {
   ++adam_step_;
   access_cursor_ = 0;
   TCB_CK(cudaMemsetAsync(d_checksums_, 0, std::max<std::size_t>(n_accesses_, 1) * sizeof(std::uint64_t), compute));
-  std::size_t first_opt = trace_.steps.size();
-  for (std::size_t i = 0; i < trace_.steps.size(); ++i)
-    if (trace_.steps[i].phase == Phase::OptimizerUpdate) {
-      first_opt = i;
-      break;
+  const std::vector<Hook> hooks = decide_iteration();
+  const std::vector<std::size_t> hoist = plan_hoisting(hooks);
+  const std::size_t n = trace_.steps.size();
+  std::vector<std::vector<std::size_t>> after(n);
+  for (std::size_t j = 0; j < n; ++j)
+    if (hoist[j] < n) after[hoist[j]].push_back(j);
+  auto mark = [&] {
+    cudaEvent_t e = events_.get(true);
+    TCB_CK(cudaEventRecord(e, compute));
+    phase_marks_.push_back(e);
+  };
+  mark();
+  Phase prev = Phase::Forward;
+  for (const Hook& h : hooks) {
+    if (h.kind == 0) {
+      const TraceStep& step = trace_.steps[h.step];
+      if (step.phase != prev) {
+        mark();
+        prev = step.phase;
+      }
+      execute(h.reqs);
+      if (step.phase == Phase::OptimizerUpdate) {
+        if (hoist[h.step] == n) {  // in place: waits for the state's decisions
+          TensorRec& s = rec(step.tensor_ids.front());
+          if (s.partner < 0) throw DeviceError(TC_EINTERNAL, "optimizer step without a paired state");
+          wait_barriers(opt_);
+          optimizer_work(s, recs_[static_cast<std::size_t>(s.partner)]);
+        }
+      } else {
+        param_step(step, h.step, compute);
+        for (std::size_t j : after[h.step]) {
+          TensorRec& s = rec(trace_.steps[j].tensor_ids.front());
+          optimizer_work(s, recs_[static_cast<std::size_t>(s.partner)]);
+        }
+      }
+    } else {
+      execute(h.reqs);
     }
-  bool restored = false;
-  for (std::size_t i = 0; i < trace_.steps.size(); ++i) {
-    const TraceStep& step = trace_.steps[i];
-    if (cfg_.restore_overlap && i == first_opt && !restored) {
-      restored = true;
-      execute(policy_->on_param_restore_point());
-    }
-    execute(policy_->on_step_begin(step));
-    if (step.phase == Phase::OptimizerUpdate)
-      optimizer_step(step, compute);
-    else
-      param_step(step, i, compute);
-    execute(policy_->on_step_end(step));
   }
-  if (!restored) execute(policy_->on_param_restore_point());
-  execute(policy_->on_iteration_end());
-  policy_->reset_iteration();
+  // join every stream into the compute stream: the iteration ends when the
+  // last copy and update have landed
+  for (cudaStream_t x : {h2d_, d2h_, opt_}) {
+    cudaEvent_t e = events_.get(false);
+    TCB_CK(cudaEventRecord(e, x));
+    TCB_CK(cudaStreamWaitEvent(compute, e, 0));
+  }
+  mark();
   finish_iteration();
 }
 
@@ -630,7 +723,14 @@ void Executor::finish_iteration() {
   TCB_CK(cudaStreamSynchronize(h2d_));
   TCB_CK(cudaStreamSynchronize(d2h_));
   TCB_CK(cudaStreamSynchronize(compute_));
+  TCB_CK(cudaStreamSynchronize(opt_));
   float ms = 0;
+  phase_ms_.assign(phase_marks_.size() > 1 ? phase_marks_.size() - 1 : 0, 0.0);
+  for (std::size_t i = 0; i + 1 < phase_marks_.size(); ++i) {
+    TCB_CK(cudaEventElapsedTime(&ms, phase_marks_[i], phase_marks_[i + 1]));
+    phase_ms_[i] = ms;
+  }
+  phase_marks_.clear();
   for (const Copy& c : copies_) {
     TCB_CK(cudaEventElapsedTime(&ms, c.start, c.end));
     (c.h2d ? stats_.h2d_busy_ms : stats_.d2h_busy_ms) += ms;
@@ -860,6 +960,7 @@ int tc_engine_iteration(tc_engine* e, const tc_step_options* so, void* compute_s
       o.grad_scale = so->grad_scale;
       o.compute_mode = so->compute_mode;
       o.spin_ctas = so->spin_ctas;
+      o.hoist_optimizer = (so->flags & 1) == 0;
     }
     e->ex->iteration(o, static_cast<cudaStream_t>(compute_stream));
     return TC_OK;
@@ -876,6 +977,14 @@ int tc_engine_sync(tc_engine* e) {
 int tc_engine_stats_get(tc_engine* e, tc_engine_stats* out) {
   if (!e || !out) return set_error(TC_EARG, "null argument");
   *out = e->ex->stats();
+  return TC_OK;
+}
+
+int tc_engine_phase_ms(tc_engine* e, double* out, size_t cap, size_t* n) {
+  if (!e) return set_error(TC_EARG, "null argument");
+  const auto& v = e->ex->phase_ms();
+  for (std::size_t i = 0; i < v.size() && i < cap; ++i) out[i] = v[i];
+  if (n) *n = v.size();
   return TC_OK;
 }
 

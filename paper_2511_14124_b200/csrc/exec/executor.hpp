@@ -108,6 +108,7 @@ struct StepOptions {
   float grad_scale = 1.0f;
   int compute_mode = 0;
   int spin_ctas = 1;
+  bool hoist_optimizer = true;  // run each update right after its parameter's last fwd/bwd access
 };
 
 class Executor {
@@ -126,6 +127,7 @@ class Executor {
   tc_engine_stats stats() const { return stats_; }
   void reset_stats() { stats_ = tc_engine_stats{}; }
   const std::vector<std::uint64_t>& access_checksums();
+  const std::vector<double>& phase_ms() const { return phase_ms_; }
   const tencache::IPolicy& policy() const { return *policy_; }
 
  private:
@@ -158,8 +160,15 @@ class Executor {
   void ensure_nvme_fresh(TensorRec& r);
 
   // compute
+  struct Hook {
+    int kind;           // 0 begin, 1 end, 2 restore point, 3 iteration end
+    std::size_t step;   // trace step (begin/end)
+    std::vector<Req> reqs;
+  };
+  std::vector<Hook> decide_iteration();
+  std::vector<std::size_t> plan_hoisting(const std::vector<Hook>& hooks);
   void param_step(const tencache::TraceStep& step, std::size_t step_idx, cudaStream_t cs);
-  void optimizer_step(const tencache::TraceStep& step, cudaStream_t cs);
+  void optimizer_work(TensorRec& s, TensorRec& p);
   void wait_barriers(cudaStream_t cs);
   void finish_iteration();
 
@@ -189,7 +198,8 @@ class Executor {
   int nvme_fd_ = -1;
   std::string nvme_path_;
 
-  cudaStream_t h2d_ = nullptr, d2h_ = nullptr;
+  cudaStream_t h2d_ = nullptr, d2h_ = nullptr, opt_ = nullptr;
+  std::vector<cudaEvent_t> phase_marks_;  // compute-stream timing marks: start, fwd end, bwd end, end
   cudaStream_t compute_ = nullptr;
   cudaStream_t compute_owned_ = nullptr;
   EventArena events_;
@@ -199,6 +209,7 @@ class Executor {
   std::vector<std::pair<cudaEvent_t, cudaEvent_t>> ontime_;        // (reach, arrival)
   std::vector<std::pair<cudaEvent_t, cudaEvent_t>> adam_;          // kernel start/end
   std::int64_t adam_step_ = 0;
+  std::vector<double> phase_ms_;
   StepOptions so_;
   tc_engine_stats stats_{};
 };

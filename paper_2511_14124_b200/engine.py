@@ -53,8 +53,9 @@ class Engine:
 
     # -- execution --------------------------------------------------------
     def iteration(self, lr=1e-4, beta1=0.9, beta2=0.999, eps=1e-8, weight_decay=0.01, grad_scale=1.0,
-                  compute_mode=0, spin_ctas=1, stream=None):
-        so = N.tc_step_options(lr, beta1, beta2, eps, weight_decay, grad_scale, compute_mode, spin_ctas)
+                  compute_mode=0, spin_ctas=1, stream=None, hoist=True):
+        so = N.tc_step_options(lr, beta1, beta2, eps, weight_decay, grad_scale, compute_mode, spin_ctas,
+                               0 if hoist else 1)
         N.check(N.lib().tc_engine_iteration(self._h, C.byref(so), C.c_void_p(stream or 0)))
 
     def sync(self):
@@ -66,6 +67,12 @@ class Engine:
         if reset:
             N.check(N.lib().tc_engine_stats_reset(self._h))
         return s.as_dict()
+
+    def phase_ms(self):
+        out = (C.c_double * 8)()
+        n = C.c_size_t()
+        N.check(N.lib().tc_engine_phase_ms(self._h, out, 8, C.byref(n)))
+        return list(out[: n.value])
 
     def reset_stats(self):
         N.check(N.lib().tc_engine_stats_reset(self._h))

@@ -75,6 +75,11 @@ def adamw_split(p32, m, v, grad, param_out, lr, beta1, beta2, eps, weight_decay,
                                    weight_decay, step, grad_scale, _stream(stream)))
 
 
+def set_adamw_variant(v):
+    """0 register-unrolled, 1 register-lean, 2 TMA bulk pipeline; returns previous."""
+    return N.lib().tc_set_adamw_variant(int(v))
+
+
 def adamw_scalars(lr, beta1, beta2, eps, weight_decay, step):
     out = (C.c_float * 8)()
     N.check(N.lib().tc_adamw_scalars(lr, beta1, beta2, eps, weight_decay, step, out))

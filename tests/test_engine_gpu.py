@@ -40,7 +40,7 @@ def load(tr):
     return tensors, steps
 
 
-def check_engine(tr, m, cfg, iters=2, nvme_dir=""):
+def check_engine(tr, m, cfg, iters=2, nvme_dir="", hoist=True):
     tensors, steps = load(tr)
     e = Engine(tr, m, cfg, nvme_dir=nvme_dir)
     e.seed(7)
@@ -50,7 +50,7 @@ def check_engine(tr, m, cfg, iters=2, nvme_dir=""):
     accesses = [i for s in steps if s["phase"] != "o" for i in s["ids"]]
     opt_steps = [s["ids"] for s in steps if s["phase"] == "o"]
     for it in range(1, iters + 1):
-        e.iteration(**HP)
+        e.iteration(hoist=hoist, **HP)
         got = e.access_checksums()
         want = np.array([ref.checksum(params[i]) for i in accesses], dtype=np.uint64)
         assert np.array_equal(got, want), f"iteration {it}: access checksum mismatch"
@@ -81,10 +81,11 @@ def write_with_states(d, name, sizes, gpu, cpu, fwd_multi=False, iters=2, order=
 
 @pytest.mark.parametrize("pol", ["tencache", "tencache+opt"])
 @pytest.mark.parametrize("ro", [True, False])
-def test_fig8_shape(tmpd, pol, ro):
+@pytest.mark.parametrize("hoist", [True, False])
+def test_fig8_shape(tmpd, pol, ro, hoist):
     tr, m = write_with_states(tmpd, "f8", [4096] * 6, 3 * 4096, 3 * 4096 + 6 * 6 * 4096)
     cfg = {"policy": pol, "restore_overlap": ro}
-    st = check_engine(tr, m, cfg)
+    st = check_engine(tr, m, cfg, hoist=hoist)
     rep = P.run(tr, m, cfg)
     assert st["param_accesses"] == rep["param_accesses"] and st["param_hits"] == rep["param_hits"]
 
@@ -133,7 +134,7 @@ def test_random_traces(tmpd, seed):
             continue
     else:
         pytest.skip("no plannable machine drawn")
-    st = check_engine(tr, m, cfg, iters=3, nvme_dir=tmpd)
+    st = check_engine(tr, m, cfg, iters=3, nvme_dir=tmpd, hoist=seed % 3 != 0)
     assert st["param_accesses"] == rep["param_accesses"] and st["param_hits"] == rep["param_hits"]
 
 
