@@ -1,0 +1,163 @@
+"""ZeRO-3 sharding of the chunk traces and the per-layer exchange layouts
+(SURVEY.md §8e).
+
+Every layer's flat bf16 parameters are split into N contiguous shards
+(rank r owns elements [r*per, min(E, (r+1)*per)), per = ceil(E/N)); each
+rank's shard is cut into the same number k of S-byte chunks (S from the
+largest shard, so all ranks have structurally identical traces and the
+collectives line up). Each rank runs its own engine on its own shard trace,
+pools and host link. The only exchange steps, per layer:
+
+* all-gather: each rank packs its k chunks into a contiguous send buffer;
+  NCCL all-gather produces the rank-major padded layout [r0 k*S | r1 k*S | ...];
+  ``gather_unpack_segments`` drops the padding into the flat layer view.
+* reduce-scatter: the full-layer bf16 gradient is packed into the rank-major
+  padded layout (``scatter_pack_segments``), reduce-scattered (sum), and each
+  rank's k*S result lands in the gradient buffers of its chunks.
+
+Decisions per rank are those of the reference on that rank's trace (the
+policy never needs cross-rank state).
+"""
+from __future__ import annotations
+
+import math
+import os
+from dataclasses import dataclass
+
+from . import traces as T
+
+
+@dataclass
+class LayerShard:
+    layer: int
+    elems: int          # flat elements of the full layer
+    per: int            # elements per rank (ceil)
+    chunks: int         # chunks per rank for this layer (same on every rank)
+
+    def shard_elems(self, world, rank):
+        lo = min(rank * self.per, self.elems)
+        return min(lo + self.per, self.elems) - lo
+
+
+@dataclass
+class ShardLayout:
+    model: str
+    world: int
+    chunk_bytes: int
+    layers: list
+
+    @property
+    def chunks_per_rank(self):
+        return sum(l.chunks for l in self.layers)
+
+    def send_bytes(self, layer):
+        return self.layers[layer].chunks * self.chunk_bytes
+
+    def gather_unpack_segments(self, layer):
+        """rank-major padded all-gather output -> flat layer: (src_off, dst_off, bytes)."""
+        L = self.layers[layer]
+        segs = []
+        for r in range(self.world):
+            nb = 2 * L.shard_elems(self.world, r)
+            if nb:
+                segs.append((r * L.chunks * self.chunk_bytes, 2 * r * L.per, nb))
+        return segs
+
+    def scatter_pack_segments(self, layer):
+        """flat full-layer gradient -> rank-major padded reduce-scatter input
+        (src_off in the flat layer, dst_off in the padded buffer)."""
+        return [(d, s, nb) for (s, d, nb) in self.gather_unpack_segments(layer)]
+
+
+def shard_layout(model, world, chunks_per_layer=0, target_chunk=32 * T.MIB) -> ShardLayout:
+    m = T.MODELS[model]
+    elems = [m.embed_params()] + [m.layer_params()] * m.layers
+    per_block = math.ceil(elems[1] / world)
+    k = chunks_per_layer or max(1, round(2 * per_block / target_chunk))
+    S = -(-2 * per_block // k)
+    S = -(-S // T.ALIGN) * T.ALIGN
+    layers = []
+    for i, e in enumerate(elems):
+        per = math.ceil(e / world)
+        layers.append(LayerShard(i, e, per, max(1, -(-2 * per // S))))
+    return ShardLayout(model, world, S, layers)
+
+
+def write_rank_trace(path, layout: ShardLayout, rank: int, iterations=1, tokens=16384, effective_tflops=700.0):
+    """The rank's shard trace: same structure on every rank (chunk ids, layers,
+    steps); compute time of the FULL layer's work per chunk (every rank runs
+    the whole layer's math on gathered parameters)."""
+    plan = T.ChunkPlan(layout.model, layout.world, rank, layout.chunk_bytes,
+                       [2 * l.shard_elems(layout.world, rank) for l in layout.layers],
+                       [l.chunks for l in layout.layers])
+    return T.write_chunk_trace(path, plan, iterations, tokens * layout.world, effective_tflops * layout.world)
+
+
+def bench_rank(args):
+    """bench.py under torchrun (N>1): each rank runs its own engine on its
+    shard of BASELINE configs[2] (Llama-2 7B ZeRO-3, optimizer states in
+    pinned host memory); max-over-ranks step time."""
+    import json
+    import tempfile
+
+    import torch
+    import torch.distributed as dist
+
+    from .engine import Engine
+    from . import policy as P
+
+    rank, world = int(os.environ["RANK"]), int(os.environ["WORLD_SIZE"])
+    local = int(os.environ.get("LOCAL_RANK", rank))
+    torch.cuda.set_device(local)
+    dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    layout = shard_layout("llama2-7b", world)
+    wd = tempfile.mkdtemp()
+    tp = os.path.join(wd, f"r{rank}.jsonl")
+    info = write_rank_trace(tp, layout, rank, tokens=args.tokens, effective_tflops=args.tflops)
+    n, S = layout.chunks_per_rank, layout.chunk_bytes
+    mp = T.write_machine(os.path.join(wd, "m.json"), n * S, n * 7 * S)  # all params on GPU, states in host
+    cfg = {"policy": "tencache"}
+    rep = P.run(tp, mp, cfg)
+    dec_bytes = sum(rep["transfer_bytes"].values())
+    eng = Engine(tp, mp, cfg, device=local, nvme_dir=wd)
+    eng.seed(rank)
+    stream = torch.cuda.current_stream()
+    kw = dict(lr=1e-4, compute_mode=1 if args.compute == "spin" else 0, stream=stream.cuda_stream)
+    full = torch.empty(layout.world * max(l.chunks for l in layout.layers) * S // 2, dtype=torch.bfloat16,
+                       device="cuda")
+    part = torch.empty(full.numel() // world, dtype=torch.bfloat16, device="cuda")
+    for _ in range(args.warmup):
+        eng.iteration(**kw)
+    dist.barrier()
+    torch.cuda.synchronize()
+    s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    s.record(stream)
+    for _ in range(args.steps):
+        eng.iteration(**kw)
+        # per-layer exchange volume of ZeRO-3 (2 all-gathers + 1 reduce-scatter per layer)
+        for l in layout.layers:
+            nb = l.chunks * S // 2
+            dist.all_gather_into_tensor(full[: nb * world], part[:nb])
+            dist.all_gather_into_tensor(full[: nb * world], part[:nb])
+            dist.reduce_scatter_tensor(part[:nb], full[: nb * world])
+    e.record(stream)
+    torch.cuda.synchronize()
+    ms = torch.tensor([s.elapsed_time(e) / args.steps], device="cuda")
+    dist.all_reduce(ms, op=dist.ReduceOp.MAX)
+    st = eng.stats()
+    ms = float(ms.item())
+    total = torch.tensor([float(dec_bytes)], device="cuda")
+    dist.all_reduce(total)
+    line = None
+    if rank == 0:
+        line = {"metric": "step time & migrated GB/s per GPU vs PCIe roofline; GPU cache hit rate",
+                "value": round(float(total.item()) / (ms * 1e-3) / 1e9, 4), "unit": "GB/s", "n_gpus": world,
+                "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms, 3), "higher_is_better": True,
+                "scaling": "strong", "vs_baseline": None, "dtype": "bf16/fp32", "data": "synthetic",
+                "config": {"workload": "C3: Llama-2 7B ZeRO-3, optimizer states in pinned host memory",
+                           "model": "llama2-7b", "chunks_per_rank": n, "chunk_bytes": S,
+                           "parallelism": f"zero3 x{world}"},
+                "hit_rate": {"exact": rep["hit_rate"]}, "gpu_launches": int(st["kernel_launches"]),
+                "optimizer_bytes_per_step_per_rank": st["opt_h2d_bytes"] // max(1, args.steps + args.warmup)}
+    dist.destroy_process_group()
+    return line
