@@ -127,7 +127,8 @@ def run_ours(args):
     setup_s = time.perf_counter() - t0
     stream = torch.cuda.current_stream()
     mode = 1 if args.compute == "spin" else 0
-    step_kw = dict(lr=1e-4, compute_mode=mode, spin_ctas=1, stream=stream.cuda_stream, hoist=not args.no_hoist)
+    step_kw = dict(lr=1e-4, compute_mode=mode, spin_ctas=1, stream=stream.cuda_stream, hoist=not args.no_hoist,
+                   prestage=not args.no_prestage)
     for _ in range(args.warmup):
         eng.iteration(**step_kw)
     eng.reset_stats()
@@ -211,7 +212,7 @@ def run_ours(args):
         "migration_hidden_frac": round(hidden, 4) if hidden is not None else None,
         "stall_ms_per_step": round(st["stall_ms"] / K, 3),
         "phase_ms_last_step": {k: round(v, 2) for k, v in zip(("forward", "backward", "optimizer_and_drain"), phases)},
-        "optimizer_hoisted": not args.no_hoist,
+        "optimizer_hoisted": not args.no_hoist, "optimizer_prestaged": not args.no_prestage,
         "roofline": {"kernel": "fused AdamW (adamw_kernel<2>)", "bound": "hbm", "achieved": round(achieved, 1),
                      "peak": hbm, "unit": "GB/s", "frac": round(achieved / hbm, 4), "traffic": traffic,
                      "algorithmic_bytes_per_launch": int(ADAM_BYTES_PER_ELEM * elems_per_launch),
@@ -400,6 +401,7 @@ def main():
     ap.add_argument("--pcie-d2h", type=float, default=57.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-hoist", action="store_true", help="run optimizer updates in place (after backward)")
+    ap.add_argument("--no-prestage", action="store_true", help="no staging of optimizer states ahead of updates")
     args = ap.parse_args()
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", "1"))

@@ -194,7 +194,8 @@ typedef struct {
   float grad_scale;
   int compute_mode;    /* 0: checksum only, 1: checksum + spin for compute_us*batch_scale */
   int spin_ctas;
-  int flags;           /* bit 0: run optimizer updates in place (no hoisting after the last access) */
+  int flags;           /* bit 0: run optimizer updates in place (no hoisting after the last access);
+                          bit 1: no pre-staging of optimizer states ahead of their updates */
 } tc_step_options;
 
 /* One training iteration: every trace step in order, policy decisions at the
@@ -228,6 +229,21 @@ int tc_engine_phase_ms(tc_engine* e, double* out, size_t cap, size_t* n);
 /* checksum the fwd/bwd stand-in computed for each parameter access of the
  * last iteration (device -> host copy), in access order. */
 int tc_engine_access_checksums(tc_engine* e, uint64_t* out, size_t cap, size_t* n);
+
+/* ===================== ZeRO-3 exchange ================= */
+/* NCCL (libnccl.so.2 loaded at run time) unique id, to be broadcast by the
+ * caller (e.g. torch.distributed) before tc_engine_enable_zero3. */
+int tc_nccl_unique_id(uint8_t out[128]);
+/* Switch the engine's parameter accesses to ZeRO-3: every forward/backward
+ * access all-gathers the chunk from all ranks and unpacks it into the flat
+ * layer view; every backward access packs the full-layer gradient and
+ * reduce-scatters it (sum) into this rank's gradient chunk. layer_elems[l] =
+ * flat bf16 elements of trace layer l, layer_per[l] = elements per rank
+ * (ceil). Chunks of one layer are its parameter tensors in id order. */
+int tc_engine_enable_zero3(tc_engine* e, int world, int rank, const uint8_t id[128], const uint64_t* layer_elems,
+                           const uint64_t* layer_per, uint32_t n_layers);
+/* Bytes all-gathered + reduce-scattered (NCCL payload, all ranks' pieces) so far. */
+uint64_t tc_engine_exchanged_bytes(tc_engine* e);
 
 #ifdef __cplusplus
 }

@@ -79,7 +79,7 @@ def build(verbose=False, jobs=None):
                 logs.append(log)
     if todo or not os.path.exists(LIB):
         cmd = (["g++", "-shared", "-o", LIB + ".tmp"] + objs
-               + [f"-L{CUDA}/lib64", "-lcudart_static", "-lpthread", "-ldl", "-lrt"])
+               + [f"-L{CUDA}/lib64", "-lcudart_static", "-lpthread", "-ldl", "-lrt", "-Wl,--no-undefined"])
         r = subprocess.run(cmd, capture_output=True, text=True)
         if r.returncode != 0:
             raise RuntimeError(f"link failed:\n{r.stderr}")

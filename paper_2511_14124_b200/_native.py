@@ -133,6 +133,10 @@ _SIGS = {
     "tc_engine_stats_get": ([C.c_void_p, C.POINTER(tc_engine_stats)], C.c_int),
     "tc_engine_stats_reset": ([C.c_void_p], C.c_int),
     "tc_engine_phase_ms": ([C.c_void_p, C.POINTER(C.c_double), C.c_size_t, C.POINTER(C.c_size_t)], C.c_int),
+    "tc_nccl_unique_id": ([C.c_void_p], C.c_int),
+    "tc_engine_enable_zero3": ([C.c_void_p, C.c_int, C.c_int, C.c_void_p, C.POINTER(C.c_uint64), C.POINTER(C.c_uint64),
+                                C.c_uint32], C.c_int),
+    "tc_engine_exchanged_bytes": ([C.c_void_p], C.c_uint64),
     "tc_engine_access_checksums": ([C.c_void_p, C.POINTER(C.c_uint64), C.c_size_t, C.POINTER(C.c_size_t)], C.c_int),
 }
 

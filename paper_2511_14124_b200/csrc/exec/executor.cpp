@@ -185,6 +185,7 @@ Executor::Executor(const std::string& trace_path, const std::string& machine_pat
     TCB_CK(cudaMalloc(&p, stage_bytes_));
     stage_.push_back(static_cast<std::uint8_t*>(p));
     stage_sync_.emplace_back();
+    stage_free_.push_back(static_cast<std::size_t>(i));
   }
   for (const auto& [size, _] : pclass) {
     for (int i = 0; i < 2; ++i) {
@@ -248,6 +249,13 @@ Executor::~Executor() {
   if (opt_) cudaStreamDestroy(opt_);
   if (compute_owned_) cudaStreamDestroy(compute_owned_);
   if (nvme_fd_ >= 0) close(nvme_fd_);
+  if (z3_) {
+    for (auto& [k, cp] : z3_->plans)
+      if (cp.segs) cudaFree(cp.segs);
+    for (std::uint8_t* p : {z3_->gather, z3_->view, z3_->gview, z3_->gpad})
+      if (p) cudaFree(p);
+    if (z3_->comm) nccl().CommDestroy(z3_->comm);
+  }
 }
 
 std::int32_t Executor::index_of(TensorId id) const {
@@ -495,7 +503,9 @@ void Executor::param_step(const TraceStep& step, std::size_t, cudaStream_t cs) {
     else if (x.arrival)
       ontime_.emplace_back(reach, x.arrival);
     x.issued_since_access = 0;
-    if (access_cursor_ < n_accesses_) {
+    if (z3_) {
+      zero3_access(x, step.phase == Phase::Backward, cs);
+    } else if (access_cursor_ < n_accesses_) {
       TCB_CK(launch_checksum(where(x), x.bytes & ~3ull,
                              reinterpret_cast<unsigned long long*>(d_checksums_ + access_cursor_), cs));
       ++stats_.kernel_launches;
@@ -516,21 +526,42 @@ void Executor::param_step(const TraceStep& step, std::size_t, cudaStream_t cs) {
 // AdamW on the optimizer stream (bf16 result straight into the parameter's
 // HBM slot when resident, else a scratch buffer), updated state D2H back to
 // its pinned slot, and the parameter write-back when it lives off-GPU.
+// Issue the H2D of a host-resident optimizer state into a free HBM stage.
+std::size_t Executor::stage_state(TensorRec& s) {
+  if (s.tier != PTier::HostOpt) throw DeviceError(TC_EINTERNAL, "optimizer state not in host memory when staged");
+  if (stage_free_.empty()) throw DeviceError(TC_EINTERNAL, "no free optimizer stage");
+  const std::size_t b = stage_free_.front();
+  stage_free_.pop_front();
+  Slot& h = slot_of(s);
+  wait_for_write(h2d_, stage_sync_[b]);
+  wait_for_read(h2d_, h.sync);
+  cudaEvent_t e1 = copy(h2d_, stage_[b], h.ptr, s.bytes, true);
+  h.sync.readers.push_back(e1);
+  stage_sync_[b] = SlotSync{e1, {}};
+  stats_.opt_h2d_bytes += s.bytes;
+  staged_[index_of(s.id)] = b;
+  return b;
+}
+
+// Keep up to `want_staged` states staged ahead of their updates, in update order.
+void Executor::refill_stages(std::size_t want_staged) {
+  while (prestage_next_ < prestage_order_.size() && staged_.size() < want_staged && stage_free_.size() > 1) {
+    TensorRec& s = recs_[static_cast<std::size_t>(prestage_order_[prestage_next_++])];
+    if (!staged_.count(index_of(s.id)) && s.tier == PTier::HostOpt) stage_state(s);
+  }
+}
+
 void Executor::optimizer_work(TensorRec& s, TensorRec& p) {
   if (s.tier != PTier::HostOpt) throw DeviceError(TC_EINTERNAL, "optimizer state not in host memory at its update");
   const std::uint64_t n = p.bytes / 2;
   Slot& h = slot_of(s);
-  const std::size_t b = stage_next_;
-  stage_next_ = (stage_next_ + 1) % stage_.size();
+  auto it = staged_.find(index_of(s.id));
+  const std::size_t b = it != staged_.end() ? it->second : stage_state(s);
+  staged_.erase(index_of(s.id));
   std::uint8_t* stg = stage_[b];
-  wait_for_write(h2d_, stage_sync_[b]);
-  wait_for_read(h2d_, h.sync);
-  cudaEvent_t e1 = copy(h2d_, stg, h.ptr, s.bytes, true);
-  h.sync.readers.push_back(e1);
-  stage_sync_[b] = SlotSync{e1, {}};
-  stats_.opt_h2d_bytes += s.bytes;
-
+  cudaEvent_t e1 = stage_sync_[b].writer;
   TCB_CK(cudaStreamWaitEvent(opt_, e1, 0));
+  if (p.grad_ready) TCB_CK(cudaStreamWaitEvent(opt_, p.grad_ready, 0));
   std::uint8_t* pout;
   SlotSync* psync;
   const bool on_gpu = p.tier == PTier::Gpu;
@@ -565,6 +596,7 @@ void Executor::optimizer_work(TensorRec& s, TensorRec& p) {
   cudaEvent_t e3 = copy(d2h_, h.ptr, stg, s.bytes, false);
   h.sync = SlotSync{e3, {}};
   stage_sync_[b].readers.push_back(e3);
+  stage_free_.push_back(b);
   stats_.opt_d2h_bytes += s.bytes;
 
   if (!on_gpu) {  // updated-parameter write-back to its home tier (category iii)
@@ -658,6 +690,30 @@ std::vector<std::size_t> Executor::plan_hoisting(const std::vector<Hook>& hooks)
   return at;
 }
 
+// How many optimizer states fit through the H2D link during the forward
+// pass on top of the forward's own parameter prefetches, by the machine's
+// bandwidth model (machine.cpp:101-111) and the trace's compute time.
+std::size_t Executor::forward_prestage_budget(const std::vector<Hook>& hooks) const {
+  double fwd_us = 0, fwd_h2d = 0;
+  for (const Hook& h : hooks) {
+    if ((h.kind == 0 || h.kind == 1) && trace_.steps[h.step].phase == Phase::Forward) {
+      if (h.kind == 0) fwd_us += trace_.steps[h.step].compute_us * cfg_.batch_scale;
+      for (const Req& r : h.reqs)
+        if (!r.instant && r.dst == Tier::Gpu) fwd_h2d += static_cast<double>(r.size_bytes);
+    }
+  }
+  double bw;
+  try {
+    bw = to_double(machine_.effective_bandwidth(Tier::Cpu, Tier::Gpu)) * 1e3;  // bytes per us
+  } catch (...) {
+    return 0;
+  }
+  const double spare = fwd_us * bw - fwd_h2d;
+  if (spare <= 0 || prestage_order_.empty()) return std::min<std::size_t>(1, prestage_order_.size());
+  const double sbytes = static_cast<double>(recs_[static_cast<std::size_t>(prestage_order_.front())].bytes);
+  return std::max<std::size_t>(1, static_cast<std::size_t>(spare / sbytes));
+}
+
 void Executor::iteration(const StepOptions& so, cudaStream_t compute) {
   TCB_CK(cudaSetDevice(device_));
   if (compute == nullptr) {
@@ -675,6 +731,14 @@ void Executor::iteration(const StepOptions& so, cudaStream_t compute) {
   std::vector<std::vector<std::size_t>> after(n);
   for (std::size_t j = 0; j < n; ++j)
     if (hoist[j] < n) after[hoist[j]].push_back(j);
+  // Hoisted updates in execution order; their states can be staged any time
+  // (no decision touches them before their update, plan_hoisting).
+  prestage_order_.clear();
+  prestage_next_ = 0;
+  staged_.clear();
+  for (std::size_t i = 0; i < n; ++i)
+    for (std::size_t j : after[i]) prestage_order_.push_back(index_of(trace_.steps[j].tensor_ids.front()));
+  if (so_.prestage) refill_stages(forward_prestage_budget(hooks));
   auto mark = [&] {
     cudaEvent_t e = events_.get(true);
     TCB_CK(cudaEventRecord(e, compute));
@@ -702,6 +766,7 @@ void Executor::iteration(const StepOptions& so, cudaStream_t compute) {
         for (std::size_t j : after[h.step]) {
           TensorRec& s = rec(trace_.steps[j].tensor_ids.front());
           optimizer_work(s, recs_[static_cast<std::size_t>(s.partner)]);
+          if (so_.prestage) refill_stages(prestage_lookahead_);
         }
       }
     } else {
@@ -759,10 +824,111 @@ void Executor::finish_iteration() {
       for (Slot& s : c.slots) s.sync = SlotSync{};
   for (auto& [k, v] : bounce_sync_) v = SlotSync{};
   for (auto& v : stage_sync_) v = SlotSync{};
+  staged_.clear();
+  stage_free_.clear();
+  for (std::size_t i = 0; i < stage_.size(); ++i) stage_free_.push_back(i);
   for (auto& [k, v] : pout_sync_)
     for (auto& y : v) y = SlotSync{};
-  for (auto& r : recs_) r.arrival = nullptr;
+  for (auto& r : recs_) r.arrival = r.grad_ready = nullptr;
   events_.recycle();
+}
+
+// ZeRO-3: attach a NCCL communicator and precompute, per parameter chunk, the
+// fragment list between the rank-major gathered buffer [r0 S | r1 S | ...] and
+// the flat layer view (same list reversed packs the full-layer gradient for
+// the reduce-scatter).
+void Executor::enable_zero3(int world, int rank, const ncclUniqueId& id, const std::uint64_t* layer_elems,
+                            const std::uint64_t* layer_per, std::uint32_t n_layers) {
+  TCB_CK(cudaSetDevice(device_));
+  auto z = std::make_unique<Zero3>();
+  z->world = world;
+  z->rank = rank;
+  z->layer_elems.assign(layer_elems, layer_elems + n_layers);
+  z->layer_per.assign(layer_per, layer_per + n_layers);
+  std::map<std::uint32_t, std::vector<std::int32_t>> by_layer;
+  std::uint64_t S = 0;
+  for (const auto& t : trace_.tensors)
+    if (t.kind == TensorKind::ParamFP16) {
+      if (S != 0 && t.size_bytes != S) throw ConfigError("ZeRO-3 exchange needs uniform parameter chunks");
+      S = t.size_bytes;
+      if (t.layer >= n_layers) throw ConfigError("ZeRO-3 layer table shorter than the trace's layers");
+      by_layer[t.layer].push_back(index_of(t.id));
+    }
+  z->S = S;
+  std::uint64_t max_layer = 0;
+  for (std::uint32_t l = 0; l < n_layers; ++l) max_layer = std::max(max_layer, 2 * layer_elems[l]);
+  for (auto& [layer, idxs] : by_layer) {
+    std::sort(idxs.begin(), idxs.end(), [&](std::int32_t a, std::int32_t b) { return recs_[a].id < recs_[b].id; });
+    const std::uint64_t E = layer_elems[layer], per = layer_per[layer];
+    if (per * static_cast<std::uint64_t>(world) < E) throw ConfigError("ZeRO-3: per * world < layer elements");
+    for (std::size_t c = 0; c < idxs.size(); ++c) {
+      Zero3::ChunkPlan cp;
+      cp.layer = layer;
+      std::vector<PackSeg> segs;
+      std::uint64_t v = 0;
+      for (int r = 0; r < world; ++r) {
+        const std::uint64_t lo = std::min<std::uint64_t>(static_cast<std::uint64_t>(r) * per, E);
+        const std::uint64_t shard = 2 * (std::min<std::uint64_t>(lo + per, E) - lo);
+        const std::uint64_t start = c * S;
+        if (shard <= start) continue;
+        const std::uint64_t nb = std::min<std::uint64_t>(S, shard - start);
+        segs.push_back(PackSeg{static_cast<std::uint64_t>(r) * S, 2 * lo + start, nb, v});
+        cp.pieces.emplace_back(2 * lo + start, nb);
+        cp.vec = cp.vec && ((2 * lo + start) % 16 == 0) && nb % 16 == 0;
+        v += nb;
+      }
+      cp.nseg = static_cast<std::uint32_t>(segs.size());
+      cp.total = v;
+      if (!segs.empty()) {
+        TCB_CK(cudaMalloc(&cp.segs, sizeof(PackSeg) * segs.size()));
+        TCB_CK(cudaMemcpy(cp.segs, segs.data(), sizeof(PackSeg) * segs.size(), cudaMemcpyHostToDevice));
+      }
+      z->plans[idxs[c]] = std::move(cp);
+    }
+  }
+  TCB_CK(cudaMalloc(&z->gather, world * S));
+  TCB_CK(cudaMalloc(&z->view, std::max<std::uint64_t>(max_layer, 16)));
+  TCB_CK(cudaMalloc(&z->gview, std::max<std::uint64_t>(max_layer, 16)));
+  TCB_CK(cudaMalloc(&z->gpad, world * S));
+  TCB_CK(cudaMemset(z->gpad, 0, world * S));
+  nccl_check(nccl().CommInitRank(&z->comm, world, id, rank), "ncclCommInitRank");
+  z3_ = std::move(z);
+}
+
+// One parameter access under ZeRO-3, on the compute stream: all-gather the
+// chunk from every rank, unpack into the flat layer view, checksum the view's
+// pieces (the layer compute reads exactly those). Backward also produces the
+// full-layer gradient of those pieces (stand-in: seeded per rank), packs it
+// rank-major and reduce-scatters it (sum) into this rank's gradient chunk.
+void Executor::zero3_access(TensorRec& x, bool backward, cudaStream_t cs) {
+  Zero3& z = *z3_;
+  const Zero3::ChunkPlan& cp = z.plans.at(index_of(x.id));
+  nccl_check(nccl().AllGather(where(x), z.gather, z.S, ncclUint8, z.comm, cs), "ncclAllGather");
+  z.gathered_bytes += z.S * static_cast<std::uint64_t>(z.world);
+  TCB_CK(launch_pack(cp.segs, cp.nseg, cp.total, z.gather, z.view, false, cp.vec, cs));
+  stats_.kernel_launches += 1;
+  if (access_cursor_ < n_accesses_) {
+    for (const auto& [off, nb] : cp.pieces) {
+      TCB_CK(launch_checksum(z.view + off, nb & ~3ull, reinterpret_cast<unsigned long long*>(d_checksums_ + access_cursor_),
+                             cs));
+      ++stats_.kernel_launches;
+    }
+    ++access_cursor_;
+  }
+  if (!backward) return;
+  for (const auto& [off, nb] : cp.pieces) {
+    TCB_CK(launch_fill_normal_bf16(reinterpret_cast<std::uint16_t*>(z.gview + off), nb / 2, 1e-3f,
+                                   static_cast<std::uint64_t>(adam_step_) * 1000003ull + static_cast<std::uint64_t>(z.rank),
+                                   (static_cast<std::uint64_t>(cp.layer) << 40) + off / 2, cs));
+    ++stats_.kernel_launches;
+  }
+  TCB_CK(launch_pack(cp.segs, cp.nseg, cp.total, z.gview, z.gpad, true, cp.vec, cs));
+  ++stats_.kernel_launches;
+  nccl_check(nccl().ReduceScatter(z.gpad, x.grad, z.S / 2, ncclBfloat16, ncclSum, z.comm, cs), "ncclReduceScatter");
+  z.reduced_bytes += z.S * static_cast<std::uint64_t>(z.world);
+  cudaEvent_t e = events_.get(false);
+  TCB_CK(cudaEventRecord(e, cs));
+  x.grad_ready = e;
 }
 
 void Executor::sync() {
@@ -889,7 +1055,7 @@ int tc_engine_create(const char* trace_path, const char* machine_path, const cha
     tc_engine_options o{};
     o.gpu_spare_slots = 1;
     o.host_spare_slots = 1;
-    o.opt_stage_slots = 3;
+    o.opt_stage_slots = 12;
     o.grad_bytes_per_param_byte = 1;
     if (opts) o = *opts;
     auto e = std::make_unique<tc_engine>();
@@ -961,6 +1127,7 @@ int tc_engine_iteration(tc_engine* e, const tc_step_options* so, void* compute_s
       o.compute_mode = so->compute_mode;
       o.spin_ctas = so->spin_ctas;
       o.hoist_optimizer = (so->flags & 1) == 0;
+      o.prestage = (so->flags & 2) == 0;
     }
     e->ex->iteration(o, static_cast<cudaStream_t>(compute_stream));
     return TC_OK;
@@ -973,6 +1140,28 @@ int tc_engine_sync(tc_engine* e) {
     return TC_OK;
   })
 }
+
+int tc_nccl_unique_id(uint8_t out[128]) {
+  TC_GUARD({
+    ncclUniqueId id;
+    nccl_check(nccl().GetUniqueId(&id), "ncclGetUniqueId");
+    std::memcpy(out, id.internal, sizeof(id.internal));
+    return TC_OK;
+  })
+}
+
+int tc_engine_enable_zero3(tc_engine* e, int world, int rank, const uint8_t id[128], const uint64_t* layer_elems,
+                           const uint64_t* layer_per, uint32_t n_layers) {
+  TC_GUARD({
+    if (!e || world < 1 || rank < 0 || rank >= world) return set_error(TC_EARG, "tc_engine_enable_zero3: bad arguments");
+    ncclUniqueId nid;
+    std::memcpy(nid.internal, id, sizeof(nid.internal));
+    e->ex->enable_zero3(world, rank, nid, layer_elems, layer_per, n_layers);
+    return TC_OK;
+  })
+}
+
+uint64_t tc_engine_exchanged_bytes(tc_engine* e) { return e ? e->ex->exchanged_bytes() : 0; }
 
 int tc_engine_stats_get(tc_engine* e, tc_engine_stats* out) {
   if (!e || !out) return set_error(TC_EARG, "null argument");

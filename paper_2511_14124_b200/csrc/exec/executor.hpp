@@ -33,6 +33,7 @@
 
 #include "capi_common.hpp"
 #include "dataplane.cuh"
+#include "nccl_dyn.hpp"
 #include "tencache/tencache.hpp"
 #include "tencache_c.h"
 
@@ -101,6 +102,31 @@ struct TensorRec {
   std::uint8_t* grad = nullptr;    // params: bf16 gradient in HBM
   int issued_since_access = 0;     // P7b hit definition
   cudaEvent_t arrival = nullptr;   // last H2D into its GPU slot (for on-time)
+  cudaEvent_t grad_ready = nullptr;  // ZeRO-3: reduce-scatter that produced its gradient
+};
+
+// ZeRO-3 exchange state of one rank. Chunk c of layer L holds
+// bytes [c*S, (c+1)*S) of this rank's shard of the layer's flat parameters;
+// rank r's shard starts at byte 2*r*per_L of the flat layer.
+struct Zero3 {
+  int world = 1, rank = 0;
+  ncclComm_t comm = nullptr;
+  std::uint64_t S = 0;
+  std::vector<std::uint64_t> layer_elems, layer_per;
+  struct ChunkPlan {
+    PackSeg* segs = nullptr;  // gathered (rank-major, r*S) <-> flat layer view
+    std::uint32_t nseg = 0;
+    std::uint64_t total = 0;
+    bool vec = true;
+    std::vector<std::pair<std::uint64_t, std::uint64_t>> pieces;  // (view offset, bytes)
+    std::uint32_t layer = 0;
+  };
+  std::unordered_map<std::int32_t, ChunkPlan> plans;  // by parameter rec index
+  std::uint8_t* gather = nullptr;  // world * S
+  std::uint8_t* view = nullptr;    // flat parameters of the largest layer
+  std::uint8_t* gview = nullptr;   // full-layer gradient of the current chunk's pieces
+  std::uint8_t* gpad = nullptr;    // world * S rank-major padded gradient (padding zero)
+  std::uint64_t gathered_bytes = 0, reduced_bytes = 0;
 };
 
 struct StepOptions {
@@ -109,6 +135,7 @@ struct StepOptions {
   int compute_mode = 0;
   int spin_ctas = 1;
   bool hoist_optimizer = true;  // run each update right after its parameter's last fwd/bwd access
+  bool prestage = true;         // stage optimizer states into HBM ahead of their updates
 };
 
 class Executor {
@@ -124,6 +151,9 @@ class Executor {
   void write_tensor(tencache::TensorId id, const void* src, std::uint64_t bytes);
   void* gpu_ptr(tencache::TensorId id);
   void* grad_ptr(tencache::TensorId id);
+  void enable_zero3(int world, int rank, const ncclUniqueId& id, const std::uint64_t* layer_elems,
+                    const std::uint64_t* layer_per, std::uint32_t n_layers);
+  std::uint64_t exchanged_bytes() const { return z3_ ? z3_->gathered_bytes + z3_->reduced_bytes : 0; }
   tc_engine_stats stats() const { return stats_; }
   void reset_stats() { stats_ = tc_engine_stats{}; }
   const std::vector<std::uint64_t>& access_checksums();
@@ -168,7 +198,11 @@ class Executor {
   std::vector<Hook> decide_iteration();
   std::vector<std::size_t> plan_hoisting(const std::vector<Hook>& hooks);
   void param_step(const tencache::TraceStep& step, std::size_t step_idx, cudaStream_t cs);
+  void zero3_access(TensorRec& x, bool backward, cudaStream_t cs);
   void optimizer_work(TensorRec& s, TensorRec& p);
+  std::size_t stage_state(TensorRec& s);
+  void refill_stages(std::size_t want_staged);
+  std::size_t forward_prestage_budget(const std::vector<Hook>& hooks) const;
   void wait_barriers(cudaStream_t cs);
   void finish_iteration();
 
@@ -184,10 +218,16 @@ class Executor {
   SlotPool gpu_, host_param_, host_opt_;
   std::map<std::uint64_t, std::uint8_t*> bounce_;  // pinned NVMe staging per class
   std::map<std::uint64_t, SlotSync> bounce_sync_;
-  std::vector<std::uint8_t*> stage_;              // HBM optimizer ring
+  // HBM optimizer-state stages: a state is staged (H2D) ahead of its update,
+  // updated in place, written back (D2H); the stage is then free again.
+  std::vector<std::uint8_t*> stage_;
   std::vector<SlotSync> stage_sync_;
+  std::deque<std::size_t> stage_free_;
+  std::unordered_map<std::int32_t, std::size_t> staged_;  // state index -> stage
+  std::vector<std::int32_t> prestage_order_;              // states in update (hoist) order
+  std::size_t prestage_next_ = 0;
+  std::size_t prestage_lookahead_ = 2;
   std::uint64_t stage_bytes_ = 0;
-  std::size_t stage_next_ = 0;
   std::map<std::uint64_t, std::vector<std::uint8_t*>> pout_scratch_;  // HBM updated-param scratch
   std::map<std::uint64_t, std::vector<SlotSync>> pout_sync_;
   std::map<std::uint64_t, std::size_t> pout_next_;
@@ -209,6 +249,7 @@ class Executor {
   std::vector<std::pair<cudaEvent_t, cudaEvent_t>> ontime_;        // (reach, arrival)
   std::vector<std::pair<cudaEvent_t, cudaEvent_t>> adam_;          // kernel start/end
   std::int64_t adam_step_ = 0;
+  std::unique_ptr<Zero3> z3_;
   std::vector<double> phase_ms_;
   StepOptions so_;
   tc_engine_stats stats_{};

@@ -18,7 +18,7 @@ from . import _native as N
 
 class Engine:
     def __init__(self, trace_path, machine_path="", config=None, device=0, nvme_dir="", gpu_spare_slots=1,
-                 host_spare_slots=1, opt_stage_slots=3, direct_io=False):
+                 host_spare_slots=1, opt_stage_slots=12, direct_io=False):
         import json
         o = N.tc_engine_options(device, N.b(nvme_dir), gpu_spare_slots, host_spare_slots, opt_stage_slots,
                                 1 if direct_io else 0, 1)
@@ -53,9 +53,9 @@ class Engine:
 
     # -- execution --------------------------------------------------------
     def iteration(self, lr=1e-4, beta1=0.9, beta2=0.999, eps=1e-8, weight_decay=0.01, grad_scale=1.0,
-                  compute_mode=0, spin_ctas=1, stream=None, hoist=True):
-        so = N.tc_step_options(lr, beta1, beta2, eps, weight_decay, grad_scale, compute_mode, spin_ctas,
-                               0 if hoist else 1)
+                  compute_mode=0, spin_ctas=1, stream=None, hoist=True, prestage=True):
+        flags = (0 if hoist else 1) | (0 if prestage else 2)
+        so = N.tc_step_options(lr, beta1, beta2, eps, weight_decay, grad_scale, compute_mode, spin_ctas, flags)
         N.check(N.lib().tc_engine_iteration(self._h, C.byref(so), C.c_void_p(stream or 0)))
 
     def sync(self):

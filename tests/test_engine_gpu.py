@@ -40,9 +40,9 @@ def load(tr):
     return tensors, steps
 
 
-def check_engine(tr, m, cfg, iters=2, nvme_dir="", hoist=True):
+def check_engine(tr, m, cfg, iters=2, nvme_dir="", hoist=True, prestage=True, stages=12):
     tensors, steps = load(tr)
-    e = Engine(tr, m, cfg, nvme_dir=nvme_dir)
+    e = Engine(tr, m, cfg, nvme_dir=nvme_dir, opt_stage_slots=stages)
     e.seed(7)
     params = {i: e.read_tensor(i, t["size"]).view(np.uint16).copy() for i, t in tensors.items() if t["kind"] == "p16"}
     states = {i: e.read_tensor(i, t["size"]).view(np.float32).copy() for i, t in tensors.items() if t["kind"] == "o32"}
@@ -50,7 +50,7 @@ def check_engine(tr, m, cfg, iters=2, nvme_dir="", hoist=True):
     accesses = [i for s in steps if s["phase"] != "o" for i in s["ids"]]
     opt_steps = [s["ids"] for s in steps if s["phase"] == "o"]
     for it in range(1, iters + 1):
-        e.iteration(hoist=hoist, **HP)
+        e.iteration(hoist=hoist, prestage=prestage, **HP)
         got = e.access_checksums()
         want = np.array([ref.checksum(params[i]) for i in accesses], dtype=np.uint64)
         assert np.array_equal(got, want), f"iteration {it}: access checksum mismatch"
@@ -134,7 +134,8 @@ def test_random_traces(tmpd, seed):
             continue
     else:
         pytest.skip("no plannable machine drawn")
-    st = check_engine(tr, m, cfg, iters=3, nvme_dir=tmpd, hoist=seed % 3 != 0)
+    st = check_engine(tr, m, cfg, iters=3, nvme_dir=tmpd, hoist=seed % 3 != 0, prestage=seed % 2 == 0,
+                      stages=[2, 3, 12][seed % 3])
     assert st["param_accesses"] == rep["param_accesses"] and st["param_hits"] == rep["param_hits"]
 
 
@@ -149,3 +150,44 @@ def test_chunk_trace_c2_mini(tmpd):
     rep = P.run(tp, mp, {"policy": "tencache"})
     assert st["param_hits"] == rep["param_hits"]
     assert st["h2d_bytes"] > 0 and st["d2h_bytes"] > 0
+
+
+def test_zero3_exchange_world1(tmpd):
+    """ZeRO-3 mode on one rank (NCCL nranks=1): per-chunk all-gather + unpack
+    into the layer view (checksums cover exactly the valid pieces), gradient
+    pack + reduce-scatter, AdamW on the reduce-scattered gradient."""
+    from paper_2511_14124_b200 import zero3 as Z
+    lay = Z.shard_layout("gpt2-small", 1, chunks_per_layer=3)
+    tp = os.path.join(tmpd, "z.jsonl")
+    Z.write_rank_trace(tp, lay, 0, iterations=2, tokens=64)
+    tensors, steps = load(tp)
+    n, S = lay.chunks_per_rank, lay.chunk_bytes
+    mp = T.write_machine(os.path.join(tmpd, "m.json"), int(0.5 * n) * S, n * 7 * S)
+    e = Engine(tp, mp, {"policy": "tencache"})
+    e.seed(3)
+    Z.enable(e, lay, 0, 1)
+    params = {i: e.read_tensor(i, S).view(np.uint16).copy() for i in range(1, n + 1)}
+    states = {n + i: e.read_tensor(n + i, 6 * S).view(np.float32).copy() for i in range(1, n + 1)}
+    # valid bytes of each chunk = its piece of the (single) shard
+    valid = {}
+    pid = 1
+    for L in lay.layers:
+        shard = 2 * L.shard_elems(1, 0)
+        for c in range(L.chunks):
+            valid[pid] = max(0, min(S, shard - c * S))
+            pid += 1
+    accesses = [i for s in steps if s["phase"] != "o" for i in s["ids"]]
+    for it in (1, 2):
+        e.iteration(**HP)
+        want = np.array([ref.checksum(params[i][: valid[i] // 2]) for i in accesses], dtype=np.uint64)
+        assert np.array_equal(e.access_checksums(), want), f"iteration {it}"
+        for i in range(1, n + 1):
+            g = e.read_grad(i, S)
+            st = states[n + i]
+            k = S // 2
+            params[i] = ref.adamw(st[:k], st[k:2 * k], st[2 * k:], g, HP["lr"], HP["beta1"], HP["beta2"], HP["eps"],
+                                  HP["weight_decay"], it)
+            assert np.array_equal(e.read_tensor(i, S).view(np.uint16), params[i])
+            assert np.all(g.reshape(-1)[valid[i] // 2:] == 0), "padding gradient must be zero"
+    assert Z.exchanged_bytes(e) > 0
+    e.close()
