@@ -18,13 +18,13 @@ void cuda_check(cudaError_t e, const char* what) {
 
 // ------------------------------------------------------------ EventArena
 EventArena::~EventArena() {
-  for (auto* v : {&free_, &free_timed_, &used_, &used_timed_})
+  for (auto* v : {&free_, &free_timed_})
     for (cudaEvent_t e : *v) cudaEventDestroy(e);
+  for (const Used& u : used_) cudaEventDestroy(u.e);
 }
 
 cudaEvent_t EventArena::get(bool timing) {
   auto& fr = timing ? free_timed_ : free_;
-  auto& us = timing ? used_timed_ : used_;
   cudaEvent_t e;
   if (fr.empty()) {
     TCB_CK(cudaEventCreateWithFlags(&e, timing ? cudaEventDefault : cudaEventDisableTiming));
@@ -32,16 +32,26 @@ cudaEvent_t EventArena::get(bool timing) {
     e = fr.back();
     fr.pop_back();
   }
-  us.push_back(e);
+  used_.push_back(Used{e, timing, gen_});
+  gen_of_[e] = gen_;
   return e;
 }
 
-void EventArena::recycle() {
-  free_.insert(free_.end(), used_.begin(), used_.end());
-  free_timed_.insert(free_timed_.end(), used_timed_.begin(), used_timed_.end());
-  used_.clear();
-  used_timed_.clear();
+bool EventArena::done_by(cudaEvent_t e, std::uint64_t gen) const {
+  auto it = gen_of_.find(e);
+  return it == gen_of_.end() || it->second <= gen;
 }
+
+void EventArena::recycle_upto(std::uint64_t gen) {
+  while (!used_.empty() && used_.front().gen <= gen) {
+    const Used u = used_.front();
+    used_.pop_front();
+    gen_of_.erase(u.e);
+    (u.timed ? free_timed_ : free_).push_back(u.e);
+  }
+}
+
+void EventArena::recycle_all() { recycle_upto(~0ull); }
 
 // -------------------------------------------------------------- SlotPool
 void SlotPool::allocate(bool device, int dev) {
@@ -208,11 +218,13 @@ Executor::Executor(const std::string& trace_path, const std::string& machine_pat
     }
   for (const auto& s : trace_.steps)
     if (s.phase != Phase::OptimizerUpdate) n_accesses_ += s.tensor_ids.size();
-  TCB_CK(cudaMalloc(&d_checksums_, std::max<std::size_t>(n_accesses_, 1) * sizeof(std::uint64_t)));
+  TCB_CK(cudaMalloc(&d_checksums_, 2 * std::max<std::size_t>(n_accesses_, 1) * sizeof(std::uint64_t)));
   h_checksums_.assign(n_accesses_, 0);
   TCB_CK(cudaStreamCreateWithFlags(&h2d_, cudaStreamNonBlocking));
   TCB_CK(cudaStreamCreateWithFlags(&d2h_, cudaStreamNonBlocking));
   TCB_CK(cudaStreamCreateWithFlags(&opt_, cudaStreamNonBlocking));
+  TCB_CK(cudaStreamCreateWithFlags(&h2d_opt_, cudaStreamNonBlocking));
+  TCB_CK(cudaStreamCreateWithFlags(&d2h_opt_, cudaStreamNonBlocking));
 
   // initial physical placement = the policy's placement
   for (auto& r : recs_) {
@@ -232,6 +244,10 @@ Executor::Executor(const std::string& trace_path, const std::string& machine_pat
 
 Executor::~Executor() {
   cudaSetDevice(device_);
+  try {
+    drain();
+  } catch (...) {
+  }
   if (h2d_) cudaStreamSynchronize(h2d_);
   if (d2h_) cudaStreamSynchronize(d2h_);
   cudaDeviceSynchronize();
@@ -247,6 +263,8 @@ Executor::~Executor() {
   if (h2d_) cudaStreamDestroy(h2d_);
   if (d2h_) cudaStreamDestroy(d2h_);
   if (opt_) cudaStreamDestroy(opt_);
+  if (h2d_opt_) cudaStreamDestroy(h2d_opt_);
+  if (d2h_opt_) cudaStreamDestroy(d2h_opt_);
   if (compute_owned_) cudaStreamDestroy(compute_owned_);
   if (nvme_fd_ >= 0) close(nvme_fd_);
   if (z3_) {
@@ -507,7 +525,7 @@ void Executor::param_step(const TraceStep& step, std::size_t, cudaStream_t cs) {
       zero3_access(x, step.phase == Phase::Backward, cs);
     } else if (access_cursor_ < n_accesses_) {
       TCB_CK(launch_checksum(where(x), x.bytes & ~3ull,
-                             reinterpret_cast<unsigned long long*>(d_checksums_ + access_cursor_), cs));
+                             reinterpret_cast<unsigned long long*>(cks_base_ + access_cursor_), cs));
       ++stats_.kernel_launches;
       ++access_cursor_;
     }
@@ -533,9 +551,9 @@ std::size_t Executor::stage_state(TensorRec& s) {
   const std::size_t b = stage_free_.front();
   stage_free_.pop_front();
   Slot& h = slot_of(s);
-  wait_for_write(h2d_, stage_sync_[b]);
-  wait_for_read(h2d_, h.sync);
-  cudaEvent_t e1 = copy(h2d_, stage_[b], h.ptr, s.bytes, true);
+  wait_for_write(h2d_opt_, stage_sync_[b]);
+  wait_for_read(h2d_opt_, h.sync);
+  cudaEvent_t e1 = copy(h2d_opt_, stage_[b], h.ptr, s.bytes, true);
   h.sync.readers.push_back(e1);
   stage_sync_[b] = SlotSync{e1, {}};
   stats_.opt_h2d_bytes += s.bytes;
@@ -591,9 +609,10 @@ void Executor::optimizer_work(TensorRec& s, TensorRec& p) {
   p.nvme_valid = false;  // any NVMe replica of the parameter is now stale
   if (on_gpu) p.arrival = nullptr;
 
-  wait_for_read(d2h_, stage_sync_[b]);
-  TCB_CK(cudaStreamWaitEvent(d2h_, a1, 0));
-  cudaEvent_t e3 = copy(d2h_, h.ptr, stg, s.bytes, false);
+  wait_for_read(d2h_opt_, stage_sync_[b]);
+  wait_for_write(d2h_opt_, h.sync);
+  TCB_CK(cudaStreamWaitEvent(d2h_opt_, a1, 0));
+  cudaEvent_t e3 = copy(d2h_opt_, h.ptr, stg, s.bytes, false);
   h.sync = SlotSync{e3, {}};
   stage_sync_[b].readers.push_back(e3);
   stage_free_.push_back(b);
@@ -609,8 +628,9 @@ void Executor::optimizer_work(TensorRec& s, TensorRec& p) {
       nvme_write(p, bb);
     } else {
       Slot& ph = slot_of(p);
-      wait_for_write(d2h_, ph.sync);
-      cudaEvent_t e4 = copy(d2h_, ph.ptr, pout, p.bytes, false);
+      wait_for_write(d2h_opt_, ph.sync);
+      TCB_CK(cudaStreamWaitEvent(d2h_opt_, a1, 0));
+      cudaEvent_t e4 = copy(d2h_opt_, ph.ptr, pout, p.bytes, false);
       ph.sync = SlotSync{e4, {}};
       psync->readers.push_back(e4);
     }
@@ -724,7 +744,9 @@ void Executor::iteration(const StepOptions& so, cudaStream_t compute) {
   so_ = so;
   ++adam_step_;
   access_cursor_ = 0;
-  TCB_CK(cudaMemsetAsync(d_checksums_, 0, std::max<std::size_t>(n_accesses_, 1) * sizeof(std::uint64_t), compute));
+  events_.next_generation();
+  cks_base_ = d_checksums_ + (events_.generation() % 2) * std::max<std::size_t>(n_accesses_, 1);
+  TCB_CK(cudaMemsetAsync(cks_base_, 0, std::max<std::size_t>(n_accesses_, 1) * sizeof(std::uint64_t), compute));
   const std::vector<Hook> hooks = decide_iteration();
   const std::vector<std::size_t> hoist = plan_hoisting(hooks);
   const std::size_t n = trace_.steps.size();
@@ -773,64 +795,106 @@ void Executor::iteration(const StepOptions& so, cudaStream_t compute) {
       execute(h.reqs);
     }
   }
-  // join every stream into the compute stream: the iteration ends when the
-  // last copy and update have landed
-  for (cudaStream_t x : {h2d_, d2h_, opt_}) {
-    cudaEvent_t e = events_.get(false);
-    TCB_CK(cudaEventRecord(e, x));
-    TCB_CK(cudaStreamWaitEvent(compute, e, 0));
-  }
   mark();
   finish_iteration();
 }
 
+// The iteration is enqueued; nothing waits for it here. Its timing records
+// and a fence per stream are parked; the previous iteration is harvested
+// (fences awaited, timings summed, its events recycled) so that iteration
+// t+1's forward pass overlaps iteration t's optimizer write-back tail.
 void Executor::finish_iteration() {
-  TCB_CK(cudaStreamSynchronize(h2d_));
-  TCB_CK(cudaStreamSynchronize(d2h_));
-  TCB_CK(cudaStreamSynchronize(compute_));
-  TCB_CK(cudaStreamSynchronize(opt_));
-  float ms = 0;
-  phase_ms_.assign(phase_marks_.size() > 1 ? phase_marks_.size() - 1 : 0, 0.0);
-  for (std::size_t i = 0; i + 1 < phase_marks_.size(); ++i) {
-    TCB_CK(cudaEventElapsedTime(&ms, phase_marks_[i], phase_marks_[i + 1]));
-    phase_ms_[i] = ms;
+  IterRecord rec;
+  rec.gen = events_.generation();
+  rec.copies = std::move(copies_);
+  rec.stalls = std::move(stalls_);
+  rec.ontime = std::move(ontime_);
+  rec.adam = std::move(adam_);
+  rec.marks = std::move(phase_marks_);
+  for (cudaStream_t x : {h2d_, d2h_, opt_, h2d_opt_, d2h_opt_, compute_}) {
+    cudaEvent_t e = events_.get(true);
+    TCB_CK(cudaEventRecord(e, x));
+    rec.fences.push_back(e);
   }
-  phase_marks_.clear();
-  for (const Copy& c : copies_) {
-    TCB_CK(cudaEventElapsedTime(&ms, c.start, c.end));
-    (c.h2d ? stats_.h2d_busy_ms : stats_.d2h_busy_ms) += ms;
-  }
-  for (const auto& [reach, go] : stalls_) {
-    TCB_CK(cudaEventElapsedTime(&ms, reach, go));
-    stats_.stall_ms += ms;
-  }
-  for (const auto& [reach, arrival] : ontime_) {
-    TCB_CK(cudaEventElapsedTime(&ms, reach, arrival));
-    if (ms <= 0.0f) ++stats_.ontime_accesses;
-  }
-  for (const auto& [a0, a1] : adam_) {
-    TCB_CK(cudaEventElapsedTime(&ms, a0, a1));
-    stats_.adam_ms += ms;
-  }
-  TCB_CK(cudaMemcpy(h_checksums_.data(), d_checksums_, n_accesses_ * sizeof(std::uint64_t), cudaMemcpyDeviceToHost));
+  rec.cks_buf = static_cast<std::size_t>(events_.generation() % 2);
   copies_.clear();
   stalls_.clear();
   ontime_.clear();
   adam_.clear();
-  barriers_.clear();
-  // Every recorded event has completed: drop all slot references, recycle.
+  phase_marks_.clear();
+  if (!staged_.empty()) {  // defensive: a staged state whose update did not run
+    for (auto& [idx, b] : staged_) stage_free_.push_back(b);
+    staged_.clear();
+  }
+  pending_.push_back(std::move(rec));
+  while (pending_.size() > 1) harvest_front();
+}
+
+void Executor::harvest_front() {
+  IterRecord rec = std::move(pending_.front());
+  pending_.pop_front();
+  for (cudaEvent_t f : rec.fences) TCB_CK(cudaEventSynchronize(f));
+  float ms = 0;
+  phase_ms_.clear();
+  for (std::size_t i = 0; i + 1 < rec.marks.size(); ++i) {
+    TCB_CK(cudaEventElapsedTime(&ms, rec.marks[i], rec.marks[i + 1]));
+    phase_ms_.push_back(ms);
+  }
+  if (!rec.marks.empty()) {  // whole iteration: start mark -> last fence
+    float end = 0;
+    for (cudaEvent_t f : rec.fences) {
+      TCB_CK(cudaEventElapsedTime(&ms, rec.marks.front(), f));
+      end = std::max(end, ms);
+    }
+    phase_ms_.push_back(end);
+  }
+  for (const Copy& c : rec.copies) {
+    TCB_CK(cudaEventElapsedTime(&ms, c.start, c.end));
+    (c.h2d ? stats_.h2d_busy_ms : stats_.d2h_busy_ms) += ms;
+  }
+  for (const auto& [reach, go] : rec.stalls) {
+    TCB_CK(cudaEventElapsedTime(&ms, reach, go));
+    stats_.stall_ms += ms;
+  }
+  for (const auto& [reach, arrival] : rec.ontime) {
+    TCB_CK(cudaEventElapsedTime(&ms, reach, arrival));
+    if (ms <= 0.0f) ++stats_.ontime_accesses;
+  }
+  for (const auto& [a0, a1] : rec.adam) {
+    TCB_CK(cudaEventElapsedTime(&ms, a0, a1));
+    stats_.adam_ms += ms;
+  }
+  TCB_CK(cudaMemcpy(h_checksums_.data(), d_checksums_ + rec.cks_buf * std::max<std::size_t>(n_accesses_, 1),
+                    n_accesses_ * sizeof(std::uint64_t), cudaMemcpyDeviceToHost));
+  scrub(rec.gen);
+  events_.recycle_upto(rec.gen);
+}
+
+// Drop every reference to events of generations <= gen (all complete).
+void Executor::scrub(std::uint64_t gen) {
+  auto clean = [&](SlotSync& y) {
+    if (y.writer && events_.done_by(y.writer, gen)) y.writer = nullptr;
+    std::erase_if(y.readers, [&](cudaEvent_t e) { return events_.done_by(e, gen); });
+  };
   for (SlotPool* p : {&gpu_, &host_param_, &host_opt_})
     for (auto& [size, c] : p->classes())
-      for (Slot& s : c.slots) s.sync = SlotSync{};
-  for (auto& [k, v] : bounce_sync_) v = SlotSync{};
-  for (auto& v : stage_sync_) v = SlotSync{};
-  staged_.clear();
-  stage_free_.clear();
-  for (std::size_t i = 0; i < stage_.size(); ++i) stage_free_.push_back(i);
+      for (Slot& s : c.slots) clean(s.sync);
+  for (auto& [k, v] : bounce_sync_) clean(v);
+  for (auto& v : stage_sync_) clean(v);
   for (auto& [k, v] : pout_sync_)
-    for (auto& y : v) y = SlotSync{};
-  for (auto& r : recs_) r.arrival = r.grad_ready = nullptr;
-  events_.recycle();
+    for (auto& y : v) clean(y);
+  for (auto& r : recs_) {
+    if (r.arrival && events_.done_by(r.arrival, gen)) r.arrival = nullptr;
+    if (r.grad_ready && events_.done_by(r.grad_ready, gen)) r.grad_ready = nullptr;
+  }
+  std::erase_if(barriers_, [&](cudaEvent_t e) { return events_.done_by(e, gen); });
+}
+
+void Executor::drain() {
+  while (!pending_.empty()) harvest_front();
+  TCB_CK(cudaDeviceSynchronize());
+  scrub(events_.generation());
+  events_.recycle_all();
 }
 
 // ZeRO-3: attach a NCCL communicator and precompute, per parameter chunk, the
@@ -909,7 +973,7 @@ void Executor::zero3_access(TensorRec& x, bool backward, cudaStream_t cs) {
   stats_.kernel_launches += 1;
   if (access_cursor_ < n_accesses_) {
     for (const auto& [off, nb] : cp.pieces) {
-      TCB_CK(launch_checksum(z.view + off, nb & ~3ull, reinterpret_cast<unsigned long long*>(d_checksums_ + access_cursor_),
+      TCB_CK(launch_checksum(z.view + off, nb & ~3ull, reinterpret_cast<unsigned long long*>(cks_base_ + access_cursor_),
                              cs));
       ++stats_.kernel_launches;
     }
@@ -922,6 +986,8 @@ void Executor::zero3_access(TensorRec& x, bool backward, cudaStream_t cs) {
                                    (static_cast<std::uint64_t>(cp.layer) << 40) + off / 2, cs));
     ++stats_.kernel_launches;
   }
+  if (cp.total < z.S * static_cast<std::uint64_t>(z.world))  // padded chunk: padding gradient is zero
+    TCB_CK(cudaMemsetAsync(z.gpad, 0, z.S * static_cast<std::uint64_t>(z.world), cs));
   TCB_CK(launch_pack(cp.segs, cp.nseg, cp.total, z.gview, z.gpad, true, cp.vec, cs));
   ++stats_.kernel_launches;
   nccl_check(nccl().ReduceScatter(z.gpad, x.grad, z.S / 2, ncclBfloat16, ncclSum, z.comm, cs), "ncclReduceScatter");
@@ -933,10 +999,13 @@ void Executor::zero3_access(TensorRec& x, bool backward, cudaStream_t cs) {
 
 void Executor::sync() {
   TCB_CK(cudaSetDevice(device_));
-  TCB_CK(cudaDeviceSynchronize());
+  drain();
 }
 
-const std::vector<std::uint64_t>& Executor::access_checksums() { return h_checksums_; }
+const std::vector<std::uint64_t>& Executor::access_checksums() {
+  drain();
+  return h_checksums_;
+}
 
 void Executor::seed(std::uint64_t seed) {
   TCB_CK(cudaSetDevice(device_));
@@ -1053,7 +1122,7 @@ int tc_engine_create(const char* trace_path, const char* machine_path, const cha
   TC_GUARD({
     if (out == nullptr || trace_path == nullptr) return set_error(TC_EARG, "tc_engine_create: null argument");
     tc_engine_options o{};
-    o.gpu_spare_slots = 1;
+    o.gpu_spare_slots = 4;
     o.host_spare_slots = 1;
     o.opt_stage_slots = 12;
     o.grad_bytes_per_param_byte = 1;
@@ -1164,13 +1233,21 @@ int tc_engine_enable_zero3(tc_engine* e, int world, int rank, const uint8_t id[1
 uint64_t tc_engine_exchanged_bytes(tc_engine* e) { return e ? e->ex->exchanged_bytes() : 0; }
 
 int tc_engine_stats_get(tc_engine* e, tc_engine_stats* out) {
-  if (!e || !out) return set_error(TC_EARG, "null argument");
-  *out = e->ex->stats();
-  return TC_OK;
+  TC_GUARD({
+    if (!e || !out) return set_error(TC_EARG, "null argument");
+    e->ex->sync();
+    *out = e->ex->stats();
+    return TC_OK;
+  })
 }
 
 int tc_engine_phase_ms(tc_engine* e, double* out, size_t cap, size_t* n) {
   if (!e) return set_error(TC_EARG, "null argument");
+  try {
+    e->ex->sync();
+  } catch (const std::exception& ex) {
+    return set_error(TC_ECUDA, ex.what());
+  }
   const auto& v = e->ex->phase_ms();
   for (std::size_t i = 0; i < v.size() && i < cap; ++i) out[i] = v[i];
   if (n) *n = v.size();
@@ -1178,9 +1255,12 @@ int tc_engine_phase_ms(tc_engine* e, double* out, size_t cap, size_t* n) {
 }
 
 int tc_engine_stats_reset(tc_engine* e) {
-  if (!e) return set_error(TC_EARG, "null argument");
-  e->ex->reset_stats();
-  return TC_OK;
+  TC_GUARD({
+    if (!e) return set_error(TC_EARG, "null argument");
+    e->ex->sync();
+    e->ex->reset_stats();
+    return TC_OK;
+  })
 }
 
 int tc_engine_access_checksums(tc_engine* e, uint64_t* out, size_t cap, size_t* n) {

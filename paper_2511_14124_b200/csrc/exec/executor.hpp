@@ -42,15 +42,30 @@ namespace tcb {
 void cuda_check(cudaError_t e, const char* what);
 #define TCB_CK(x) ::tcb::cuda_check((x), #x)
 
-// Events are recycled only at iteration boundaries (after a full sync), so a
-// slot's recorded event is never re-recorded underneath it.
+// Events are tagged with the iteration (generation) that recorded them and
+// recycled only once that iteration's fences have completed, after every slot
+// reference to them has been scrubbed — a recorded event is never re-recorded
+// underneath a waiter.
 class EventArena {
  public:
   ~EventArena();
   cudaEvent_t get(bool timing = false);
-  void recycle();  // caller guarantees every event has completed
+  std::uint64_t generation() const { return gen_; }
+  void next_generation() { ++gen_; }
+  bool done_by(cudaEvent_t e, std::uint64_t gen) const;  // recorded in a generation <= gen
+  void recycle_upto(std::uint64_t gen);
+  void recycle_all();
+
  private:
-  std::vector<cudaEvent_t> free_, free_timed_, used_, used_timed_;
+  struct Used {
+    cudaEvent_t e;
+    bool timed;
+    std::uint64_t gen;
+  };
+  std::vector<cudaEvent_t> free_, free_timed_;
+  std::deque<Used> used_;
+  std::unordered_map<cudaEvent_t, std::uint64_t> gen_of_;
+  std::uint64_t gen_ = 0;
 };
 
 struct SlotSync {
@@ -205,6 +220,16 @@ class Executor {
   std::size_t forward_prestage_budget(const std::vector<Hook>& hooks) const;
   void wait_barriers(cudaStream_t cs);
   void finish_iteration();
+  struct IterRecord {
+    std::uint64_t gen = 0;
+    std::vector<Copy> copies;
+    std::vector<std::pair<cudaEvent_t, cudaEvent_t>> stalls, ontime, adam;
+    std::vector<cudaEvent_t> marks, fences;
+    std::size_t cks_buf = 0;
+  };
+  void harvest_front();
+  void drain();
+  void scrub(std::uint64_t gen);
 
   tencache::ExecutionTrace trace_;
   tencache::MachineConfig machine_;
@@ -232,13 +257,18 @@ class Executor {
   std::map<std::uint64_t, std::vector<SlotSync>> pout_sync_;
   std::map<std::uint64_t, std::size_t> pout_next_;
   std::uint8_t* grads_ = nullptr;
-  std::uint64_t* d_checksums_ = nullptr;
+  std::uint64_t* d_checksums_ = nullptr;  // two buffers of n_accesses_ (iteration parity)
   std::vector<std::uint64_t> h_checksums_;
+  std::uint64_t* cks_base_ = nullptr;
   std::size_t n_accesses_ = 0, access_cursor_ = 0;
   int nvme_fd_ = -1;
   std::string nvme_path_;
 
-  cudaStream_t h2d_ = nullptr, d2h_ = nullptr, opt_ = nullptr;
+  // h2d_/d2h_: cache decisions (prefetch, evict, restore); h2d_opt_/d2h_opt_:
+  // optimizer-state staging and write-back, so evictions never queue behind
+  // state traffic; opt_: the fused AdamW.
+  cudaStream_t h2d_ = nullptr, d2h_ = nullptr, opt_ = nullptr, h2d_opt_ = nullptr, d2h_opt_ = nullptr;
+  std::deque<IterRecord> pending_;
   std::vector<cudaEvent_t> phase_marks_;  // compute-stream timing marks: start, fwd end, bwd end, end
   cudaStream_t compute_ = nullptr;
   cudaStream_t compute_owned_ = nullptr;
