@@ -118,11 +118,18 @@ def run_ours(args):
 
     torch.cuda.set_device(0)
     wd = tempfile.mkdtemp(dir="/dev/shm" if os.path.isdir("/dev/shm") else None)
-    info = build_c2(wd, args.tokens, args.tflops)
-    cfg = {"policy": "tencache"}
+    if args.config == "c4":
+        from paper_2511_14124_b200 import traces as T
+        info = T.config_c4_rank(wd, tokens=args.tokens, effective_tflops=args.tflops)
+        cfg = {"policy": "tencache+opt"}
+        nvme_dir = tempfile.mkdtemp(dir=args.nvme_dir)
+    else:
+        info = build_c2(wd, args.tokens, args.tflops)
+        cfg = {"policy": "tencache"}
+        nvme_dir = wd
     dec_bytes, dec_h2d, dec_d2h, rep = decision_bytes_per_iter(info["trace"], info["machine"], cfg)
     t0 = time.perf_counter()
-    eng = Engine(info["trace"], info["machine"], cfg, nvme_dir=wd)
+    eng = Engine(info["trace"], info["machine"], cfg, nvme_dir=nvme_dir, direct_io=args.direct_io)
     eng.seed(0)
     setup_s = time.perf_counter() - t0
     stream = torch.cuda.current_stream()
@@ -190,10 +197,14 @@ def run_ours(args):
         "metric": METRIC, "value": round(value, 4), "unit": "GB/s", "n_gpus": 1, "steps": K, "warmup": args.warmup,
         "ms_per_step": round(ms, 3), "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
         "dtype": "bf16/fp32", "data": "synthetic (seeded N(0,0.02) params, N(0,1e-3) grads; chunk trace)",
-        "config": {"workload": "C2: OPT-1.3B offloaded training step, 1xB200, GPU->pinned-CPU tier, "
-                               "size-class buffer reuse (BASELINE.json configs[1])",
-                   "model": "opt-1.3b", "chunks": info["params"], "chunk_bytes": info["chunk_bytes"],
-                   "gpu_param_chunks": info["gpu_chunks"], "policy": "tencache",
+        "config": {"workload": ("C2: OPT-1.3B offloaded training step, 1xB200, GPU->pinned-CPU tier, "
+                                "size-class buffer reuse (BASELINE.json configs[1])") if args.config == "c2" else
+                               ("C4 rank 0 of 8: GPT-3 13B ZeRO-3 shard with GPU/CPU/NVMe tiers, NVMe via pinned "
+                                "bounce buffers (BASELINE.json configs[3]), " +
+                                ("O_DIRECT" if args.direct_io else "buffered") + f" file I/O in {args.nvme_dir}"),
+                   "model": "opt-1.3b" if args.config == "c2" else "gpt3-13b",
+                   "chunks": info["params"], "chunk_bytes": info["chunk_bytes"],
+                   "gpu_param_chunks": info["gpu_chunks"], "policy": cfg["policy"],
                    "tokens_per_step": args.tokens, "compute": args.compute,
                    "compute_model_tflops": args.tflops, "l2": "inputs larger than L2 (>15 GB streamed per step)",
                    "parallelism": "single GPU"},
@@ -227,7 +238,7 @@ def run_ours(args):
         "setup_s": round(setup_s, 2),
     }
     del eng
-    if not args.no_cpu_baseline:
+    if not args.no_cpu_baseline and args.config == "c2":
         line["cpu_baseline"] = cpu_baseline(info, cfg, dec_bytes)
     line["clocks"] = clk.summary()
     return line
@@ -404,6 +415,9 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-hoist", action="store_true", help="run optimizer updates in place (after backward)")
     ap.add_argument("--no-prestage", action="store_true", help="no staging of optimizer states ahead of updates")
+    ap.add_argument("--config", default="c2", choices=["c2", "c4"])
+    ap.add_argument("--nvme-dir", default="/tmp", help="directory of the NVMe tier file (c4)")
+    ap.add_argument("--direct-io", action="store_true", help="O_DIRECT NVMe tier I/O")
     args = ap.parse_args()
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", "1"))

@@ -178,6 +178,13 @@ Executor::Executor(const std::string& trace_path, const std::string& machine_pat
     fcntl(nvme_fd_, F_SETFL, fl | O_DIRECT);
   }
   if (ftruncate(nvme_fd_, static_cast<off_t>(off)) != 0) throw DeviceError(TC_EIO, "ftruncate NVMe tier file");
+  if (!std::getenv("TC_SYNC_NVME")) {
+    try {
+      io_ = std::make_unique<NvmeQueue>(device_, nvme_fd_);
+    } catch (const std::exception&) {
+      io_.reset();  // no stream memory operations: synchronous NVMe I/O
+    }
+  }
 
   for (const auto& [size, _] : pclass) {
     void* p = nullptr;
@@ -248,6 +255,7 @@ Executor::~Executor() {
     drain();
   } catch (...) {
   }
+  io_.reset();
   if (h2d_) cudaStreamSynchronize(h2d_);
   if (d2h_) cudaStreamSynchronize(d2h_);
   cudaDeviceSynchronize();
@@ -313,16 +321,43 @@ void Executor::free_slot(PTier t, std::uint64_t size, std::uint32_t s) {
 
 void Executor::wait_for_read(cudaStream_t s, const SlotSync& y) {
   if (y.writer) TCB_CK(cudaStreamWaitEvent(s, y.writer, 0));
+  if (y.io_write && io_) io_->stream_wait(s, y.io_write);
 }
 
 void Executor::wait_for_write(cudaStream_t s, const SlotSync& y) {
   if (y.writer) TCB_CK(cudaStreamWaitEvent(s, y.writer, 0));
   for (cudaEvent_t e : y.readers) TCB_CK(cudaStreamWaitEvent(s, e, 0));
+  if (io_) io_->stream_wait(s, std::max(y.io_read, y.io_write));
 }
 
 void Executor::host_wait_all(const SlotSync& y) {
   if (y.writer) TCB_CK(cudaEventSynchronize(y.writer));
   for (cudaEvent_t e : y.readers) TCB_CK(cudaEventSynchronize(e));
+  if (io_) io_->wait(std::max(y.io_read, y.io_write));
+}
+
+// NVMe -> host buffer once every GPU op touching `target` is done; returns the
+// job (GPU consumers wait on it through target.io_write).
+std::uint64_t Executor::nvme_read_async(TensorRec& r, void* dst, SlotSync& target) {
+  std::vector<cudaEvent_t> waits(target.readers.begin(), target.readers.end());
+  if (target.writer) waits.push_back(target.writer);
+  const std::uint64_t k = io_->submit_read(dst, r.bytes, r.nvme_off, std::move(waits));
+  target = SlotSync{};
+  target.io_write = k;
+  stats_.nvme_read_bytes += r.bytes;
+  return k;
+}
+
+// host buffer -> NVMe once the copy that filled `source` is done; later writers
+// of the buffer wait on source.io_read.
+std::uint64_t Executor::nvme_write_async(TensorRec& r, const void* src, SlotSync& source) {
+  std::vector<cudaEvent_t> waits;
+  if (source.writer) waits.push_back(source.writer);
+  const std::uint64_t k = io_->submit_write(src, r.bytes, r.nvme_off, std::move(waits));
+  source.io_read = k;
+  r.nvme_valid = true;
+  stats_.nvme_write_bytes += r.bytes;
+  return k;
 }
 
 cudaEvent_t Executor::copy(cudaStream_t s, void* dst, const void* src, std::uint64_t n, bool h2d) {
@@ -370,17 +405,28 @@ void Executor::ensure_nvme_fresh(TensorRec& r) {
   if (r.tier == PTier::Gpu) {
     Slot& g = slot_of(r);
     std::uint8_t* b = bounce_.at(r.bytes);
-    host_wait_all(bounce_sync_[r.bytes]);
+    SlotSync& bs = bounce_sync_[r.bytes];
+    if (!io_) host_wait_all(bs);
     wait_for_read(d2h_, g.sync);
+    wait_for_write(d2h_, bs);
     cudaEvent_t e = copy(d2h_, b, g.ptr, r.bytes, false);
     g.sync.readers.push_back(e);
-    TCB_CK(cudaEventSynchronize(e));
-    bounce_sync_[r.bytes] = SlotSync{};
-    nvme_write(r, b);
+    if (io_) {
+      bs = SlotSync{e, {}};
+      nvme_write_async(r, b, bs);
+    } else {
+      TCB_CK(cudaEventSynchronize(e));
+      bs = SlotSync{};
+      nvme_write(r, b);
+    }
   } else {
     Slot& h = slot_of(r);
-    host_wait_all(h.sync);
-    nvme_write(r, h.ptr);
+    if (io_) {
+      nvme_write_async(r, h.ptr, h.sync);
+    } else {
+      host_wait_all(h.sync);
+      nvme_write(r, h.ptr);
+    }
   }
   stats_.writeback_bytes += r.bytes;
 }
@@ -456,11 +502,18 @@ void Executor::apply(const Req& r) {
     const std::uint32_t gs = take_slot(PTier::Gpu, x.bytes, xi);
     Slot& g = gpu_.cls(x.bytes).slots[gs];
     std::uint8_t* b = bounce_.at(x.bytes);
-    host_wait_all(bounce_sync_[x.bytes]);
-    nvme_read(x, b);
+    SlotSync& bs = bounce_sync_[x.bytes];
+    if (io_) {
+      nvme_read_async(x, b, bs);
+    } else {
+      host_wait_all(bs);
+      nvme_read(x, b);
+      bs = SlotSync{};
+    }
     wait_for_write(h2d_, g.sync);
+    wait_for_read(h2d_, bs);
     done = copy(h2d_, g.ptr, b, x.bytes, true);
-    bounce_sync_[x.bytes] = SlotSync{nullptr, {done}};
+    bs.readers.push_back(done);
     g.sync.writer = done;
     g.sync.readers.clear();
     if (!r.src_retains) x.nvme_valid = false;
@@ -472,19 +525,26 @@ void Executor::apply(const Req& r) {
     const PTier ht = host_tier(x);
     const std::uint32_t hs = take_slot(ht, x.bytes, xi);
     Slot& h = pool(ht).cls(x.bytes).slots[hs];
-    host_wait_all(h.sync);
-    nvme_read(x, h.ptr);
-    h.sync = SlotSync{};
+    if (io_) {
+      nvme_read_async(x, h.ptr, h.sync);
+    } else {
+      host_wait_all(h.sync);
+      nvme_read(x, h.ptr);
+      h.sync = SlotSync{};
+    }
     x.tier = ht;
     x.slot = hs;
   } else if (r.src == Tier::Cpu && r.dst == Tier::Nvme) {  // spill / state write-back
-    if (!r.instant || !x.nvme_valid) {
-      Slot& h = slot_of(x);
-      host_wait_all(h.sync);
-      nvme_write(x, h.ptr);
-    }
     Slot& h = slot_of(x);
-    h.sync = SlotSync{};
+    if (!r.instant || !x.nvme_valid) {
+      if (io_) {
+        nvme_write_async(x, h.ptr, h.sync);  // later writers of the slot wait on the job
+      } else {
+        host_wait_all(h.sync);
+        nvme_write(x, h.ptr);
+        h.sync = SlotSync{};
+      }
+    }
     free_slot(x.tier, x.bytes, x.slot);
     x.tier = PTier::Nvme;
   } else if (r.src == Tier::Gpu && r.dst == Tier::Nvme) {  // drop (replica authoritative) or write-back
@@ -620,12 +680,22 @@ void Executor::optimizer_work(TensorRec& s, TensorRec& p) {
 
   if (!on_gpu) {  // updated-parameter write-back to its home tier (category iii)
     if (p.tier == PTier::Nvme) {
-      TCB_CK(cudaEventSynchronize(a1));
       std::uint8_t* bb = bounce_.at(p.bytes);
-      host_wait_all(bounce_sync_[p.bytes]);
-      TCB_CK(cudaMemcpy(bb, pout, p.bytes, cudaMemcpyDeviceToHost));
-      bounce_sync_[p.bytes] = SlotSync{};
-      nvme_write(p, bb);
+      SlotSync& bs = bounce_sync_[p.bytes];
+      if (io_) {
+        wait_for_write(d2h_opt_, bs);
+        TCB_CK(cudaStreamWaitEvent(d2h_opt_, a1, 0));
+        cudaEvent_t e4 = copy(d2h_opt_, bb, pout, p.bytes, false);
+        psync->readers.push_back(e4);
+        bs = SlotSync{e4, {}};
+        nvme_write_async(p, bb, bs);
+      } else {
+        TCB_CK(cudaEventSynchronize(a1));
+        host_wait_all(bs);
+        TCB_CK(cudaMemcpy(bb, pout, p.bytes, cudaMemcpyDeviceToHost));
+        bs = SlotSync{};
+        nvme_write(p, bb);
+      }
     } else {
       Slot& ph = slot_of(p);
       wait_for_write(d2h_opt_, ph.sync);
@@ -817,6 +887,7 @@ void Executor::finish_iteration() {
     rec.fences.push_back(e);
   }
   rec.cks_buf = static_cast<std::size_t>(events_.generation() % 2);
+  rec.io_seq = io_ ? io_->submitted() : 0;
   copies_.clear();
   stalls_.clear();
   ontime_.clear();
@@ -834,6 +905,7 @@ void Executor::harvest_front() {
   IterRecord rec = std::move(pending_.front());
   pending_.pop_front();
   for (cudaEvent_t f : rec.fences) TCB_CK(cudaEventSynchronize(f));
+  if (io_) io_->wait(rec.io_seq);  // no queued job may still name an event we recycle
   float ms = 0;
   phase_ms_.clear();
   for (std::size_t i = 0; i + 1 < rec.marks.size(); ++i) {
@@ -872,9 +944,12 @@ void Executor::harvest_front() {
 
 // Drop every reference to events of generations <= gen (all complete).
 void Executor::scrub(std::uint64_t gen) {
+  const std::uint64_t io_done = io_ ? io_->done() : 0;
   auto clean = [&](SlotSync& y) {
     if (y.writer && events_.done_by(y.writer, gen)) y.writer = nullptr;
     std::erase_if(y.readers, [&](cudaEvent_t e) { return events_.done_by(e, gen); });
+    if (y.io_read <= io_done) y.io_read = 0;
+    if (y.io_write <= io_done) y.io_write = 0;
   };
   for (SlotPool* p : {&gpu_, &host_param_, &host_opt_})
     for (auto& [size, c] : p->classes())
@@ -892,6 +967,7 @@ void Executor::scrub(std::uint64_t gen) {
 
 void Executor::drain() {
   while (!pending_.empty()) harvest_front();
+  if (io_) io_->wait_all();
   TCB_CK(cudaDeviceSynchronize());
   scrub(events_.generation());
   events_.recycle_all();

@@ -34,6 +34,7 @@
 #include "capi_common.hpp"
 #include "dataplane.cuh"
 #include "nccl_dyn.hpp"
+#include "nvme_io.hpp"
 #include "tencache/tencache.hpp"
 #include "tencache_c.h"
 
@@ -71,6 +72,8 @@ class EventArena {
 struct SlotSync {
   cudaEvent_t writer = nullptr;         // last op that wrote the slot
   std::vector<cudaEvent_t> readers;     // ops that read it since
+  std::uint64_t io_write = 0;           // NVMe job that filled it (host buffers)
+  std::uint64_t io_read = 0;            // NVMe job that last read it
 };
 
 enum class PTier : std::uint8_t { Gpu, HostParam, HostOpt, Nvme };
@@ -226,6 +229,7 @@ class Executor {
     std::vector<std::pair<cudaEvent_t, cudaEvent_t>> stalls, ontime, adam;
     std::vector<cudaEvent_t> marks, fences;
     std::size_t cks_buf = 0;
+    std::uint64_t io_seq = 0;  // last NVMe job submitted in the iteration
   };
   void harvest_front();
   void drain();
@@ -262,6 +266,9 @@ class Executor {
   std::uint64_t* cks_base_ = nullptr;
   std::size_t n_accesses_ = 0, access_cursor_ = 0;
   int nvme_fd_ = -1;
+  std::unique_ptr<NvmeQueue> io_;  // async NVMe tier I/O (null: synchronous fallback)
+  std::uint64_t nvme_read_async(TensorRec& r, void* dst, SlotSync& target);
+  std::uint64_t nvme_write_async(TensorRec& r, const void* src, SlotSync& source);
   std::string nvme_path_;
 
   // h2d_/d2h_: cache decisions (prefetch, evict, restore); h2d_opt_/d2h_opt_:

@@ -1,0 +1,61 @@
+// Asynchronous NVMe tier I/O. One worker thread executes jobs in FIFO order:
+// wait for the CUDA events the job depends on (the copy that filled a pinned
+// buffer, or the copies that last read it), then pread/pwrite between the
+// pinned buffer and the tier file, then publish the job's sequence number in
+// a mapped host word. GPU streams that consume the bytes wait on that word
+// with cuStreamWaitValue32 (no host thread blocks in the iteration, no CUDA
+// host callbacks); host code waits on a condition variable.
+#pragma once
+
+#include <condition_variable>
+#include <cstdint>
+#include <deque>
+#include <mutex>
+#include <thread>
+#include <vector>
+
+#include <cuda_runtime.h>
+
+namespace tcb {
+
+class NvmeQueue {
+ public:
+  // Throws DeviceError when stream memory operations are unavailable.
+  NvmeQueue(int device, int fd);
+  ~NvmeQueue();
+
+  std::uint64_t submit_read(void* dst, std::uint64_t bytes, std::uint64_t file_off, std::vector<cudaEvent_t> waits);
+  std::uint64_t submit_write(const void* src, std::uint64_t bytes, std::uint64_t file_off,
+                             std::vector<cudaEvent_t> waits);
+  void stream_wait(cudaStream_t s, std::uint64_t seq);  // GPU-side wait for job `seq`
+  void wait(std::uint64_t seq);                         // host-side wait
+  void wait_all() { wait(submitted_); }
+  std::uint64_t done() const;
+  std::uint64_t submitted() const { return submitted_; }
+  std::uint64_t bytes_read() const { return bytes_read_; }
+  std::uint64_t bytes_written() const { return bytes_written_; }
+
+ private:
+  struct Job {
+    bool write;
+    void* buf;
+    std::uint64_t bytes, off, seq;
+    std::vector<cudaEvent_t> waits;
+  };
+  std::uint64_t submit(Job j);
+  void run();
+
+  int device_, fd_;
+  volatile std::uint32_t* flag_ = nullptr;  // mapped pinned word: last completed seq
+  void* flag_dev_ = nullptr;
+  void* wait_fn_ = nullptr;                 // cuStreamWaitValue32
+  std::mutex mu_;
+  std::condition_variable cv_, done_cv_;
+  std::deque<Job> q_;
+  std::uint64_t submitted_ = 0, done_ = 0, bytes_read_ = 0, bytes_written_ = 0;
+  bool stop_ = false;
+  std::string error_;
+  std::thread worker_;
+};
+
+}  // namespace tcb

@@ -187,3 +187,23 @@ def config_c2(workdir: str, iterations: int = 1, gpu_fraction: float = 0.4, toke
     write_machine(mp, g * S, (n - g) * S + n * 6 * S, pinned_overrides=links)
     info.update({"gpu_chunks": g, "trace": tp, "machine": mp, "plan": plan})
     return info
+
+
+def config_c4_rank(workdir: str, world: int = 8, rank: int = 0, iterations: int = 1, cpu_state_fraction: float = 0.6,
+                   tokens: int = 16384, effective_tflops: float = 700.0, links: dict | None = None):
+    """BASELINE configs[3] (GPT-3 13B ZeRO-3 with GPU/CPU/NVMe tiers), one
+    rank's shard: every parameter chunk on the GPU, the optimizer states split
+    by the +Opt posture: floor(cpu_state_fraction * n) in pinned host memory,
+    the rest in NVMe, streamed through pinned bounce buffers."""
+    import os
+    from . import zero3 as Z
+    lay = Z.shard_layout("gpt3-13b", world)
+    tp = os.path.join(workdir, f"c4_r{rank}.jsonl")
+    info = Z.write_rank_trace(tp, lay, rank, iterations, tokens, effective_tflops)
+    S, n = lay.chunk_bytes, lay.chunks_per_rank
+    k = int(cpu_state_fraction * n)
+    mp = os.path.join(workdir, "c4_machine.json")
+    links = links or {"cpu->gpu": 55.3, "gpu->cpu": 57.0}
+    write_machine(mp, n * S, k * 6 * S + 1, pinned_overrides=links)
+    info.update({"trace": tp, "machine": mp, "gpu_chunks": n, "cpu_states": k, "params": n, "chunk_bytes": S})
+    return info

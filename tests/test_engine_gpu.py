@@ -91,7 +91,10 @@ def test_fig8_shape(tmpd, pol, ro, hoist):
 
 
 @pytest.mark.parametrize("pol", ["tencache", "tencache+opt"])
-def test_nvme_tiers(tmpd, pol):
+@pytest.mark.parametrize("io", ["async", "sync"])
+def test_nvme_tiers(tmpd, pol, io, monkeypatch):
+    if io == "sync":
+        monkeypatch.setenv("TC_SYNC_NVME", "1")
     # fig9 shape: tensor 7 placed in NVMe, CPU victim spilled, staged fetches;
     # optimizer states partly (or, base posture, all) in NVMe.
     tr, m = write_with_states(tmpd, "f9", [4096] * 7, 3 * 4096, 3 * 4096 + 2 * 6 * 4096, iters=3)
