@@ -137,7 +137,8 @@ int tc_adamw_split(float* p32, float* m, float* v, const void* grad, void* param
                    double beta1, double beta2, double eps, double weight_decay, int64_t step, float grad_scale,
                    void* stream);
 /* Select the AdamW kernel implementation (all are bit-identical): 0 register-
- * unrolled, 1 register-lean one-wave, 2 TMA bulk-copy pipeline (default).
+ * unrolled, 1 register-lean one-wave, 2 TMA bulk-copy pipeline 256 thr x 3 stages
+ * (default), 3 TMA 512 thr x 3 stages, 4 TMA 512 thr x 6 stages, 5 TMA 1024 thr x 6.
  * Returns the previous selection. */
 int tc_set_adamw_variant(int variant);
 /* The 8 fp32 scalars the update uses, for parity tests. */

@@ -15,7 +15,7 @@ from paper_2511_14124_b200 import kernels as K  # noqa: E402
 S = int(os.environ.get("CHUNK", "33574912"))  # C2 chunk bytes
 n = S // 2
 reps = int(os.environ.get("REPS", "20"))
-variants = [int(v) for v in os.environ.get("VARIANTS", "0,1,2").split(",")]
+variants = [int(v) for v in os.environ.get("VARIANTS", "0,1,2,3,4,5").split(",")]
 state = torch.zeros(3 * n, dtype=torch.float32, device="cuda")
 state[:n] = torch.randn(n, device="cuda") * 0.02
 grad = (torch.randn(n, device="cuda") * 1e-3).to(torch.bfloat16)
