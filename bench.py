@@ -125,8 +125,8 @@ def run_ours(args):
         nvme_dir = tempfile.mkdtemp(dir=args.nvme_dir)
     else:
         info = build_c2(wd, args.tokens, args.tflops)
-        cfg = {"policy": "tencache"}
-        nvme_dir = wd
+        cfg = {"policy": args.policy}
+        nvme_dir = wd if args.policy in ("tencache", "tencache+opt") else tempfile.mkdtemp(dir=args.nvme_dir)
     dec_bytes, dec_h2d, dec_d2h, rep = decision_bytes_per_iter(info["trace"], info["machine"], cfg)
     t0 = time.perf_counter()
     eng = Engine(info["trace"], info["machine"], cfg, nvme_dir=nvme_dir, direct_io=args.direct_io)
@@ -416,6 +416,9 @@ def main():
     ap.add_argument("--no-hoist", action="store_true", help="run optimizer updates in place (after backward)")
     ap.add_argument("--no-prestage", action="store_true", help="no staging of optimizer states ahead of updates")
     ap.add_argument("--config", default="c2", choices=["c2", "c4"])
+    ap.add_argument("--policy", default="tencache",
+                    choices=["tencache", "tencache+opt", "zero-infinity", "l2l", "no-offload"],
+                    help="C2 cache policy on the same executor (the paper's baselines for comparison)")
     ap.add_argument("--nvme-dir", default="/tmp", help="directory of the NVMe tier file (c4)")
     ap.add_argument("--direct-io", action="store_true", help="O_DIRECT NVMe tier I/O")
     args = ap.parse_args()

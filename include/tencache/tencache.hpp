@@ -489,6 +489,9 @@ class IPolicy {
   // contents for buffer-assignment parity and the CUDA executor); nullptr for
   // the comparison policies.
   virtual const SchedulerState* scheduler_state() const { return nullptr; }
+  // b200 addition: the tier each tensor occupies after init() (before any
+  // request), so an executor can materialise the initial placement.
+  virtual std::optional<Tier> initial_tier(TensorId id) const { return std::nullopt; }
 };
 
 std::unique_ptr<IPolicy> make_policy(const ExecutionTrace& trace, const MachineConfig& machine,

@@ -141,6 +141,7 @@ class TenCache final : public IPolicy {
   std::vector<Req> on_iteration_end() override { return restore_final_locations(state_, RestoreScope::OptimizerStates); }
   void reset_iteration() override { tencache::reset_iteration(state_); }
   const SchedulerState* scheduler_state() const override { return &state_; }
+  std::optional<Tier> initial_tier(TensorId id) const override { return state_.final_loc(id); }
 
  private:
   // Every forward/backward step must be servable from the planned GPU slots.
@@ -216,6 +217,11 @@ class ZeroInfinity final : public IPolicy {
   std::vector<Req> on_param_restore_point() override { return {}; }
   std::vector<Req> on_iteration_end() override { return {}; }
   void reset_iteration() override { st_ = make_zero_infinity_state(trace_, machine_, cfg_.zero_lookahead_k); }
+  std::optional<Tier> initial_tier(TensorId id) const override {
+    if (trace_.tensor(id).kind == TensorKind::OptStateFP32) return Tier::Nvme;  // states all in NVMe
+    if (st_.fits_gpu) return Tier::Gpu;
+    return st_.param_home.at(id);
+  }
 
  private:
   const ExecutionTrace& trace_;
@@ -239,6 +245,7 @@ class LayerToLayer final : public IPolicy {
   std::vector<Req> on_param_restore_point() override { return {}; }
   std::vector<Req> on_iteration_end() override { return {}; }
   void reset_iteration() override { st_ = make_l2l_state(trace_); }
+  std::optional<Tier> initial_tier(TensorId) const override { return Tier::Cpu; }
 
  private:
   const ExecutionTrace& trace_;
@@ -259,6 +266,7 @@ class NoOffload final : public IPolicy {
   std::vector<Req> on_param_restore_point() override { return {}; }
   std::vector<Req> on_iteration_end() override { return {}; }
   void reset_iteration() override {}
+  std::optional<Tier> initial_tier(TensorId) const override { return Tier::Gpu; }
 
  private:
   const ExecutionTrace& trace_;

@@ -113,11 +113,8 @@ Executor::Executor(const std::string& trace_path, const std::string& machine_pat
   trace_ = load_trace(trace_path);
   machine_ = machine_from(machine_path.c_str());
   cfg_ = parse_run_config(cfg_json.c_str());
-  if (cfg_.policy != PolicyKind::TenCache && cfg_.policy != PolicyKind::TenCachePlusOpt)
-    throw ConfigError("the CUDA executor runs the TenCache policies (tencache, tencache+opt)");
   policy_ = make_policy(trace_, machine_, cfg_);
   policy_->init();
-  const SchedulerState& st = *policy_->scheduler_state();
 
   // tensor table
   recs_.reserve(trace_.tensors.size());
@@ -139,19 +136,28 @@ Executor::Executor(const std::string& trace_path, const std::string& machine_pat
     p.partner = index_.at(sid);
   }
 
-  // physical pools: logical counts from the policy's pools + spares
+  // physical pools: the peak number of tensors of each (tier, class) holding
+  // a slot over the policy's decisions (dry run), at least the policy's own
+  // logical pool sizes, plus spare slots per class.
   const int gspare = std::max(opts.gpu_spare_slots, 1), hspare = std::max(opts.host_spare_slots, 1);
-  std::map<std::uint64_t, std::uint32_t> gcount, hcount, ocount;
-  for (const Chunk& c : st.gpu_pool.chunks()) ++gcount[c.size];
-  for (const Chunk& c : st.cpu_pool.chunks()) ++hcount[c.size];
-  for (const Chunk& c : st.cpu_opt_pool.chunks()) ++ocount[c.size];
+  std::map<std::pair<int, std::uint64_t>, std::uint32_t> need = simulate_occupancy();
+  if (const SchedulerState* st = policy_->scheduler_state()) {
+    std::map<std::pair<int, std::uint64_t>, std::uint32_t> logical;
+    for (const Chunk& c : st->gpu_pool.chunks()) ++logical[{0, c.size}];
+    for (const Chunk& c : st->cpu_pool.chunks()) ++logical[{1, c.size}];
+    for (const Chunk& c : st->cpu_opt_pool.chunks()) ++logical[{2, c.size}];
+    for (const auto& [k, v] : logical) need[k] = std::max(need[k], v);
+  }
   std::map<std::uint64_t, bool> pclass, sclass;
   for (const auto& r : recs_) (r.is_state ? sclass : pclass)[r.bytes] = true;
   for (const auto& [size, _] : pclass) {
-    gpu_.plan(size, gcount[size] + gspare);
-    host_param_.plan(size, hcount[size] + hspare);
+    gpu_.plan(size, need[{0, size}] + gspare);
+    host_param_.plan(size, need[{1, size}] + hspare);
   }
-  for (const auto& [size, _] : sclass) host_opt_.plan(size, ocount[size] + hspare + 1);  // +1 transient
+  for (const auto& [size, _] : sclass) {
+    if (need[{0, size}]) gpu_.plan(size, need[{0, size}] + 1);  // GPU-resident states (no offload)
+    host_opt_.plan(size, need[{2, size}] + hspare + 1);          // +1 transient
+  }
   gpu_.allocate(true, device_);
   host_param_.allocate(false, device_);
   host_opt_.allocate(false, device_);
@@ -235,7 +241,7 @@ Executor::Executor(const std::string& trace_path, const std::string& machine_pat
 
   // initial physical placement = the policy's placement
   for (auto& r : recs_) {
-    const Tier t = st.final_loc(r.id);
+    const Tier t = policy_->initial_tier(r.id).value_or(Tier::Cpu);
     if (t == Tier::Gpu) {
       r.tier = PTier::Gpu;
       r.slot = take_slot(PTier::Gpu, r.bytes, index_of(r.id));
@@ -282,6 +288,64 @@ Executor::~Executor() {
       if (p) cudaFree(p);
     if (z3_->comm) nccl().CommDestroy(z3_->comm);
   }
+}
+
+// Dry run of one iteration of decisions on a fresh policy: the peak number
+// of tensors per (tier, size) that must hold a slot at once. Tier keys: 0 GPU,
+// 1 host parameter cache, 2 host optimizer-state cache. A retained source
+// (src_retains) keeps its slot; a destination that already has the bytes
+// (dst_has_copy) takes none.
+std::map<std::pair<int, std::uint64_t>, std::uint32_t> Executor::simulate_occupancy() const {
+  std::unique_ptr<IPolicy> pol = make_policy(trace_, machine_, cfg_);
+  pol->init();
+  std::unordered_map<TensorId, std::set<Tier>> where;
+  std::unordered_map<TensorId, std::pair<std::uint64_t, bool>> info;  // size, is_state
+  std::map<std::pair<int, std::uint64_t>, std::int64_t> cur;
+  std::map<std::pair<int, std::uint64_t>, std::uint32_t> peak;
+  auto key = [&](TensorId id, Tier t) -> std::pair<int, std::uint64_t> {
+    const auto& [size, st] = info.at(id);
+    return {t == Tier::Gpu ? 0 : (st ? 2 : 1), size};
+  };
+  auto add = [&](TensorId id, Tier t, int d) {
+    if (t == Tier::Nvme) return;
+    auto k = key(id, t);
+    cur[k] += d;
+    if (cur[k] > 0) peak[k] = std::max<std::uint32_t>(peak[k], static_cast<std::uint32_t>(cur[k]));
+  };
+  for (const auto& t : trace_.tensors) {
+    info[t.id] = {t.size_bytes, t.kind == TensorKind::OptStateFP32};
+    const Tier tier = pol->initial_tier(t.id).value_or(Tier::Cpu);
+    where[t.id] = {tier};
+    add(t.id, tier, +1);
+  }
+  auto apply_reqs = [&](const std::vector<TransferRequest>& reqs) {
+    for (const TransferRequest& r : reqs) {
+      auto& w = where[r.tensor_id];
+      if (!r.src_retains && w.erase(r.src)) add(r.tensor_id, r.src, -1);
+      if (w.insert(r.dst).second) add(r.tensor_id, r.dst, +1);
+    }
+  };
+  std::size_t first_opt = trace_.steps.size();
+  for (std::size_t i = 0; i < trace_.steps.size(); ++i)
+    if (trace_.steps[i].phase == Phase::OptimizerUpdate) {
+      first_opt = i;
+      break;
+    }
+  for (int it = 0; it < 2; ++it) {
+    bool restored = false;
+    for (std::size_t i = 0; i < trace_.steps.size(); ++i) {
+      if (cfg_.restore_overlap && i == first_opt && !restored) {
+        restored = true;
+        apply_reqs(pol->on_param_restore_point());
+      }
+      apply_reqs(pol->on_step_begin(trace_.steps[i]));
+      apply_reqs(pol->on_step_end(trace_.steps[i]));
+    }
+    if (!restored) apply_reqs(pol->on_param_restore_point());
+    apply_reqs(pol->on_iteration_end());
+    pol->reset_iteration();
+  }
+  return peak;
 }
 
 std::int32_t Executor::index_of(TensorId id) const {
@@ -467,7 +531,23 @@ void Executor::apply(const Req& r) {
   const std::int32_t xi = index_of(x.id);
   cudaEvent_t done = nullptr;
 
-  if (r.src == Tier::Gpu && r.dst == Tier::Cpu) {  // evict / restore, D2H
+  if (r.src == Tier::Gpu && r.dst == Tier::Cpu && r.instant) {  // drop: the retained home copy is primary again
+    if (!x.has_home) throw DeviceError(TC_EINTERNAL, "instant GPU->CPU drop without a retained home copy");
+    Slot& g = slot_of(x);
+    Slot& h = pool(x.home_tier).cls(x.bytes).slots[x.home_slot];
+    if (!x.home_valid) {  // updated on the GPU since the fetch: write the bytes home first
+      wait_for_read(d2h_, g.sync);
+      wait_for_write(d2h_, h.sync);
+      done = copy(d2h_, h.ptr, g.ptr, x.bytes, false);
+      g.sync.readers.push_back(done);
+      h.sync = SlotSync{done, {}};
+      stats_.writeback_bytes += x.bytes;
+    }
+    free_slot(PTier::Gpu, x.bytes, x.slot);
+    x.tier = x.home_tier;
+    x.slot = x.home_slot;
+    x.has_home = x.home_valid = false;
+  } else if (r.src == Tier::Gpu && r.dst == Tier::Cpu) {  // evict / restore, D2H
     Slot& g = slot_of(x);
     const PTier ht = host_tier(x);
     const std::uint32_t hs = take_slot(ht, x.bytes, xi);
@@ -483,7 +563,6 @@ void Executor::apply(const Req& r) {
     x.slot = hs;
     stats_.d2h_bytes += x.bytes;
   } else if (r.src == Tier::Cpu && r.dst == Tier::Gpu) {  // prefetch / restore, H2D
-    if (r.src_retains) throw ConfigError("executor: host-retaining fetches (comparison policies) are not executed");
     Slot& h = slot_of(x);
     const std::uint32_t gs = take_slot(PTier::Gpu, x.bytes, xi);
     Slot& g = gpu_.cls(x.bytes).slots[gs];
@@ -493,7 +572,14 @@ void Executor::apply(const Req& r) {
     h.sync.readers.push_back(done);
     g.sync.writer = done;
     g.sync.readers.clear();
-    free_slot(x.tier, x.bytes, x.slot);
+    if (r.src_retains) {  // comparison policies: the home copy stays valid and allocated
+      x.has_home = true;
+      x.home_valid = true;
+      x.home_tier = x.tier;
+      x.home_slot = x.slot;
+    } else {
+      free_slot(x.tier, x.bytes, x.slot);
+    }
     x.tier = PTier::Gpu;
     x.slot = gs;
     x.arrival = done;
@@ -532,13 +618,15 @@ void Executor::apply(const Req& r) {
       nvme_read(x, h.ptr);
       h.sync = SlotSync{};
     }
+    if (!r.src_retains) x.nvme_valid = false;
     x.tier = ht;
     x.slot = hs;
   } else if (r.src == Tier::Cpu && r.dst == Tier::Nvme) {  // spill / state write-back
     Slot& h = slot_of(x);
     if (!r.instant || !x.nvme_valid) {
       if (io_) {
-        nvme_write_async(x, h.ptr, h.sync);  // later writers of the slot wait on the job
+        const std::uint64_t k = nvme_write_async(x, h.ptr, h.sync);  // later writers of the slot wait on the job
+        if (r.blocking) barrier_io_ = std::max(barrier_io_, k);
       } else {
         host_wait_all(h.sync);
         nvme_write(x, h.ptr);
@@ -560,6 +648,8 @@ void Executor::apply(const Req& r) {
 void Executor::wait_barriers(cudaStream_t cs) {
   for (cudaEvent_t e : barriers_) TCB_CK(cudaStreamWaitEvent(cs, e, 0));
   barriers_.clear();
+  if (barrier_io_ && io_) io_->stream_wait(cs, barrier_io_);
+  barrier_io_ = 0;
 }
 
 void Executor::param_step(const TraceStep& step, std::size_t, cudaStream_t cs) {
@@ -630,15 +720,23 @@ void Executor::refill_stages(std::size_t want_staged) {
 }
 
 void Executor::optimizer_work(TensorRec& s, TensorRec& p) {
-  if (s.tier != PTier::HostOpt) throw DeviceError(TC_EINTERNAL, "optimizer state not in host memory at its update");
+  const bool state_on_gpu = s.tier == PTier::Gpu;  // no-offload posture: update in place in HBM
+  if (!state_on_gpu && s.tier != PTier::HostOpt)
+    throw DeviceError(TC_EINTERNAL, "optimizer state not in host memory at its update");
   const std::uint64_t n = p.bytes / 2;
-  Slot& h = slot_of(s);
-  auto it = staged_.find(index_of(s.id));
-  const std::size_t b = it != staged_.end() ? it->second : stage_state(s);
-  staged_.erase(index_of(s.id));
-  std::uint8_t* stg = stage_[b];
-  cudaEvent_t e1 = stage_sync_[b].writer;
-  TCB_CK(cudaStreamWaitEvent(opt_, e1, 0));
+  std::uint8_t* stg;
+  std::size_t b = 0;
+  if (state_on_gpu) {
+    Slot& gs = slot_of(s);
+    stg = gs.ptr;
+    wait_for_write(opt_, gs.sync);
+  } else {
+    auto it = staged_.find(index_of(s.id));
+    b = it != staged_.end() ? it->second : stage_state(s);
+    staged_.erase(index_of(s.id));
+    stg = stage_[b];
+    TCB_CK(cudaStreamWaitEvent(opt_, stage_sync_[b].writer, 0));
+  }
   if (p.grad_ready) TCB_CK(cudaStreamWaitEvent(opt_, p.grad_ready, 0));
   std::uint8_t* pout;
   SlotSync* psync;
@@ -665,18 +763,24 @@ void Executor::optimizer_work(TensorRec& s, TensorRec& p) {
   ++stats_.kernel_launches;
   stats_.adam_elems += n;
   *psync = SlotSync{a1, {}};
-  stage_sync_[b].readers.push_back(a1);
   p.nvme_valid = false;  // any NVMe replica of the parameter is now stale
+  if (p.has_home) p.home_valid = false;
   if (on_gpu) p.arrival = nullptr;
 
-  wait_for_read(d2h_opt_, stage_sync_[b]);
-  wait_for_write(d2h_opt_, h.sync);
-  TCB_CK(cudaStreamWaitEvent(d2h_opt_, a1, 0));
-  cudaEvent_t e3 = copy(d2h_opt_, h.ptr, stg, s.bytes, false);
-  h.sync = SlotSync{e3, {}};
-  stage_sync_[b].readers.push_back(e3);
-  stage_free_.push_back(b);
-  stats_.opt_d2h_bytes += s.bytes;
+  if (state_on_gpu) {
+    slot_of(s).sync = SlotSync{a1, {}};
+  } else {
+    Slot& h = slot_of(s);
+    stage_sync_[b].readers.push_back(a1);
+    wait_for_read(d2h_opt_, stage_sync_[b]);
+    wait_for_write(d2h_opt_, h.sync);
+    TCB_CK(cudaStreamWaitEvent(d2h_opt_, a1, 0));
+    cudaEvent_t e3 = copy(d2h_opt_, h.ptr, stg, s.bytes, false);
+    h.sync = SlotSync{e3, {}};
+    stage_sync_[b].readers.push_back(e3);
+    stage_free_.push_back(b);
+    stats_.opt_d2h_bytes += s.bytes;
+  }
 
   if (!on_gpu) {  // updated-parameter write-back to its home tier (category iii)
     if (p.tier == PTier::Nvme) {
@@ -757,8 +861,7 @@ std::vector<std::size_t> Executor::plan_hoisting(const std::vector<Hook>& hooks)
     if (hooks[k].kind == 1) end_pos[hooks[k].step] = k;
     for (const Req& r : hooks[k].reqs) touched[r.tensor_id].push_back(k);
   }
-  // the state's host residency at iteration start = its placement
-  const SchedulerState& st = *policy_->scheduler_state();
+  // the state's residency at iteration start = the policy's placement
   for (std::size_t j = 0; j < n; ++j) {
     const TraceStep& os = trace_.steps[j];
     if (os.phase != Phase::OptimizerUpdate) continue;
@@ -769,7 +872,8 @@ std::vector<std::size_t> Executor::plan_hoisting(const std::vector<Hook>& hooks)
     auto la = last_access.find(pid);
     if (la == last_access.end()) continue;
     const std::size_t a = la->second;
-    if (st.final_loc(sid) != Tier::Cpu) continue;
+    const Tier home = policy_->initial_tier(sid).value_or(Tier::Nvme);
+    if (home != Tier::Cpu && home != Tier::Gpu) continue;
     bool moved = false;  // any decision moving the state before its update's end
     auto t = touched.find(sid);
     if (t != touched.end())

@@ -121,6 +121,11 @@ struct TensorRec {
   int issued_since_access = 0;     // P7b hit definition
   cudaEvent_t arrival = nullptr;   // last H2D into its GPU slot (for on-time)
   cudaEvent_t grad_ready = nullptr;  // ZeRO-3: reduce-scatter that produced its gradient
+  // A retained home copy (comparison policies fetch with src_retains and drop
+  // instantly): the host slot stays allocated while the GPU copy is primary.
+  bool has_home = false, home_valid = false;
+  PTier home_tier = PTier::HostParam;
+  std::uint32_t home_slot = 0;
 };
 
 // ZeRO-3 exchange state of one rank. Chunk c of layer L holds
@@ -281,6 +286,8 @@ class Executor {
   cudaStream_t compute_owned_ = nullptr;
   EventArena events_;
   std::vector<cudaEvent_t> barriers_;
+  std::uint64_t barrier_io_ = 0;  // NVMe job a blocking request ended with
+  std::map<std::pair<int, std::uint64_t>, std::uint32_t> simulate_occupancy() const;
   std::vector<Copy> copies_;
   std::vector<std::pair<cudaEvent_t, cudaEvent_t>> stalls_;        // (reach, go) on compute
   std::vector<std::pair<cudaEvent_t, cudaEvent_t>> ontime_;        // (reach, arrival)

@@ -142,6 +142,23 @@ def test_random_traces(tmpd, seed):
     assert st["param_accesses"] == rep["param_accesses"] and st["param_hits"] == rep["param_hits"]
 
 
+@pytest.mark.parametrize("pol", ["zero-infinity", "l2l", "no-offload"])
+@pytest.mark.parametrize("k", [0, 1, 2])
+def test_comparison_policies_on_the_executor(tmpd, pol, k):
+    """The paper's baselines run on the same B200 executor (SURVEY.md §8f rank
+    3): host-retaining fetches, instant drops, synchronous NVMe optimizer
+    swaps, GPU-resident optimizer states (no offload)."""
+    if pol != "zero-infinity" and k:
+        pytest.skip("lookahead only applies to zero-infinity")
+    sizes = [4096] * 4 + [8192] * 3
+    gpu = 3 * 8192 if pol != "no-offload" else 10 ** 7
+    tr, m = write_with_states(tmpd, "b", sizes, gpu, 10 ** 6, iters=2)
+    cfg = {"policy": pol, "zero_lookahead_k": k}
+    st = check_engine(tr, m, cfg, iters=2, nvme_dir=tmpd)
+    rep = P.run(tr, m, cfg)
+    assert st["param_accesses"] == rep["param_accesses"] and st["param_hits"] == rep["param_hits"]
+
+
 def test_chunk_trace_c2_mini(tmpd):
     plan = T.plan_chunks("opt-1.3b", world=64, rank=5, chunks_per_layer=2)
     tp = os.path.join(tmpd, "c2mini.jsonl")
