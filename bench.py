@@ -129,7 +129,8 @@ def run_ours(args):
         nvme_dir = wd if args.policy in ("tencache", "tencache+opt") else tempfile.mkdtemp(dir=args.nvme_dir)
     dec_bytes, dec_h2d, dec_d2h, rep = decision_bytes_per_iter(info["trace"], info["machine"], cfg)
     t0 = time.perf_counter()
-    eng = Engine(info["trace"], info["machine"], cfg, nvme_dir=nvme_dir, direct_io=args.direct_io)
+    eng = Engine(info["trace"], info["machine"], cfg, nvme_dir=nvme_dir, direct_io=args.direct_io,
+                 opt_stage_slots=args.stages, gpu_spare_slots=args.gpu_spares)
     eng.seed(0)
     setup_s = time.perf_counter() - t0
     stream = torch.cuda.current_stream()
@@ -206,7 +207,7 @@ def run_ours(args):
                    "chunks": info["params"], "chunk_bytes": info["chunk_bytes"],
                    "gpu_param_chunks": info["gpu_chunks"], "policy": cfg["policy"],
                    "tokens_per_step": args.tokens, "compute": args.compute,
-                   "compute_model_tflops": args.tflops, "l2": "inputs larger than L2 (>15 GB streamed per step)",
+                   "compute_model_tflops": args.tflops, "opt_stages": args.stages, "gpu_spares": args.gpu_spares, "l2": "inputs larger than L2 (>15 GB streamed per step)",
                    "parallelism": "single GPU"},
         "hit_rate": {"exact": rep["hit_rate"], "hits": st["param_hits"] // K, "accesses": st["param_accesses"] // K,
                      "model_clock_hits": rep["param_hits"]},
@@ -416,6 +417,8 @@ def main():
     ap.add_argument("--no-hoist", action="store_true", help="run optimizer updates in place (after backward)")
     ap.add_argument("--no-prestage", action="store_true", help="no staging of optimizer states ahead of updates")
     ap.add_argument("--config", default="c2", choices=["c2", "c4"])
+    ap.add_argument("--stages", type=int, default=12, help="HBM optimizer-state stages")
+    ap.add_argument("--gpu-spares", type=int, default=4, help="spare HBM slots per parameter class")
     ap.add_argument("--policy", default="tencache",
                     choices=["tencache", "tencache+opt", "zero-infinity", "l2l", "no-offload"],
                     help="C2 cache policy on the same executor (the paper's baselines for comparison)")

@@ -235,7 +235,9 @@ Executor::Executor(const std::string& trace_path, const std::string& machine_pat
   h_checksums_.assign(n_accesses_, 0);
   TCB_CK(cudaStreamCreateWithFlags(&h2d_, cudaStreamNonBlocking));
   TCB_CK(cudaStreamCreateWithFlags(&d2h_, cudaStreamNonBlocking));
-  TCB_CK(cudaStreamCreateWithFlags(&opt_, cudaStreamNonBlocking));
+  int lo_prio = 0, hi_prio = 0;  // the fused AdamW gets the highest stream priority
+  TCB_CK(cudaDeviceGetStreamPriorityRange(&lo_prio, &hi_prio));
+  TCB_CK(cudaStreamCreateWithPriority(&opt_, cudaStreamNonBlocking, hi_prio));
   TCB_CK(cudaStreamCreateWithFlags(&h2d_opt_, cudaStreamNonBlocking));
   TCB_CK(cudaStreamCreateWithFlags(&d2h_opt_, cudaStreamNonBlocking));
 
