@@ -207,3 +207,22 @@ def config_c4_rank(workdir: str, world: int = 8, rank: int = 0, iterations: int 
     write_machine(mp, n * S, k * 6 * S + 1, pinned_overrides=links)
     info.update({"trace": tp, "machine": mp, "gpu_chunks": n, "cpu_states": k, "params": n, "chunk_bytes": S})
     return info
+
+
+def config_c3_rank(workdir: str, world: int = 1, rank: int = 0, iterations: int = 1, tokens: int = 16384,
+                   effective_tflops: float = 700.0, links: dict | None = None):
+    """BASELINE configs[2] (Llama-2 7B ZeRO-3, optimizer states offloaded to
+    pinned host memory), one rank's shard: every parameter chunk on the GPU
+    (GPU tier holds the whole shard), every optimizer state in pinned host
+    memory."""
+    import os
+    from . import zero3 as Z
+    lay = Z.shard_layout("llama2-7b", world)
+    tp = os.path.join(workdir, f"c3_w{world}_r{rank}.jsonl")
+    info = Z.write_rank_trace(tp, lay, rank, iterations, tokens, effective_tflops)
+    S, n = lay.chunk_bytes, lay.chunks_per_rank
+    mp = os.path.join(workdir, "c3_machine.json")
+    links = links or {"cpu->gpu": 55.3, "gpu->cpu": 57.0}
+    write_machine(mp, n * S, n * 6 * S + 1, pinned_overrides=links)
+    info.update({"trace": tp, "machine": mp, "gpu_chunks": n, "params": n, "chunk_bytes": S, "layout": lay})
+    return info

@@ -211,3 +211,42 @@ def test_zero3_exchange_world1(tmpd):
             assert np.all(g.reshape(-1)[valid[i] // 2:] == 0), "padding gradient must be zero"
     assert Z.exchanged_bytes(e) > 0
     e.close()
+
+
+def test_captured_model_trace_runs_on_engine(tmpd):
+    """§8f rank 1 end to end on the B200: capture a real (tiny, random-init)
+    transformer's execution order on the GPU, run the engine on the captured
+    chunk trace, check bytes and updates against the oracle."""
+    import torch
+    from paper_2511_14124_b200 import capture as CAP
+
+    class Block(torch.nn.Module):
+        def __init__(self, h):
+            super().__init__()
+            self.ln = torch.nn.LayerNorm(h)
+            self.fc1 = torch.nn.Linear(h, 4 * h)
+            self.fc2 = torch.nn.Linear(4 * h, h)
+
+        def forward(self, x):
+            return x + self.fc2(torch.nn.functional.gelu(self.fc1(self.ln(x))))
+
+    class Tiny(torch.nn.Module):
+        def __init__(self):
+            super().__init__()
+            self.emb = torch.nn.Embedding(2000, 128)
+            self.h = torch.nn.ModuleList([Block(128) for _ in range(6)])
+
+        def forward(self, ids):
+            x = self.emb(ids)
+            for b in self.h:
+                x = b(x)
+            return x
+
+    model = Tiny().cuda()
+    ct = CAP.capture(model, (torch.randint(0, 2000, (4, 32), device="cuda"),), chunk_bytes=65536)
+    tp = CAP.write_trace(ct, os.path.join(tmpd, "cap.jsonl"), iterations=2)
+    n, S = ct.n_chunks, ct.chunk_bytes
+    mp = T.write_machine(os.path.join(tmpd, "m.json"), max(2, n // 2) * S, n * 7 * S)
+    st = check_engine(tp, mp, {"policy": "tencache"}, iters=2)
+    rep = P.run(tp, mp, {"policy": "tencache"})
+    assert st["param_hits"] == rep["param_hits"]
