@@ -243,6 +243,11 @@ int tc_nccl_unique_id(uint8_t out[128]);
  * (ceil). Chunks of one layer are its parameter tensors in id order. */
 int tc_engine_enable_zero3(tc_engine* e, int world, int rank, const uint8_t id[128], const uint64_t* layer_elems,
                            const uint64_t* layer_per, uint32_t n_layers);
+/* Measured event log: for every harvested iteration, one JSONL line per copy
+ * in the reference's event-log schema (engine_internal.hpp:35-47: us, kind,
+ * tensor, src, dst) plus end_us, bytes and iter from CUDA events, and a
+ * "stall" line (wait_us) per compute-stream wait. path "" switches it off. */
+int tc_engine_event_log(tc_engine* e, const char* path);
 /* Bytes all-gathered + reduce-scattered (NCCL payload, all ranks' pieces) so far. */
 uint64_t tc_engine_exchanged_bytes(tc_engine* e);
 

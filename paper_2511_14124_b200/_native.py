@@ -137,6 +137,7 @@ _SIGS = {
     "tc_engine_enable_zero3": ([C.c_void_p, C.c_int, C.c_int, C.c_void_p, C.POINTER(C.c_uint64), C.POINTER(C.c_uint64),
                                 C.c_uint32], C.c_int),
     "tc_engine_exchanged_bytes": ([C.c_void_p], C.c_uint64),
+    "tc_engine_event_log": ([C.c_void_p, C.c_char_p], C.c_int),
     "tc_engine_access_checksums": ([C.c_void_p, C.POINTER(C.c_uint64), C.c_size_t, C.POINTER(C.c_size_t)], C.c_int),
 }
 

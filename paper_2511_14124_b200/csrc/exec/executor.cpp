@@ -1,6 +1,8 @@
 // Per-GPU migration executor (see executor.hpp for the physical layout).
 #include "executor.hpp"
 
+#include <nvtx3/nvToolsExt.h>
+
 #include <fcntl.h>
 #include <unistd.h>
 
@@ -432,6 +434,7 @@ cudaEvent_t Executor::copy(cudaStream_t s, void* dst, const void* src, std::uint
   c.end = events_.get(true);
   c.h2d = h2d;
   c.bytes = n;
+  c.tag = tag_;
   TCB_CK(cudaEventRecord(c.start, s));
   TCB_CK(cudaMemcpyAsync(dst, src, n, h2d ? cudaMemcpyHostToDevice : cudaMemcpyDeviceToHost, s));
   TCB_CK(cudaEventRecord(c.end, s));
@@ -468,6 +471,7 @@ void Executor::nvme_write(TensorRec& r, const void* src) {
 // (SURVEY.md §7 traffic category iii).
 void Executor::ensure_nvme_fresh(TensorRec& r) {
   if (r.nvme_valid) return;
+  tag_ = CopyTag{"writeback", r.id, 0, 2};
   if (r.tier == PTier::Gpu) {
     Slot& g = slot_of(r);
     std::uint8_t* b = bounce_.at(r.bytes);
@@ -532,6 +536,9 @@ void Executor::apply(const Req& r) {
     throw DeviceError(TC_EINTERNAL, "executor/policy desync: tensor " + std::to_string(x.id) + " not in " + to_string(r.src));
   const std::int32_t xi = index_of(x.id);
   cudaEvent_t done = nullptr;
+  static const char* const kKinds[] = {"prefetch", "evict", "restore"};
+  tag_ = CopyTag{kKinds[static_cast<int>(r.kind)], r.tensor_id, static_cast<std::uint8_t>(r.src),
+                 static_cast<std::uint8_t>(r.dst)};
 
   if (r.src == Tier::Gpu && r.dst == Tier::Cpu && r.instant) {  // drop: the retained home copy is primary again
     if (!x.has_home) throw DeviceError(TC_EINTERNAL, "instant GPU->CPU drop without a retained home copy");
@@ -664,7 +671,7 @@ void Executor::param_step(const TraceStep& step, std::size_t, cudaStream_t cs) {
   }
   wait_barriers(cs);
   TCB_CK(cudaEventRecord(go, cs));
-  stalls_.emplace_back(reach, go);
+  stalls_.push_back(Stall{reach, go, step.tensor_ids.front()});
   for (TensorId id : step.tensor_ids) {
     TensorRec& x = rec(id);
     ++stats_.param_accesses;
@@ -703,6 +710,7 @@ std::size_t Executor::stage_state(TensorRec& s) {
   const std::size_t b = stage_free_.front();
   stage_free_.pop_front();
   Slot& h = slot_of(s);
+  tag_ = CopyTag{"opt_load", s.id, 1, 0};
   wait_for_write(h2d_opt_, stage_sync_[b]);
   wait_for_read(h2d_opt_, h.sync);
   cudaEvent_t e1 = copy(h2d_opt_, stage_[b], h.ptr, s.bytes, true);
@@ -777,6 +785,7 @@ void Executor::optimizer_work(TensorRec& s, TensorRec& p) {
     wait_for_read(d2h_opt_, stage_sync_[b]);
     wait_for_write(d2h_opt_, h.sync);
     TCB_CK(cudaStreamWaitEvent(d2h_opt_, a1, 0));
+    tag_ = CopyTag{"opt_store", s.id, 0, 1};
     cudaEvent_t e3 = copy(d2h_opt_, h.ptr, stg, s.bytes, false);
     h.sync = SlotSync{e3, {}};
     stage_sync_[b].readers.push_back(e3);
@@ -785,6 +794,7 @@ void Executor::optimizer_work(TensorRec& s, TensorRec& p) {
   }
 
   if (!on_gpu) {  // updated-parameter write-back to its home tier (category iii)
+    tag_ = CopyTag{"writeback", p.id, 0, static_cast<std::uint8_t>(p.tier == PTier::Nvme ? 2 : 1)};
     if (p.tier == PTier::Nvme) {
       std::uint8_t* bb = bounce_.at(p.bytes);
       SlotSync& bs = bounce_sync_[p.bytes];
@@ -923,7 +933,9 @@ void Executor::iteration(const StepOptions& so, cudaStream_t compute) {
   events_.next_generation();
   cks_base_ = d_checksums_ + (events_.generation() % 2) * std::max<std::size_t>(n_accesses_, 1);
   TCB_CK(cudaMemsetAsync(cks_base_, 0, std::max<std::size_t>(n_accesses_, 1) * sizeof(std::uint64_t), compute));
+  nvtxRangePushA("tencache.decide");
   const std::vector<Hook> hooks = decide_iteration();
+  nvtxRangePop();
   const std::vector<std::size_t> hoist = plan_hoisting(hooks);
   const std::size_t n = trace_.steps.size();
   std::vector<std::vector<std::size_t>> after(n);
@@ -951,6 +963,8 @@ void Executor::iteration(const StepOptions& so, cudaStream_t compute) {
         mark();
         prev = step.phase;
       }
+      nvtxRangePushA(step.phase == Phase::Forward ? "tencache.fwd" : step.phase == Phase::Backward ? "tencache.bwd"
+                                                                                                   : "tencache.opt");
       execute(h.reqs);
       if (step.phase == Phase::OptimizerUpdate) {
         if (hoist[h.step] == n) {  // in place: waits for the state's decisions
@@ -967,6 +981,7 @@ void Executor::iteration(const StepOptions& so, cudaStream_t compute) {
           if (so_.prestage) refill_stages(prestage_lookahead_);
         }
       }
+      nvtxRangePop();
     } else {
       execute(h.reqs);
     }
@@ -1030,9 +1045,28 @@ void Executor::harvest_front() {
     TCB_CK(cudaEventElapsedTime(&ms, c.start, c.end));
     (c.h2d ? stats_.h2d_busy_ms : stats_.d2h_busy_ms) += ms;
   }
-  for (const auto& [reach, go] : rec.stalls) {
-    TCB_CK(cudaEventElapsedTime(&ms, reach, go));
+  for (const Stall& st : rec.stalls) {
+    TCB_CK(cudaEventElapsedTime(&ms, st.reach, st.go));
     stats_.stall_ms += ms;
+  }
+  if (event_log_ && !rec.marks.empty()) {  // measured timeline in the reference's event-log schema
+    static const char* const kTiers[] = {"gpu", "cpu", "nvme"};
+    float t0 = 0, t1 = 0;
+    for (const Copy& c : rec.copies) {
+      TCB_CK(cudaEventElapsedTime(&t0, rec.marks.front(), c.start));
+      TCB_CK(cudaEventElapsedTime(&t1, rec.marks.front(), c.end));
+      *event_log_ << "{\"bytes\":" << c.bytes << ",\"dst\":\"" << kTiers[c.tag.dst] << "\",\"end_us\":" << t1 * 1e3
+                  << ",\"iter\":" << rec.gen << ",\"kind\":\"" << c.tag.kind << "\",\"src\":\"" << kTiers[c.tag.src]
+                  << "\",\"tensor\":" << c.tag.tensor << ",\"us\":" << t0 * 1e3 << "}\n";
+    }
+    for (const Stall& st : rec.stalls) {
+      TCB_CK(cudaEventElapsedTime(&ms, st.reach, st.go));
+      if (ms <= 0.0005f) continue;
+      TCB_CK(cudaEventElapsedTime(&t0, rec.marks.front(), st.reach));
+      *event_log_ << "{\"dst\":\"gpu\",\"iter\":" << rec.gen << ",\"kind\":\"stall\",\"src\":\"gpu\",\"tensor\":"
+                  << st.tensor << ",\"us\":" << t0 * 1e3 << ",\"wait_us\":" << ms * 1e3 << "}\n";
+    }
+    event_log_->flush();
   }
   for (const auto& [reach, arrival] : rec.ontime) {
     TCB_CK(cudaEventElapsedTime(&ms, reach, arrival));
@@ -1177,6 +1211,16 @@ void Executor::zero3_access(TensorRec& x, bool backward, cudaStream_t cs) {
   cudaEvent_t e = events_.get(false);
   TCB_CK(cudaEventRecord(e, cs));
   x.grad_ready = e;
+}
+
+void Executor::set_event_log(const std::string& path) {
+  drain();
+  if (path.empty()) {
+    event_log_.reset();
+    return;
+  }
+  event_log_ = std::make_unique<std::ofstream>(path);
+  if (!*event_log_) throw DeviceError(TC_EIO, "cannot open event log " + path);
 }
 
 void Executor::sync() {
@@ -1413,6 +1457,14 @@ int tc_engine_enable_zero3(tc_engine* e, int world, int rank, const uint8_t id[1
 }
 
 uint64_t tc_engine_exchanged_bytes(tc_engine* e) { return e ? e->ex->exchanged_bytes() : 0; }
+
+int tc_engine_event_log(tc_engine* e, const char* path) {
+  TC_GUARD({
+    if (!e) return set_error(TC_EARG, "null engine");
+    e->ex->set_event_log(path ? path : "");
+    return TC_OK;
+  })
+}
 
 int tc_engine_stats_get(tc_engine* e, tc_engine_stats* out) {
   TC_GUARD({

@@ -26,6 +26,7 @@
 #include <map>
 #include <memory>
 #include <string>
+#include <fstream>
 #include <unordered_map>
 #include <vector>
 
@@ -185,11 +186,22 @@ class Executor {
 
  private:
   using Req = tencache::TransferRequest;
+  struct CopyTag {  // what a copy is, for the measured event log
+    const char* kind = "";
+    tencache::TensorId tensor = 0;
+    std::uint8_t src = 0, dst = 0;
+  };
   struct Copy {
     cudaEvent_t start = nullptr, end = nullptr;
     bool h2d = true;
     std::uint64_t bytes = 0;
+    CopyTag tag;
   };
+  struct Stall {
+    cudaEvent_t reach = nullptr, go = nullptr;
+    tencache::TensorId tensor = 0;
+  };
+  CopyTag tag_;
 
   TensorRec& rec(tencache::TensorId id);
   std::int32_t index_of(tencache::TensorId id) const;
@@ -231,7 +243,8 @@ class Executor {
   struct IterRecord {
     std::uint64_t gen = 0;
     std::vector<Copy> copies;
-    std::vector<std::pair<cudaEvent_t, cudaEvent_t>> stalls, ontime, adam;
+    std::vector<Stall> stalls;
+    std::vector<std::pair<cudaEvent_t, cudaEvent_t>> ontime, adam;
     std::vector<cudaEvent_t> marks, fences;
     std::size_t cks_buf = 0;
     std::uint64_t io_seq = 0;  // last NVMe job submitted in the iteration
@@ -289,10 +302,14 @@ class Executor {
   std::uint64_t barrier_io_ = 0;  // NVMe job a blocking request ended with
   std::map<std::pair<int, std::uint64_t>, std::uint32_t> simulate_occupancy() const;
   std::vector<Copy> copies_;
-  std::vector<std::pair<cudaEvent_t, cudaEvent_t>> stalls_;        // (reach, go) on compute
+  std::vector<Stall> stalls_;                                      // (reach, go) on compute
   std::vector<std::pair<cudaEvent_t, cudaEvent_t>> ontime_;        // (reach, arrival)
   std::vector<std::pair<cudaEvent_t, cudaEvent_t>> adam_;          // kernel start/end
   std::int64_t adam_step_ = 0;
+  std::unique_ptr<std::ofstream> event_log_;  // measured per-copy JSONL (reference event-log schema + timings)
+ public:
+  void set_event_log(const std::string& path);
+ private:
   std::unique_ptr<Zero3> z3_;
   std::vector<double> phase_ms_;
   StepOptions so_;

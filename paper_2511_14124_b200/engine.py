@@ -74,6 +74,10 @@ class Engine:
         N.check(N.lib().tc_engine_phase_ms(self._h, out, 8, C.byref(n)))
         return list(out[: n.value])
 
+    def event_log(self, path):
+        """Measured per-copy timeline (JSONL, reference event-log schema + timings); None/'' = off."""
+        N.check(N.lib().tc_engine_event_log(self._h, N.b(path or "")))
+
     def reset_stats(self):
         N.check(N.lib().tc_engine_stats_reset(self._h))
 

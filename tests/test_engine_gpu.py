@@ -250,3 +250,28 @@ def test_captured_model_trace_runs_on_engine(tmpd):
     st = check_engine(tp, mp, {"policy": "tencache"}, iters=2)
     rep = P.run(tp, mp, {"policy": "tencache"})
     assert st["param_hits"] == rep["param_hits"]
+
+
+def test_measured_event_log(tmpd):
+    import json
+    tr, m = write_with_states(tmpd, "ev", [4096] * 6, 3 * 4096, 3 * 4096 + 6 * 6 * 4096, iters=2)
+    e = Engine(tr, m, {"policy": "tencache"})
+    e.seed(0)
+    lp = os.path.join(tmpd, "ev.jsonl")
+    e.event_log(lp)
+    e.iteration(**HP)
+    e.iteration(**HP)
+    e.sync()
+    lines = [json.loads(x) for x in open(lp)]
+    kinds = {x["kind"] for x in lines}
+    assert {"prefetch", "evict", "opt_load", "opt_store"} <= kinds
+    for x in lines:
+        if "end_us" in x:
+            assert x["end_us"] >= x["us"] >= 0
+    # the decision copies of one iteration are exactly the model clock's non-instant requests
+    _, ev = P.run(tr, m, {"policy": "tencache"}, events=True)
+    model = [json.loads(x) for x in ev if json.loads(x)["kind"] in ("prefetch", "evict", "restore")]
+    real = [x for x in lines if x["kind"] in ("prefetch", "evict", "restore")]
+    assert sorted((x["tensor"], x["src"], x["dst"]) for x in real) == \
+        sorted((x["tensor"], x["src"], x["dst"]) for x in model)
+    e.close()
