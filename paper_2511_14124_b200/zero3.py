@@ -100,6 +100,7 @@ def enable(engine, layout: ShardLayout, rank: int, world: int, group=None):
     import ctypes as C
 
     from . import _native as N
+    os.environ.setdefault("NCCL_DEBUG", "WARN")  # keep NCCL's version banner off stdout
     idbuf = (C.c_uint8 * 128)()
     if rank == 0:
         N.check(N.lib().tc_nccl_unique_id(idbuf))
