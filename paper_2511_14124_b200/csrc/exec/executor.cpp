@@ -56,35 +56,51 @@ void EventArena::recycle_upto(std::uint64_t gen) {
 void EventArena::recycle_all() { recycle_upto(~0ull); }
 
 // -------------------------------------------------------------- SlotPool
+// One region per tier carved in ascending class order (bufpool.cpp:47-66).
+// Host regions are pinned in pieces of at most 16 GiB (whole slots each): a
+// single ~80 GB cudaHostAlloc is fragile on VMs, slots never straddle pieces.
 void SlotPool::allocate(bool device, int dev) {
   device_ = device;
   bytes_ = 0;
   for (const auto& [size, n] : want_) bytes_ += size * n;
   if (bytes_ == 0) return;
-  if (device)
-    TCB_CK(cudaMalloc(&base_, bytes_));
-  else
-    TCB_CK(cudaHostAlloc(reinterpret_cast<void**>(&base_), bytes_, cudaHostAllocPortable));
-  std::uint64_t off = 0;
-  for (const auto& [size, n] : want_) {  // carved like BufferPool::build: ascending class, then index
-    SlotClass& c = classes_[size];
-    c.size = size;
-    c.slots.resize(n);
-    for (std::uint32_t i = 0; i < n; ++i) {
-      c.slots[i].ptr = base_ + off;
-      off += size;
-      c.free_fifo.push_back(i);
+  constexpr std::uint64_t kRegion = 16ull << 30;
+  std::vector<std::pair<std::uint64_t, std::uint32_t>> slots;  // (size, class) in carving order
+  for (const auto& [size, n] : want_)
+    for (std::uint32_t i = 0; i < n; ++i) slots.emplace_back(size, i);
+  std::size_t k = 0;
+  while (k < slots.size()) {
+    std::uint64_t piece = 0;
+    std::size_t end = k;
+    while (end < slots.size() && (piece == 0 || piece + slots[end].first <= kRegion || device)) piece += slots[end++].first;
+    std::uint8_t* base = nullptr;
+    if (device)
+      TCB_CK(cudaMalloc(&base, piece));
+    else
+      TCB_CK(cudaHostAlloc(reinterpret_cast<void**>(&base), piece, cudaHostAllocPortable));
+    regions_.push_back(base);
+    std::uint64_t off = 0;
+    for (; k < end; ++k) {
+      SlotClass& c = classes_[slots[k].first];
+      c.size = slots[k].first;
+      Slot s;
+      s.ptr = base + off;
+      off += slots[k].first;
+      c.free_fifo.push_back(static_cast<std::uint32_t>(c.slots.size()));
+      c.slots.push_back(s);
     }
   }
+  (void)dev;
 }
 
 void SlotPool::release_memory() {
-  if (base_ == nullptr) return;
-  if (device_)
-    cudaFree(base_);
-  else
-    cudaFreeHost(base_);
-  base_ = nullptr;
+  for (std::uint8_t* r : regions_) {
+    if (device_)
+      cudaFree(r);
+    else
+      cudaFreeHost(r);
+  }
+  regions_.clear();
 }
 
 SlotClass& SlotPool::cls(std::uint64_t size) {
@@ -128,6 +144,9 @@ Executor::Executor(const std::string& trace_path, const std::string& machine_pat
     r.is_state = t.kind == TensorKind::OptStateFP32;
     recs_.push_back(r);
   }
+  for (const TraceStep& st : trace_.steps)  // decisions key the update on the first id (scheduler.cpp:321)
+    if (st.phase == Phase::OptimizerUpdate && trace_.tensor(st.tensor_ids.front()).kind != TensorKind::OptStateFP32)
+      throw ConfigError("executor: optimizer step " + std::to_string(st.step_index) + " must list its state first");
   for (const auto& [sid, pid] : trace_.optimizer_pairs()) {
     if (pid == 0) continue;
     TensorRec& s = rec(sid);

@@ -104,7 +104,7 @@ class SlotPool {
  private:
   std::map<std::uint64_t, std::uint32_t> want_;
   std::map<std::uint64_t, SlotClass> classes_;
-  std::uint8_t* base_ = nullptr;
+  std::vector<std::uint8_t*> regions_;  // contiguous carving, split into <= kRegion pieces for pinning
   bool device_ = false;
   std::uint64_t bytes_ = 0;
 };

@@ -275,3 +275,19 @@ def test_measured_event_log(tmpd):
     assert sorted((x["tensor"], x["src"], x["dst"]) for x in real) == \
         sorted((x["tensor"], x["src"], x["dst"]) for x in model)
     e.close()
+
+
+def test_tied_weight_reuse_and_duplicate_access(tmpd):
+    """A parameter used twice per pass (tied embedding: layer order 0,1,2,3,0)
+    and a step listing one id twice: checksums per access, the update after
+    the LAST access (hoisting), hits == model clock."""
+    p = [(1, 4096, "p16", 0), (2, 4096, "p16", 1), (3, 4096, "p16", 2), (4, 4096, "p16", 3)]
+    steps = [("f", [1], 1.0), ("f", [2, 2], 1.0), ("f", [3], 1.0), ("f", [4], 1.0), ("f", [1], 1.0),
+             ("b", [1], 2.0), ("b", [4], 2.0), ("b", [3], 2.0), ("b", [2, 2], 2.0), ("b", [1], 2.0)]
+    st, opt = cases.with_states(p)
+    tr = cases.write_trace(os.path.join(tmpd, "tied.jsonl"), p + st, steps + opt, 3)
+    m = cases.write_machine(os.path.join(tmpd, "tied_m.json"), 2 * 4096, 10 ** 6)
+    for pol in ("tencache", "tencache+opt"):
+        stt = check_engine(tr, m, {"policy": pol}, iters=3)
+        rep = P.run(tr, m, {"policy": pol})
+        assert stt["param_hits"] == rep["param_hits"]
