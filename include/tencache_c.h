@@ -83,6 +83,11 @@ int tc_run(const char* trace_path, const char* machine_path, const char* cfg_jso
  * as JSON (same schema as the oracle's golden streams). */
 int tc_decisions(const char* trace_path, const char* machine_path, const char* cfg_json, const char* out_path,
                  int with_pools);
+/* sweep (engine.hpp:85-92, engine.cpp:334-384): one SimReport per value of
+ * axis ("batch_scale" | "gpu_capacity" | "cpu_capacity" | "pinned"), in value
+ * order, on `threads` threads; a JSON array of reports to out_path. */
+int tc_sweep(const char* trace_path, const char* machine_path, const char* cfg_json, const char* axis,
+             const double* values, uint32_t n, uint32_t threads, const char* out_path);
 /* synthesize_transformer_trace + save_trace (trace.hpp:76-87). */
 int tc_synthesize(uint32_t layers, uint32_t tensors_per_layer, const uint64_t* sizes, int nsizes,
                   double compute_us_per_byte, uint64_t seed, uint32_t iterations, double opt_us_per_byte,

@@ -97,6 +97,8 @@ _SIGS = {
     "tc_decisions": ([C.c_char_p, C.c_char_p, C.c_char_p, C.c_char_p, C.c_int], C.c_int),
     "tc_synthesize": ([C.c_uint32, C.c_uint32, C.POINTER(C.c_uint64), C.c_int, C.c_double, C.c_uint64, C.c_uint32,
                        C.c_double, C.c_int, C.c_char_p], C.c_int),
+    "tc_sweep": ([C.c_char_p, C.c_char_p, C.c_char_p, C.c_char_p, C.POINTER(C.c_double), C.c_uint32, C.c_uint32,
+                  C.c_char_p], C.c_int),
     "tc_trace_roundtrip": ([C.c_char_p, C.c_char_p], C.c_int),
     "tc_transfer_time": ([C.c_char_p, C.c_int, C.c_int, C.c_uint64, C.c_char_p, C.c_size_t], C.c_int),
     "tc_time_decisions": ([C.c_char_p, C.c_char_p, C.c_char_p, C.c_int, C.POINTER(C.c_double),

@@ -316,6 +316,21 @@ int tc_decisions(const char* trace_path, const char* machine_path, const char* c
   })
 }
 
+int tc_sweep(const char* trace_path, const char* machine_path, const char* cfg_json, const char* axis,
+             const double* values, uint32_t n, uint32_t threads, const char* out_path) {
+  TC_GUARD({
+    const ExecutionTrace trace = load_trace(trace_path);
+    const MachineConfig m = machine_from(machine_path);
+    const RunConfig c = parse_run_config(cfg_json);
+    const std::vector<SimReport> reps =
+        sweep(trace, m, c, sweep_axis_from_string(axis), std::vector<double>(values, values + n), threads);
+    json arr = json::array();
+    for (const SimReport& r : reps) arr.push_back(report_json(r));
+    std::ofstream(out_path) << arr.dump() << "\n";
+    return TC_OK;
+  })
+}
+
 int tc_synthesize(uint32_t layers, uint32_t tensors_per_layer, const uint64_t* sizes, int nsizes,
                   double compute_us_per_byte, uint64_t seed, uint32_t iterations, double opt_us_per_byte,
                   int optimizer_steps, const char* out_path) {

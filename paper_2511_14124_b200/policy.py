@@ -173,3 +173,13 @@ def time_run(trace_path, machine_path="", config=None, repeats=1):
     a = C.c_double()
     N.check(N.lib().tc_time_run(N.b(trace_path), N.b(machine_path), N.b(_cfg_json(config)), repeats, C.byref(a)))
     return a.value
+
+
+def sweep(trace_path, machine_path="", config=None, axis="gpu_capacity", values=(), threads=1):
+    """sweep() (engine.hpp:90-92): one SimReport dict per value, in value order."""
+    vals = (C.c_double * max(len(values), 1))(*values)
+    with tempfile.TemporaryDirectory() as d:
+        op = os.path.join(d, "s.json")
+        N.check(N.lib().tc_sweep(N.b(trace_path), N.b(machine_path), N.b(_cfg_json(config)), N.b(axis), vals,
+                                 len(values), threads, N.b(op)))
+        return json.load(open(op))
