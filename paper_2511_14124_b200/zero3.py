@@ -120,10 +120,15 @@ def exchanged_bytes(engine):
 
 
 def bench_rank(args):
-    """bench.py under torchrun (N>1): each rank runs its own engine on its
-    shard of BASELINE configs[2] (Llama-2 7B ZeRO-3, optimizer states in
-    pinned host memory) with the per-chunk NCCL all-gather / reduce-scatter
-    inside the step; step time is the max over ranks."""
+    """bench.py under torchrun (N>1, or --zero3): each rank runs its own
+    engine on its ZeRO-3 shard with the per-chunk NCCL all-gather /
+    reduce-scatter inside the step; step time is the max over ranks.
+
+    --config c2 (default): OPT-1.3B — the N=1 workload, sharded (strong
+    scaling: the model and the global batch are fixed, each rank holds 1/N);
+    the GPU parameter tier is 40 % of the rank's chunks, every optimizer state
+    in pinned host memory. --config c3: Llama-2 7B with the whole shard on the
+    GPU (BASELINE configs[2])."""
     import tempfile
 
     import torch
@@ -140,12 +145,15 @@ def bench_rank(args):
     os.environ.setdefault("WORLD_SIZE", str(world))
     torch.cuda.set_device(local)
     dist.init_process_group("nccl", device_id=torch.device("cuda", local))
-    layout = shard_layout("llama2-7b", world)
-    wd = tempfile.mkdtemp()
+    model = "llama2-7b" if args.config == "c3" else "opt-1.3b"
+    layout = shard_layout(model, world)
+    wd = tempfile.mkdtemp(dir="/dev/shm" if os.path.isdir("/dev/shm") else None)
     tp = os.path.join(wd, f"r{rank}.jsonl")
     write_rank_trace(tp, layout, rank, tokens=args.tokens, effective_tflops=args.tflops)
     n, S = layout.chunks_per_rank, layout.chunk_bytes
-    mp = T.write_machine(os.path.join(wd, "m.json"), n * S, n * 7 * S)  # all params on GPU, states in host
+    g = n if args.config == "c3" else int(0.4 * n)
+    mp = T.write_machine(os.path.join(wd, "m.json"), g * S, (n - g) * S + n * 6 * S + 1,
+                         pinned_overrides={"cpu->gpu": args.pcie_h2d, "gpu->cpu": args.pcie_d2h})
     cfg = {"policy": "tencache"}
     rep = P.run(tp, mp, cfg)
     dec_bytes = sum(rep["transfer_bytes"].values())
@@ -164,13 +172,15 @@ def bench_rank(args):
     s.record(stream)
     for _ in range(args.steps):
         eng.iteration(**kw)
+    eng.sync()
     e.record(stream)
     torch.cuda.synchronize()
     ms = torch.tensor([s.elapsed_time(e) / args.steps], device="cuda")
     dist.all_reduce(ms, op=dist.ReduceOp.MAX)
     st = eng.stats()
     ms = float(ms.item())
-    total = torch.tensor([float(dec_bytes + (st["opt_h2d_bytes"] + st["opt_d2h_bytes"]) / args.steps)], device="cuda")
+    per_rank = dec_bytes if args.config != "c3" else (st["opt_h2d_bytes"] + st["opt_d2h_bytes"]) / args.steps
+    total = torch.tensor([float(per_rank)], device="cuda")
     dist.all_reduce(total)
     xb = (exchanged_bytes(eng) - x0) / args.steps
     line = None
@@ -179,12 +189,16 @@ def bench_rank(args):
                 "value": round(float(total.item()) / (ms * 1e-3) / 1e9, 4), "unit": "GB/s", "n_gpus": world,
                 "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms, 3), "higher_is_better": True,
                 "scaling": "strong", "vs_baseline": None, "dtype": "bf16/fp32", "data": "synthetic",
-                "config": {"workload": "C3: Llama-2 7B ZeRO-3, optimizer states in pinned host memory",
-                           "model": "llama2-7b", "chunks_per_rank": n, "chunk_bytes": S,
+                "config": {"workload": (f"{model} ZeRO-3 over {world} GPU(s), per-rank engine, NCCL all-gather / "
+                                        "reduce-scatter per chunk access, optimizer states in pinned host memory"),
+                           "model": model, "chunks_per_rank": n, "gpu_chunks_per_rank": g, "chunk_bytes": S,
                            "parallelism": f"zero3 x{world}"},
-                "value_definition": "sum over ranks of (cache-decision + optimizer round-trip PCIe bytes) / step",
+                "value_definition": ("sum over ranks of cache-decision bytes per step / max-over-ranks step time"
+                                     if args.config != "c3" else
+                                     "sum over ranks of optimizer-state PCIe bytes per step / step time"),
                 "nccl_bytes_per_step_per_rank": int(xb),
-                "hit_rate": {"exact": rep["hit_rate"]}, "gpu_launches": int(st["kernel_launches"])}
+                "hit_rate": {"exact_rank0": rep["hit_rate"]}, "gpu_launches": int(st["kernel_launches"]),
+                "e2e": {"value": None, "note": "e2e is measured by the single-GPU path"}}
     eng.close()
     dist.destroy_process_group()
     return line
