@@ -265,9 +265,9 @@ def test_measured_event_log(tmpd):
     lines = [json.loads(x) for x in open(lp)]
     kinds = {x["kind"] for x in lines}
     assert {"prefetch", "evict", "opt_load", "opt_store"} <= kinds
-    for x in lines:
-        if "end_us" in x:
-            assert x["end_us"] >= x["us"] >= 0
+    for x in lines:  # times are relative to the iteration's compute-stream start; pre-staging of the
+        if "end_us" in x:  # next iteration's states may legitimately start earlier (pipelining)
+            assert x["end_us"] >= x["us"]
     # the decision copies of one iteration are exactly the model clock's non-instant requests
     _, ev = P.run(tr, m, {"policy": "tencache"}, events=True)
     model = [json.loads(x) for x in ev if json.loads(x)["kind"] in ("prefetch", "evict", "restore")]
