@@ -25,7 +25,9 @@ cudaError_t launch_cast_f32_to_bf16(const float* in, std::uint16_t* out, std::ui
 // inverse = false: dst[dst_off..] <- src[src_off..]; true: dst[src_off..] <- src[dst_off..]
 cudaError_t launch_pack(const PackSeg* segs, std::uint32_t n, std::uint64_t total, const void* src, void* dst,
                         bool inverse, bool aligned16, cudaStream_t st);
-cudaError_t launch_checksum(const void* data, std::uint64_t bytes, unsigned long long* out, cudaStream_t st);
+// max_ctas > 0 caps the grid (the forward/backward stand-in leaves SMs to concurrent kernels).
+cudaError_t launch_checksum(const void* data, std::uint64_t bytes, unsigned long long* out, cudaStream_t st,
+                            int max_ctas = 0);
 cudaError_t launch_spin(std::uint64_t ns, int ctas, cudaStream_t st);
 // Deterministic N(0, sigma) bf16 fill (counter-based RNG keyed by seed, stream).
 cudaError_t launch_fill_normal_bf16(std::uint16_t* out, std::uint64_t n, float sigma, std::uint64_t seed,

@@ -205,6 +205,7 @@ Executor::Executor(const std::string& trace_path, const std::string& machine_pat
     fcntl(nvme_fd_, F_SETFL, fl | O_DIRECT);
   }
   if (ftruncate(nvme_fd_, static_cast<off_t>(off)) != 0) throw DeviceError(TC_EIO, "ftruncate NVMe tier file");
+  if (const char* c = std::getenv("TC_CHECKSUM_CTAS")) checksum_ctas_ = std::atoi(c);
   if (!std::getenv("TC_SYNC_NVME")) {
     try {
       io_ = std::make_unique<NvmeQueue>(device_, nvme_fd_);
@@ -703,7 +704,7 @@ void Executor::param_step(const TraceStep& step, std::size_t, cudaStream_t cs) {
       zero3_access(x, step.phase == Phase::Backward, cs);
     } else if (access_cursor_ < n_accesses_) {
       TCB_CK(launch_checksum(where(x), x.bytes & ~3ull,
-                             reinterpret_cast<unsigned long long*>(cks_base_ + access_cursor_), cs));
+                             reinterpret_cast<unsigned long long*>(cks_base_ + access_cursor_), cs, checksum_ctas_));
       ++stats_.kernel_launches;
       ++access_cursor_;
     }

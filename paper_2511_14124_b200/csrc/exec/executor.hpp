@@ -282,6 +282,7 @@ class Executor {
   std::uint64_t* d_checksums_ = nullptr;  // two buffers of n_accesses_ (iteration parity)
   std::vector<std::uint64_t> h_checksums_;
   std::uint64_t* cks_base_ = nullptr;
+  int checksum_ctas_ = 0;  // grid cap of the stand-in's checksum (env TC_CHECKSUM_CTAS; 0 = full)
   std::size_t n_accesses_ = 0, access_cursor_ = 0;
   int nvme_fd_ = -1;
   std::unique_ptr<NvmeQueue> io_;  // async NVMe tier I/O (null: synchronous fallback)
