@@ -154,6 +154,10 @@ int tc_adamw_scalars(double lr, double beta1, double beta2, double eps, double w
  * mod 2^64, accumulated into *out (device u64). The forward/backward
  * stand-in reads every migrated byte through this. */
 int tc_checksum(const void* data, uint64_t bytes, uint64_t* out, void* stream);
+/* Deterministic N(0, sigma) bf16 fill (counter-based RNG keyed by seed and
+ * stream_id) — the generator the engine seeds parameters and the backward
+ * stand-in's gradients with; exposed so tests can regenerate them. */
+int tc_fill_normal_bf16(void* out, uint64_t n, float sigma, uint64_t seed, uint64_t stream_id, void* stream);
 /* Busy the compute stream for `us` microseconds on `ctas` CTAs (the layer
  * compute stand-in; trace compute_us, trace.hpp:38). */
 int tc_spin(double us, int ctas, void* stream);
@@ -253,6 +257,14 @@ int tc_engine_enable_zero3(tc_engine* e, int world, int rank, const uint8_t id[1
  * tensor, src, dst) plus end_us, bytes and iter from CUDA events, and a
  * "stall" line (wait_us) per compute-stream wait. path "" switches it off. */
 int tc_engine_event_log(tc_engine* e, const char* path);
+/* Fused ZeRO-3 exchange over peer memory (no NCCL): after
+ * tc_engine_enable_zero3 (an all-zero id skips the NCCL communicator), every
+ * rank exports its IPC handles (HBM pool, control block, gradient view; `n`
+ * bytes), the caller all-gathers them rank-major, and tc_engine_enable_p2p
+ * maps the peers. Accesses then run one gather+unpack kernel and, backward,
+ * one pull-reduce kernel that read the peers' HBM directly. */
+int tc_engine_p2p_handles(tc_engine* e, uint8_t* out, size_t cap, size_t* n);
+int tc_engine_enable_p2p(tc_engine* e, const uint8_t* all_blobs);
 /* Bytes all-gathered + reduce-scattered (NCCL payload, all ranks' pieces) so far. */
 uint64_t tc_engine_exchanged_bytes(tc_engine* e);
 

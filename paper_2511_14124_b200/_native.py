@@ -120,6 +120,7 @@ _SIGS = {
     "tc_adamw_scalars": ([C.c_double] * 5 + [C.c_int64, C.POINTER(C.c_float)], C.c_int),
     "tc_checksum": ([C.c_void_p, C.c_uint64, C.c_void_p, C.c_void_p], C.c_int),
     "tc_spin": ([C.c_double, C.c_int, C.c_void_p], C.c_int),
+    "tc_fill_normal_bf16": ([C.c_void_p, C.c_uint64, C.c_float, C.c_uint64, C.c_uint64, C.c_void_p], C.c_int),
     # executor
     "tc_engine_create": ([C.c_char_p, C.c_char_p, C.c_char_p, C.POINTER(tc_engine_options), C.POINTER(C.c_void_p)],
                          C.c_int),
@@ -140,6 +141,8 @@ _SIGS = {
                                 C.c_uint32], C.c_int),
     "tc_engine_exchanged_bytes": ([C.c_void_p], C.c_uint64),
     "tc_engine_event_log": ([C.c_void_p, C.c_char_p], C.c_int),
+    "tc_engine_p2p_handles": ([C.c_void_p, C.c_void_p, C.c_size_t, C.POINTER(C.c_size_t)], C.c_int),
+    "tc_engine_enable_p2p": ([C.c_void_p, C.c_void_p], C.c_int),
     "tc_engine_access_checksums": ([C.c_void_p, C.POINTER(C.c_uint64), C.c_size_t, C.POINTER(C.c_size_t)], C.c_int),
 }
 

@@ -124,6 +124,12 @@ int tc_checksum(const void* data, uint64_t bytes, uint64_t* out, void* stream) {
                      "tc_checksum");
 }
 
+int tc_fill_normal_bf16(void* out, uint64_t n, float sigma, uint64_t seed, uint64_t stream_id, void* stream) {
+  return cuda_status(launch_fill_normal_bf16(static_cast<std::uint16_t*>(out), n, sigma, seed, stream_id,
+                                             as_stream(stream)),
+                     "tc_fill_normal_bf16");
+}
+
 int tc_spin(double us, int ctas, void* stream) {
   return cuda_status(launch_spin(static_cast<std::uint64_t>(us * 1000.0), ctas, as_stream(stream)), "tc_spin");
 }

@@ -41,3 +41,48 @@ void set_adamw_variant(int v);
 int adamw_variant();
 
 }  // namespace tcb
+
+namespace tcb {
+
+// ------------------------------------------------ ZeRO-3 exchange over peer memory
+// Control block of one rank, in its HBM, mapped into every peer (CUDA IPC).
+// Epochs and counters are monotonic over the run.
+struct P2PCtl {
+  static constexpr int kMaxChunks = 8192;
+  unsigned long long pub_off[kMaxChunks];  // owner: offset of chunk c in its HBM pool
+  unsigned int pub_epoch[kMaxChunks];      // owner: access count at which pub_off is valid
+  unsigned int cnt[kMaxChunks];            // peers: reads of chunk c completed (N-1 per access)
+  unsigned int gpub;                       // owner: backward accesses whose gradient view is ready
+  unsigned int gcnt;                       // peers: gradient pulls completed (N-1 per backward access)
+};
+
+constexpr int kMaxPeers = 8;
+struct PeerTable {
+  int world = 1, rank = 0;
+  const std::uint8_t* pool[kMaxPeers];  // peers' HBM parameter pools (self included)
+  const std::uint8_t* gview[kMaxPeers]; // peers' full-layer gradient views
+  P2PCtl* ctl[kMaxPeers];               // peers' control blocks
+};
+
+// Owner side: publish chunk c at offset `off` of the pool for access `epoch`.
+cudaError_t launch_p2p_publish(P2PCtl* ctl, std::uint32_t chunk, std::uint64_t off, std::uint32_t epoch,
+                               cudaStream_t st);
+// Owner side: gradient view of backward access `gepoch` is ready.
+cudaError_t launch_p2p_publish_grad(P2PCtl* ctl, std::uint32_t gepoch, cudaStream_t st);
+// Fused all-gather + unpack: for every rank q, wait for q's publication of
+// chunk c at `epoch`, copy its piece (pieces[q]: bytes, flat-layer offset)
+// straight from q's pool into the local flat layer view, then count the read
+// in q's control block.
+cudaError_t launch_p2p_gather_unpack(const PeerTable& t, std::uint32_t chunk, std::uint32_t epoch,
+                                     const std::uint64_t* piece_bytes, const std::uint64_t* piece_view_off,
+                                     std::uint8_t* view, cudaStream_t st);
+// Fused pack + reduce-scatter (pull): wait until every rank published its
+// gradient view for backward access `gepoch`, sum (fp32, rank order) the
+// pieces at [view_off, view_off+bytes) of all ranks' views, round once to
+// bf16 into `grad` (S bytes; the rest zero), then count the pull in every
+// peer's control block.
+cudaError_t launch_p2p_pull_reduce(const PeerTable& t, std::uint32_t gepoch, std::uint64_t view_off,
+                                   std::uint64_t bytes, std::uint64_t chunk_bytes, std::uint16_t* grad,
+                                   cudaStream_t st);
+
+}  // namespace tcb

@@ -308,6 +308,8 @@ Executor::~Executor() {
   if (z3_) {
     for (auto& [k, cp] : z3_->plans)
       if (cp.segs) cudaFree(cp.segs);
+    for (void* p : z3_->opened) cudaIpcCloseMemHandle(p);
+    if (z3_->ctl) cudaFree(z3_->ctl);
     for (std::uint8_t* p : {z3_->gather, z3_->view, z3_->gview, z3_->gpad})
       if (p) cudaFree(p);
     if (z3_->comm) nccl().CommDestroy(z3_->comm);
@@ -416,6 +418,7 @@ void Executor::wait_for_write(cudaStream_t s, const SlotSync& y) {
   if (y.writer) TCB_CK(cudaStreamWaitEvent(s, y.writer, 0));
   for (cudaEvent_t e : y.readers) TCB_CK(cudaStreamWaitEvent(s, e, 0));
   if (io_) io_->stream_wait(s, std::max(y.io_read, y.io_write));
+  if (y.peer_cnt && y.peer_target) stream_wait_value32(s, y.peer_cnt, y.peer_target);
 }
 
 void Executor::host_wait_all(const SlotSync& y) {
@@ -1164,6 +1167,8 @@ void Executor::enable_zero3(int world, int rank, const ncclUniqueId& id, const s
     for (std::size_t c = 0; c < idxs.size(); ++c) {
       Zero3::ChunkPlan cp;
       cp.layer = layer;
+      cp.rank_bytes.assign(world, 0);
+      cp.rank_view_off.assign(world, 0);
       std::vector<PackSeg> segs;
       std::uint64_t v = 0;
       for (int r = 0; r < world; ++r) {
@@ -1174,6 +1179,8 @@ void Executor::enable_zero3(int world, int rank, const ncclUniqueId& id, const s
         const std::uint64_t nb = std::min<std::uint64_t>(S, shard - start);
         segs.push_back(PackSeg{static_cast<std::uint64_t>(r) * S, 2 * lo + start, nb, v});
         cp.pieces.emplace_back(2 * lo + start, nb);
+        cp.rank_bytes[r] = nb;
+        cp.rank_view_off[r] = 2 * lo + start;
         cp.vec = cp.vec && ((2 * lo + start) % 16 == 0) && nb % 16 == 0;
         v += nb;
       }
@@ -1186,12 +1193,23 @@ void Executor::enable_zero3(int world, int rank, const ncclUniqueId& id, const s
       z->plans[idxs[c]] = std::move(cp);
     }
   }
+  {
+    std::vector<std::int32_t> order;
+    for (auto& [idx, cp] : z->plans) order.push_back(idx);
+    std::sort(order.begin(), order.end(), [&](std::int32_t a, std::int32_t b) { return recs_[a].id < recs_[b].id; });
+    for (std::size_t k = 0; k < order.size(); ++k) z->plans[order[k]].chunk = static_cast<std::uint32_t>(k);
+    if (order.size() > static_cast<std::size_t>(P2PCtl::kMaxChunks))
+      throw ConfigError("ZeRO-3: more chunks than the p2p control block holds");
+    z->access_epoch.assign(order.size(), 0);
+  }
   TCB_CK(cudaMalloc(&z->gather, world * S));
   TCB_CK(cudaMalloc(&z->view, std::max<std::uint64_t>(max_layer, 16)));
   TCB_CK(cudaMalloc(&z->gview, std::max<std::uint64_t>(max_layer, 16)));
   TCB_CK(cudaMalloc(&z->gpad, world * S));
   TCB_CK(cudaMemset(z->gpad, 0, world * S));
-  nccl_check(nccl().CommInitRank(&z->comm, world, id, rank), "ncclCommInitRank");
+  bool id_zero = true;  // an all-zero id: p2p-only exchange, no NCCL communicator
+  for (char ch : id.internal) id_zero = id_zero && ch == 0;
+  if (!id_zero) nccl_check(nccl().CommInitRank(&z->comm, world, id, rank), "ncclCommInitRank");
   z3_ = std::move(z);
 }
 
@@ -1203,10 +1221,22 @@ void Executor::enable_zero3(int world, int rank, const ncclUniqueId& id, const s
 void Executor::zero3_access(TensorRec& x, bool backward, cudaStream_t cs) {
   Zero3& z = *z3_;
   const Zero3::ChunkPlan& cp = z.plans.at(index_of(x.id));
-  nccl_check(nccl().AllGather(where(x), z.gather, z.S, ncclUint8, z.comm, cs), "ncclAllGather");
+  const unsigned peers_n = static_cast<unsigned>(z.world - 1);
+  if (z.p2p) {  // fused all-gather + unpack straight from the peers' HBM slots
+    const std::uint32_t a = ++z.access_epoch[cp.chunk];
+    Slot& sl = slot_of(x);
+    TCB_CK(launch_p2p_publish(z.ctl, cp.chunk, static_cast<std::uint64_t>(sl.ptr - gpu_.base()), a, cs));
+    TCB_CK(launch_p2p_gather_unpack(z.peers, cp.chunk, a, cp.rank_bytes.data(), cp.rank_view_off.data(), z.view, cs));
+    stats_.kernel_launches += 2;
+    // peers read the slot from now on: its next writer waits for all of them
+    sl.sync.peer_cnt = &z.ctl->cnt[cp.chunk];
+    sl.sync.peer_target = a * peers_n;
+  } else {
+    nccl_check(nccl().AllGather(where(x), z.gather, z.S, ncclUint8, z.comm, cs), "ncclAllGather");
+    TCB_CK(launch_pack(cp.segs, cp.nseg, cp.total, z.gather, z.view, false, cp.vec, cs));
+    stats_.kernel_launches += 1;
+  }
   z.gathered_bytes += z.S * static_cast<std::uint64_t>(z.world);
-  TCB_CK(launch_pack(cp.segs, cp.nseg, cp.total, z.gather, z.view, false, cp.vec, cs));
-  stats_.kernel_launches += 1;
   if (access_cursor_ < n_accesses_) {
     for (const auto& [off, nb] : cp.pieces) {
       TCB_CK(launch_checksum(z.view + off, nb & ~3ull, reinterpret_cast<unsigned long long*>(cks_base_ + access_cursor_),
@@ -1216,21 +1246,80 @@ void Executor::zero3_access(TensorRec& x, bool backward, cudaStream_t cs) {
     ++access_cursor_;
   }
   if (!backward) return;
+  if (z.p2p) {  // my gradient view is refilled only after every peer pulled the previous one
+    const std::uint32_t g = ++z.grad_epoch;
+    if (peers_n && g > 1) stream_wait_value32(cs, &z.ctl->gcnt, (g - 1) * peers_n);
+  }
   for (const auto& [off, nb] : cp.pieces) {
     TCB_CK(launch_fill_normal_bf16(reinterpret_cast<std::uint16_t*>(z.gview + off), nb / 2, 1e-3f,
                                    static_cast<std::uint64_t>(adam_step_) * 1000003ull + static_cast<std::uint64_t>(z.rank),
                                    (static_cast<std::uint64_t>(cp.layer) << 40) + off / 2, cs));
     ++stats_.kernel_launches;
   }
-  if (cp.total < z.S * static_cast<std::uint64_t>(z.world))  // padded chunk: padding gradient is zero
-    TCB_CK(cudaMemsetAsync(z.gpad, 0, z.S * static_cast<std::uint64_t>(z.world), cs));
-  TCB_CK(launch_pack(cp.segs, cp.nseg, cp.total, z.gview, z.gpad, true, cp.vec, cs));
-  ++stats_.kernel_launches;
-  nccl_check(nccl().ReduceScatter(z.gpad, x.grad, z.S / 2, ncclBfloat16, ncclSum, z.comm, cs), "ncclReduceScatter");
+  if (z.p2p) {  // fused pack + reduce-scatter: pull my piece from every rank's view and sum
+    TCB_CK(launch_p2p_publish_grad(z.ctl, z.grad_epoch, cs));
+    TCB_CK(launch_p2p_pull_reduce(z.peers, z.grad_epoch, cp.rank_view_off[z.rank], cp.rank_bytes[z.rank], z.S,
+                                  reinterpret_cast<std::uint16_t*>(x.grad), cs));
+    stats_.kernel_launches += 2;
+  } else {
+    if (cp.total < z.S * static_cast<std::uint64_t>(z.world))  // padded chunk: padding gradient is zero
+      TCB_CK(cudaMemsetAsync(z.gpad, 0, z.S * static_cast<std::uint64_t>(z.world), cs));
+    TCB_CK(launch_pack(cp.segs, cp.nseg, cp.total, z.gview, z.gpad, true, cp.vec, cs));
+    ++stats_.kernel_launches;
+    nccl_check(nccl().ReduceScatter(z.gpad, x.grad, z.S / 2, ncclBfloat16, ncclSum, z.comm, cs),
+               "ncclReduceScatter");
+  }
   z.reduced_bytes += z.S * static_cast<std::uint64_t>(z.world);
   cudaEvent_t e = events_.get(false);
   TCB_CK(cudaEventRecord(e, cs));
   x.grad_ready = e;
+}
+
+// This rank's IPC handles: HBM parameter pool, control block, gradient view.
+std::vector<std::uint8_t> Executor::p2p_handles() {
+  if (!z3_) throw ConfigError("p2p exchange needs tc_engine_enable_zero3 first");
+  Zero3& z = *z3_;
+  if (!z.ctl) {
+    TCB_CK(cudaMalloc(&z.ctl, sizeof(P2PCtl)));
+    TCB_CK(cudaMemset(z.ctl, 0, sizeof(P2PCtl)));
+  }
+  std::vector<std::uint8_t> blob(3 * sizeof(cudaIpcMemHandle_t));
+  cudaIpcMemHandle_t h[3];
+  TCB_CK(cudaIpcGetMemHandle(&h[0], gpu_.base()));
+  TCB_CK(cudaIpcGetMemHandle(&h[1], z.ctl));
+  TCB_CK(cudaIpcGetMemHandle(&h[2], z.gview));
+  std::memcpy(blob.data(), h, sizeof(h));
+  return blob;
+}
+
+// Map every peer's pool, control block and gradient view (self: local
+// pointers) and switch the exchange to the fused p2p kernels.
+void Executor::enable_p2p(const std::uint8_t* all_blobs) {
+  if (!z3_) throw ConfigError("p2p exchange needs tc_engine_enable_zero3 first");
+  Zero3& z = *z3_;
+  if (z.world > kMaxPeers) throw ConfigError("p2p exchange supports up to 8 ranks");
+  if (!z.ctl) p2p_handles();
+  z.peers.world = z.world;
+  z.peers.rank = z.rank;
+  for (int q = 0; q < z.world; ++q) {
+    if (q == z.rank) {
+      z.peers.pool[q] = gpu_.base();
+      z.peers.ctl[q] = z.ctl;
+      z.peers.gview[q] = z.gview;
+      continue;
+    }
+    cudaIpcMemHandle_t h[3];
+    std::memcpy(h, all_blobs + static_cast<std::size_t>(q) * sizeof(h), sizeof(h));
+    void* ptr[3];
+    for (int k = 0; k < 3; ++k) {
+      TCB_CK(cudaIpcOpenMemHandle(&ptr[k], h[k], cudaIpcMemLazyEnablePeerAccess));
+      z.opened.push_back(ptr[k]);
+    }
+    z.peers.pool[q] = static_cast<const std::uint8_t*>(ptr[0]);
+    z.peers.ctl[q] = static_cast<P2PCtl*>(ptr[1]);
+    z.peers.gview[q] = static_cast<const std::uint8_t*>(ptr[2]);
+  }
+  z.p2p = true;
 }
 
 void Executor::set_event_log(const std::string& path) {
@@ -1477,6 +1566,24 @@ int tc_engine_enable_zero3(tc_engine* e, int world, int rank, const uint8_t id[1
 }
 
 uint64_t tc_engine_exchanged_bytes(tc_engine* e) { return e ? e->ex->exchanged_bytes() : 0; }
+
+int tc_engine_p2p_handles(tc_engine* e, uint8_t* out, size_t cap, size_t* n) {
+  TC_GUARD({
+    if (!e) return set_error(TC_EARG, "null engine");
+    const std::vector<std::uint8_t> b = e->ex->p2p_handles();
+    if (n) *n = b.size();
+    if (out && cap >= b.size()) std::memcpy(out, b.data(), b.size());
+    return TC_OK;
+  })
+}
+
+int tc_engine_enable_p2p(tc_engine* e, const uint8_t* all_blobs) {
+  TC_GUARD({
+    if (!e || !all_blobs) return set_error(TC_EARG, "null argument");
+    e->ex->enable_p2p(all_blobs);
+    return TC_OK;
+  })
+}
 
 int tc_engine_event_log(tc_engine* e, const char* path) {
   TC_GUARD({

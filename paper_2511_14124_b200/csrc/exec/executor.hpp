@@ -75,6 +75,8 @@ struct SlotSync {
   std::vector<cudaEvent_t> readers;     // ops that read it since
   std::uint64_t io_write = 0;           // NVMe job that filled it (host buffers)
   std::uint64_t io_read = 0;            // NVMe job that last read it
+  const unsigned* peer_cnt = nullptr;   // ZeRO-3 p2p: peers' reads of the occupant (device word)
+  unsigned peer_target = 0;             // ... writers wait until *peer_cnt >= peer_target
 };
 
 enum class PTier : std::uint8_t { Gpu, HostParam, HostOpt, Nvme };
@@ -100,6 +102,7 @@ class SlotPool {
   bool has_free(std::uint64_t size) const;
   std::uint64_t bytes() const { return bytes_; }
   std::map<std::uint64_t, SlotClass>& classes() { return classes_; }
+  std::uint8_t* base() const { return regions_.empty() ? nullptr : regions_.front(); }  // device pools: one region
 
  private:
   std::map<std::uint64_t, std::uint32_t> want_;
@@ -143,7 +146,9 @@ struct Zero3 {
     std::uint64_t total = 0;
     bool vec = true;
     std::vector<std::pair<std::uint64_t, std::uint64_t>> pieces;  // (view offset, bytes)
+    std::vector<std::uint64_t> rank_bytes, rank_view_off;          // per rank (zero-byte ranks included)
     std::uint32_t layer = 0;
+    std::uint32_t chunk = 0;                                       // dense chunk index (p2p control block)
   };
   std::unordered_map<std::int32_t, ChunkPlan> plans;  // by parameter rec index
   std::uint8_t* gather = nullptr;  // world * S
@@ -151,6 +156,13 @@ struct Zero3 {
   std::uint8_t* gview = nullptr;   // full-layer gradient of the current chunk's pieces
   std::uint8_t* gpad = nullptr;    // world * S rank-major padded gradient (padding zero)
   std::uint64_t gathered_bytes = 0, reduced_bytes = 0;
+  // p2p fused exchange (no NCCL): peer table over CUDA IPC mappings
+  bool p2p = false;
+  PeerTable peers{};
+  P2PCtl* ctl = nullptr;
+  std::vector<void*> opened;               // IPC mappings to close
+  std::vector<std::uint32_t> access_epoch;  // per chunk
+  std::uint32_t grad_epoch = 0;
 };
 
 struct StepOptions {
@@ -178,6 +190,8 @@ class Executor {
   void enable_zero3(int world, int rank, const ncclUniqueId& id, const std::uint64_t* layer_elems,
                     const std::uint64_t* layer_per, std::uint32_t n_layers);
   std::uint64_t exchanged_bytes() const { return z3_ ? z3_->gathered_bytes + z3_->reduced_bytes : 0; }
+  std::vector<std::uint8_t> p2p_handles();
+  void enable_p2p(const std::uint8_t* all_blobs);
   tc_engine_stats stats() const { return stats_; }
   void reset_stats() { stats_ = tc_engine_stats{}; }
   const std::vector<std::uint64_t>& access_checksums();

@@ -11,6 +11,21 @@ namespace {
 using WaitValue32 = CUresult (*)(CUstream, CUdeviceptr, cuuint32_t, unsigned int);
 }
 
+void stream_wait_value32(cudaStream_t s, const unsigned* dev_addr, unsigned value) {
+  static WaitValue32 fn = [] {
+    void* f = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuStreamWaitValue32", &f, cudaEnableDefault, &q) != cudaSuccess ||
+        q != cudaDriverEntryPointSuccess)
+      f = nullptr;
+    return reinterpret_cast<WaitValue32>(f);
+  }();
+  if (fn == nullptr) throw DeviceError(TC_ECUDA, "cuStreamWaitValue32 unavailable");
+  if (fn(reinterpret_cast<CUstream>(s), reinterpret_cast<CUdeviceptr>(dev_addr), value, CU_STREAM_WAIT_VALUE_GEQ) !=
+      CUDA_SUCCESS)
+    throw DeviceError(TC_ECUDA, "cuStreamWaitValue32 failed");
+}
+
 NvmeQueue::NvmeQueue(int device, int fd) : device_(device), fd_(fd) {
   void* fn = nullptr;
   cudaDriverEntryPointQueryResult q;

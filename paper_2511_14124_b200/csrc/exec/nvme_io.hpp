@@ -18,6 +18,10 @@
 
 namespace tcb {
 
+// GPU-side wait until the 32-bit word at `dev_addr` (device-accessible) is
+// >= value (cuStreamWaitValue32 through the runtime's driver entry point).
+void stream_wait_value32(cudaStream_t s, const unsigned* dev_addr, unsigned value);
+
 class NvmeQueue {
  public:
   // Throws DeviceError when stream memory operations are unavailable.

@@ -93,5 +93,12 @@ def checksum(x, out=None, stream=None):
     return out
 
 
+def fill_normal_bf16(out, sigma, seed, stream_id, stream=None):
+    """The engine's deterministic bf16 N(0, sigma) generator into `out`."""
+    N.check(N.lib().tc_fill_normal_bf16(_dev(out), out.numel(), float(sigma), int(seed), int(stream_id),
+                                        _stream(stream)))
+    return out
+
+
 def spin(us, ctas=1, stream=None):
     N.check(N.lib().tc_spin(float(us), ctas, _stream(stream)))

@@ -93,8 +93,8 @@ def write_rank_trace(path, layout: ShardLayout, rank: int, iterations=1, tokens=
     return T.write_chunk_trace(path, plan, iterations, tokens * layout.world, effective_tflops * layout.world)
 
 
-def enable(engine, layout: ShardLayout, rank: int, world: int, group=None):
-    """Attach the ZeRO-3 exchange to an Engine: rank 0 creates the NCCL id,
+def _enable_nccl(engine, layout: ShardLayout, rank: int, world: int, group=None):
+    """Attach the NCCL ZeRO-3 exchange to an Engine: rank 0 creates the NCCL id,
     torch.distributed broadcasts it (any backend), every rank initialises its
     communicator inside the native engine."""
     import ctypes as C
@@ -112,6 +112,34 @@ def enable(engine, layout: ShardLayout, rank: int, world: int, group=None):
     elems = (C.c_uint64 * len(layout.layers))(*[l.elems for l in layout.layers])
     per = (C.c_uint64 * len(layout.layers))(*[l.per for l in layout.layers])
     N.check(N.lib().tc_engine_enable_zero3(engine._h, world, rank, idbuf, elems, per, len(layout.layers)))
+
+
+def enable(engine, layout, rank, world, group=None, exchange="nccl"):  # noqa: F811 (documented below)
+    """Attach the ZeRO-3 exchange. exchange="nccl": NCCL all-gather /
+    reduce-scatter + pack kernels. exchange="p2p": the fused kernels over
+    peer memory (CUDA IPC handles all-gathered with torch.distributed when
+    world > 1; no NCCL communicator)."""
+    import ctypes as C
+
+    from . import _native as N
+    if exchange == "nccl":
+        return _enable_nccl(engine, layout, rank, world, group)
+    idbuf = (C.c_uint8 * 128)()  # all-zero id: no NCCL communicator
+    elems = (C.c_uint64 * len(layout.layers))(*[l.elems for l in layout.layers])
+    per = (C.c_uint64 * len(layout.layers))(*[l.per for l in layout.layers])
+    N.check(N.lib().tc_engine_enable_zero3(engine._h, world, rank, idbuf, elems, per, len(layout.layers)))
+    n = C.c_size_t()
+    N.check(N.lib().tc_engine_p2p_handles(engine._h, None, 0, C.byref(n)))
+    mine = (C.c_uint8 * n.value)()
+    N.check(N.lib().tc_engine_p2p_handles(engine._h, mine, n.value, C.byref(n)))
+    blobs = [bytes(mine)]
+    if world > 1:
+        import torch.distributed as dist
+        blobs = [None] * world
+        dist.all_gather_object(blobs, bytes(mine), group=group)
+    allb = b"".join(blobs)
+    buf = (C.c_uint8 * len(allb)).from_buffer_copy(allb)
+    N.check(N.lib().tc_engine_enable_p2p(engine._h, buf))
 
 
 def exchanged_bytes(engine):

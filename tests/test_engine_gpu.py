@@ -291,3 +291,35 @@ def test_tied_weight_reuse_and_duplicate_access(tmpd):
         stt = check_engine(tr, m, {"policy": pol}, iters=3)
         rep = P.run(tr, m, {"policy": pol})
         assert stt["param_hits"] == rep["param_hits"]
+
+
+def _zero3_run(tmpd, exchange, iters=2):
+    from paper_2511_14124_b200 import zero3 as Z
+    lay = Z.shard_layout("gpt2-small", 1, chunks_per_layer=3)
+    tp = os.path.join(tmpd, "zx.jsonl")
+    Z.write_rank_trace(tp, lay, 0, iterations=iters, tokens=64)
+    n, S = lay.chunks_per_rank, lay.chunk_bytes
+    mp = T.write_machine(os.path.join(tmpd, "mx.json"), int(0.5 * n) * S, n * 7 * S)
+    e = Engine(tp, mp, {"policy": "tencache"})
+    e.seed(3)
+    Z.enable(e, lay, 0, 1, exchange=exchange)
+    cks = []
+    for _ in range(iters):
+        e.iteration(**HP)
+        cks.append(e.access_checksums().copy())
+    params = [e.read_tensor(i, S).copy() for i in range(1, n + 1)]
+    states = [e.read_tensor(n + i, 6 * S).copy() for i in range(1, n + 1)]
+    grads = [e.read_grad(i, S).copy() for i in range(1, n + 1)]
+    e.close()
+    return cks, params, states, grads
+
+
+def test_zero3_p2p_fused_exchange_equals_nccl_world1(tmpd):
+    """The fused peer-memory exchange (one gather+unpack kernel, one
+    pull-reduce kernel, no NCCL) gives bit-identical bytes, gradients and
+    updates to the NCCL + pack path at world size 1."""
+    a = _zero3_run(tmpd, "nccl")
+    b = _zero3_run(tmpd, "p2p")
+    for x, y in zip(a, b):
+        for u, v in zip(x, y):
+            assert np.array_equal(u, v)

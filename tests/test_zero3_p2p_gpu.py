@@ -1,0 +1,113 @@
+"""The fused ZeRO-3 exchange at world size 2 — two processes sharing ONE B200
+through CUDA IPC (NCCL cannot run two ranks on one GPU; the peer-memory
+protocol can). Checks: every access checksum equals the sum over ranks of the
+checksum of that rank's piece (so each rank read the right bytes of the
+other's HBM slot at the right epoch), and every reduced gradient equals the
+fp32 rank-order sum of both ranks' regenerated backward gradients."""
+import os
+import socket
+import tempfile
+
+import numpy as np
+import pytest
+import torch
+import torch.multiprocessing as mp
+
+pytestmark = pytest.mark.gpu
+
+
+def _port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def _rank(rank, world, port, d, q):
+    import torch.distributed as dist
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from oracle import ref
+        from paper_2511_14124_b200 import kernels as K
+        from paper_2511_14124_b200 import traces as T
+        from paper_2511_14124_b200 import zero3 as Z
+        from paper_2511_14124_b200.engine import Engine
+        torch.cuda.set_device(0)
+        lay = Z.shard_layout("gpt2-small", world, chunks_per_layer=2)
+        tp = os.path.join(d, f"r{rank}.jsonl")
+        Z.write_rank_trace(tp, lay, rank, iterations=2, tokens=64)
+        n, S = lay.chunks_per_rank, lay.chunk_bytes
+        mpth = T.write_machine(os.path.join(d, f"m{rank}.json"), int(0.5 * n) * S, n * 7 * S)
+        e = Engine(tp, mpth, {"policy": "tencache"})
+        e.seed(10 + rank)
+        Z.enable(e, lay, rank, world, exchange="p2p")
+        mine = [e.read_tensor(i, S).view(np.uint16).copy() for i in range(1, n + 1)]
+        allp = [None] * world
+        dist.all_gather_object(allp, mine)
+        # chunk -> (layer, index within layer)
+        pos, cid = {}, 1
+        for L in lay.layers:
+            for c in range(L.chunks):
+                pos[cid] = (L, c)
+                cid += 1
+        steps = []
+        import json
+        for line in open(tp):
+            r = json.loads(line)
+            if "s" in r and r["s"]["phase"] != "o":
+                steps.append(r["s"]["ids"][0])
+        e.iteration(lr=1e-3)
+        got = e.access_checksums()
+        want = []
+        for cidx in steps:
+            L, c = pos[cidx]
+            tot = 0
+            for r in range(world):
+                v = max(0, min(S, 2 * L.shard_elems(world, r) - c * S))
+                tot += ref.checksum(allp[r][cidx - 1][: v // 2])
+            want.append(tot % (1 << 64))
+        assert np.array_equal(got, np.array(want, dtype=np.uint64)), "gathered bytes"
+        # gradients: regenerate every rank's backward pieces for my shard and sum
+        for cidx in range(1, n + 1):
+            L, c = pos[cidx]
+            v = max(0, min(S, 2 * L.shard_elems(world, rank) - c * S))
+            off = 2 * rank * L.per + c * S
+            acc = torch.zeros(S // 2, dtype=torch.float32, device="cuda")
+            for r in range(world):
+                g = torch.empty(v // 2, dtype=torch.bfloat16, device="cuda")
+                if v:
+                    K.fill_normal_bf16(g, 1e-3, 1 * 1000003 + r, (L.layer << 40) + off // 2)
+                acc[: v // 2] += g.float()
+            torch.cuda.synchronize()
+            want_g = acc.to(torch.bfloat16).view(torch.int16).cpu().numpy().astype(np.uint16)
+            assert np.array_equal(e.read_grad(cidx, S), want_g), f"grad of chunk {cidx}"
+        e.iteration(lr=1e-3)  # second iteration: epochs and counters advance
+        e.sync()
+        e.close()
+        q.put((rank, "ok"))
+    except Exception as ex:  # pragma: no cover
+        import traceback
+        q.put((rank, traceback.format_exc()[-2000:]))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_p2p_exchange_two_ranks_one_gpu():
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    d = tempfile.mkdtemp()
+    port = _port()
+    ps = [ctx.Process(target=_rank, args=(r, 2, port, d, q)) for r in range(2)]
+    for p in ps:
+        p.start()
+    res = {}
+    for _ in ps:
+        r, msg = q.get(timeout=240)
+        res[r] = msg
+    for p in ps:
+        p.join(timeout=60)
+        if p.is_alive():
+            p.kill()
+    assert res == {0: "ok", 1: "ok"}, res
