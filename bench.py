@@ -437,7 +437,9 @@ def main():
     ap.add_argument("--no-hoist", action="store_true", help="run optimizer updates in place (after backward)")
     ap.add_argument("--no-prestage", action="store_true", help="no staging of optimizer states ahead of updates")
     ap.add_argument("--config", default="c2", choices=["c2", "c3", "c4"])
-    ap.add_argument("--zero3", action="store_true", help="the torchrun ZeRO-3 path (C3) even at world size 1")
+    ap.add_argument("--zero3", action="store_true", help="the torchrun ZeRO-3 path even at world size 1")
+    ap.add_argument("--exchange", default="p2p", choices=["p2p", "nccl"],
+                    help="ZeRO-3 exchange: fused peer-memory kernels (default) or NCCL + pack kernels")
     ap.add_argument("--stages", type=int, default=12, help="HBM optimizer-state stages")
     ap.add_argument("--gpu-spares", type=int, default=4, help="spare HBM slots per parameter class")
     ap.add_argument("--policy", default="tencache",

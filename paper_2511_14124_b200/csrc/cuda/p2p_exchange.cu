@@ -113,8 +113,13 @@ __global__ void __launch_bounds__(kThr) pull_reduce_kernel(PullArgs a) {
   const std::uint64_t n = a.chunk_bytes / 2, valid = a.bytes / 2;
   for (std::uint64_t i = (static_cast<std::uint64_t>(blockIdx.x) * kThr + threadIdx.x) * 8; i < n;
        i += static_cast<std::uint64_t>(gridDim.x) * kThr * 8) {
-    float acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
-    for (int q = 0; q < a.t.world; ++q) {
+    float acc[8];
+    {  // the sum starts from rank 0's value (not +0): a single rank reduces to an exact copy, -0 included
+      const std::uint16_t* v = reinterpret_cast<const std::uint16_t*>(a.t.gview[0] + a.view_off);
+#pragma unroll
+      for (int k = 0; k < 8; ++k) acc[k] = i + k < valid ? __uint_as_float(static_cast<unsigned>(v[i + k]) << 16) : 0.0f;
+    }
+    for (int q = 1; q < a.t.world; ++q) {
       const std::uint16_t* v = reinterpret_cast<const std::uint16_t*>(a.t.gview[q] + a.view_off);
 #pragma unroll
       for (int k = 0; k < 8; ++k)

@@ -187,7 +187,7 @@ def bench_rank(args):
     dec_bytes = sum(rep["transfer_bytes"].values())
     eng = Engine(tp, mp, cfg, device=local, nvme_dir=wd)
     eng.seed(rank)
-    enable(eng, layout, rank, world)
+    enable(eng, layout, rank, world, exchange=args.exchange)
     stream = torch.cuda.current_stream()
     kw = dict(lr=1e-4, compute_mode=1 if args.compute == "spin" else 0, stream=stream.cuda_stream)
     for _ in range(args.warmup):
@@ -236,7 +236,7 @@ def bench_rank(args):
                 "config": {"workload": (f"{model} ZeRO-3 over {world} GPU(s), per-rank engine, NCCL all-gather / "
                                         "reduce-scatter per chunk access, optimizer states in pinned host memory"),
                            "model": model, "chunks_per_rank": n, "gpu_chunks_per_rank": g, "chunk_bytes": S,
-                           "parallelism": f"zero3 x{world}"},
+                           "parallelism": f"zero3 x{world}", "exchange": args.exchange},
                 "value_definition": ("sum over ranks of cache-decision bytes per step / max-over-ranks step time"
                                      if args.config != "c3" else
                                      "sum over ranks of optimizer-state PCIe bytes per step / step time"),

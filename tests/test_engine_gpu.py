@@ -257,7 +257,7 @@ def test_measured_event_log(tmpd):
     tr, m = write_with_states(tmpd, "ev", [4096] * 6, 3 * 4096, 3 * 4096 + 6 * 6 * 4096, iters=2)
     e = Engine(tr, m, {"policy": "tencache"})
     e.seed(0)
-    lp = os.path.join(tmpd, "ev.jsonl")
+    lp = os.path.join(tmpd, "timeline.jsonl")
     e.event_log(lp)
     e.iteration(**HP)
     e.iteration(**HP)

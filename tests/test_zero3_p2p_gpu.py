@@ -79,7 +79,10 @@ def _rank(rank, world, port, d, q):
                 g = torch.empty(v // 2, dtype=torch.bfloat16, device="cuda")
                 if v:
                     K.fill_normal_bf16(g, 1e-3, 1 * 1000003 + r, (L.layer << 40) + off // 2)
-                acc[: v // 2] += g.float()
+                if r == 0:
+                    acc[: v // 2] = g.float()  # fp32 sum in rank order starting from rank 0's value
+                else:
+                    acc[: v // 2] += g.float()
             torch.cuda.synchronize()
             want_g = acc.to(torch.bfloat16).view(torch.int16).cpu().numpy().astype(np.uint16)
             assert np.array_equal(e.read_grad(cidx, S), want_g), f"grad of chunk {cidx}"
