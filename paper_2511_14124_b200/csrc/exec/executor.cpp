@@ -206,6 +206,7 @@ Executor::Executor(const std::string& trace_path, const std::string& machine_pat
   }
   if (ftruncate(nvme_fd_, static_cast<off_t>(off)) != 0) throw DeviceError(TC_EIO, "ftruncate NVMe tier file");
   if (const char* c = std::getenv("TC_CHECKSUM_CTAS")) checksum_ctas_ = std::atoi(c);
+  if (const char* c = std::getenv("TC_OPT_YIELD")) opt_yield_ = std::atoi(c) != 0;
   if (!std::getenv("TC_SYNC_NVME")) {
     try {
       io_ = std::make_unique<NvmeQueue>(device_, nvme_fd_);
@@ -675,6 +676,7 @@ void Executor::apply(const Req& r) {
     throw DeviceError(TC_EINTERNAL, "unsupported transfer direction");
   }
   if (r.blocking && done) barriers_.push_back(done);
+  if (done && !r.instant) (r.dst == Tier::Gpu ? last_h2d_ : last_d2h_) = done;
 }
 
 void Executor::wait_barriers(cudaStream_t cs) {
@@ -734,6 +736,7 @@ std::size_t Executor::stage_state(TensorRec& s) {
   stage_free_.pop_front();
   Slot& h = slot_of(s);
   tag_ = CopyTag{"opt_load", s.id, 1, 0};
+  if (opt_yield_ && last_h2d_) TCB_CK(cudaStreamWaitEvent(h2d_opt_, last_h2d_, 0));
   wait_for_write(h2d_opt_, stage_sync_[b]);
   wait_for_read(h2d_opt_, h.sync);
   cudaEvent_t e1 = copy(h2d_opt_, stage_[b], h.ptr, s.bytes, true);
@@ -808,6 +811,7 @@ void Executor::optimizer_work(TensorRec& s, TensorRec& p) {
     wait_for_read(d2h_opt_, stage_sync_[b]);
     wait_for_write(d2h_opt_, h.sync);
     TCB_CK(cudaStreamWaitEvent(d2h_opt_, a1, 0));
+    if (opt_yield_ && last_d2h_) TCB_CK(cudaStreamWaitEvent(d2h_opt_, last_d2h_, 0));
     tag_ = CopyTag{"opt_store", s.id, 0, 1};
     cudaEvent_t e3 = copy(d2h_opt_, h.ptr, stg, s.bytes, false);
     h.sync = SlotSync{e3, {}};
@@ -1126,6 +1130,8 @@ void Executor::scrub(std::uint64_t gen) {
     if (r.grad_ready && events_.done_by(r.grad_ready, gen)) r.grad_ready = nullptr;
   }
   std::erase_if(barriers_, [&](cudaEvent_t e) { return events_.done_by(e, gen); });
+  if (last_h2d_ && events_.done_by(last_h2d_, gen)) last_h2d_ = nullptr;
+  if (last_d2h_ && events_.done_by(last_d2h_, gen)) last_d2h_ = nullptr;
 }
 
 void Executor::drain() {

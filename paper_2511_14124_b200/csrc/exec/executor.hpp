@@ -296,7 +296,9 @@ class Executor {
   std::uint64_t* d_checksums_ = nullptr;  // two buffers of n_accesses_ (iteration parity)
   std::vector<std::uint64_t> h_checksums_;
   std::uint64_t* cks_base_ = nullptr;
-  int checksum_ctas_ = 0;  // grid cap of the stand-in's checksum (env TC_CHECKSUM_CTAS; 0 = full)
+  int checksum_ctas_ = 0;
+  bool opt_yield_ = false;                 // optimizer copies queue behind earlier decision copies (env TC_OPT_YIELD)
+  cudaEvent_t last_h2d_ = nullptr, last_d2h_ = nullptr;  // most recent decision copy per direction  // grid cap of the stand-in's checksum (env TC_CHECKSUM_CTAS; 0 = full)
   std::size_t n_accesses_ = 0, access_cursor_ = 0;
   int nvme_fd_ = -1;
   std::unique_ptr<NvmeQueue> io_;  // async NVMe tier I/O (null: synchronous fallback)
