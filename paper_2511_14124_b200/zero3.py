@@ -233,8 +233,10 @@ def bench_rank(args):
                 "value": round(float(total.item()) / (ms * 1e-3) / 1e9, 4), "unit": "GB/s", "n_gpus": world,
                 "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms, 3), "higher_is_better": True,
                 "scaling": "strong", "vs_baseline": None, "dtype": "bf16/fp32", "data": "synthetic",
-                "config": {"workload": (f"{model} ZeRO-3 over {world} GPU(s), per-rank engine, NCCL all-gather / "
-                                        "reduce-scatter per chunk access, optimizer states in pinned host memory"),
+                "config": {"workload": (f"{model} ZeRO-3 over {world} GPU(s), per-rank engine, per-chunk-access "
+                                        + ("fused peer-memory gather+unpack / pull-reduce kernels"
+                                           if args.exchange == "p2p" else "NCCL all-gather / reduce-scatter")
+                                        + ", optimizer states in pinned host memory"),
                            "model": model, "chunks_per_rank": n, "gpu_chunks_per_rank": g, "chunk_bytes": S,
                            "parallelism": f"zero3 x{world}", "exchange": args.exchange},
                 "value_definition": ("sum over ranks of cache-decision bytes per step / max-over-ranks step time"
