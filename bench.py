@@ -249,6 +249,12 @@ def run_ours(args):
                      "peak": hbm, "unit": "GB/s", "frac": round(achieved / hbm, 4), "traffic": traffic,
                      "algorithmic_bytes_per_launch": int(ADAM_BYTES_PER_ELEM * elems_per_launch),
                      "avg_launch_us": round(avg_launch_ms * 1e3, 2),
+                     "resident_span": ({"avg_us": round(st["adam_span_ms"] * 1e3 / st["adam_spans"], 2),
+                                        "achieved": round(ADAM_BYTES_PER_ELEM * elems_per_launch /
+                                                          (st["adam_span_ms"] / st["adam_spans"] * 1e-3) / 1e9, 1),
+                                        "note": "first CTA start to last CTA end (%globaltimer) of the same launches; "
+                                                "the event-timed avg_launch_us adds queueing behind other streams"}
+                                       if st["adam_spans"] else None),
                      "peak_source": "MEASURED_PEAKS.json hbm_gbs (burst copy)"},
         "e2e": {"value": round(value_bytes / (e2e_ms * 1e-3) / 1e9, 4), "unit": "GB/s", "ms_per_step": round(e2e_ms, 3),
                 "h2d_bytes_per_step": int(tokens_h.numel() * 4), "d2h_bytes_per_step": int(len(cks) * 8),

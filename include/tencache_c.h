@@ -227,8 +227,10 @@ typedef struct {
   uint64_t requests, kernel_launches, copies;
   double h2d_busy_ms, d2h_busy_ms;       /* copy-engine busy time (event pairs) */
   double stall_ms;                       /* compute stream waiting on copies */
-  double adam_ms;                        /* fused AdamW kernel time */
+  double adam_ms;                        /* fused AdamW kernel time (CUDA events on its stream) */
   uint64_t adam_elems;
+  double adam_span_ms;                   /* AdamW resident time: first CTA start to last CTA end */
+  uint64_t adam_spans;                   /* launches measured in adam_span_ms */
 } tc_engine_stats;
 
 int tc_engine_stats_get(tc_engine* e, tc_engine_stats* out);

@@ -74,7 +74,7 @@ class tc_engine_stats(C.Structure):
                                           "param_accesses", "param_hits", "ontime_accesses", "requests",
                                           "kernel_launches", "copies")] + \
               [(n, C.c_double) for n in ("h2d_busy_ms", "d2h_busy_ms", "stall_ms", "adam_ms")] + \
-              [("adam_elems", C.c_uint64)]
+              [("adam_elems", C.c_uint64), ("adam_span_ms", C.c_double), ("adam_spans", C.c_uint64)]
 
     def as_dict(self):
         return {n: getattr(self, n) for n, _ in self._fields_}

@@ -18,8 +18,12 @@ struct AdamScalars {
 AdamScalars adam_scalars(double lr, double b1, double b2, double eps, double wd, std::int64_t step);
 
 // All launchers return cudaGetLastError() of the launch.
+// span_min/span_max (optional, TMA variants): atomicMin'd with the first
+// CTA's start and atomicMax'd with the last CTA's end (%globaltimer ns) — the
+// kernel's resident span, free of launch and queueing gaps.
 cudaError_t launch_adamw(float* p, float* m, float* v, const std::uint16_t* g, std::uint16_t* pout, std::uint64_t n,
-                         const AdamScalars& s, float grad_scale, cudaStream_t st);
+                         const AdamScalars& s, float grad_scale, cudaStream_t st,
+                         unsigned long long* span_min = nullptr, unsigned long long* span_max = nullptr);
 cudaError_t launch_cast_bf16_to_f32(const std::uint16_t* in, float* out, std::uint64_t n, cudaStream_t st);
 cudaError_t launch_cast_f32_to_bf16(const float* in, std::uint16_t* out, std::uint64_t n, cudaStream_t st);
 // inverse = false: dst[dst_off..] <- src[src_off..]; true: dst[src_off..] <- src[dst_off..]

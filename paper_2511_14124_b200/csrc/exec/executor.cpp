@@ -255,6 +255,7 @@ Executor::Executor(const std::string& trace_path, const std::string& machine_pat
   for (const auto& s : trace_.steps)
     if (s.phase != Phase::OptimizerUpdate) n_accesses_ += s.tensor_ids.size();
   TCB_CK(cudaMalloc(&d_checksums_, 2 * std::max<std::size_t>(n_accesses_, 1) * sizeof(std::uint64_t)));
+  TCB_CK(cudaMalloc(&d_span_, 2 * 2 * std::max<std::size_t>(recs_.size(), 1) * sizeof(unsigned long long)));
   h_checksums_.assign(n_accesses_, 0);
   TCB_CK(cudaStreamCreateWithFlags(&h2d_, cudaStreamNonBlocking));
   TCB_CK(cudaStreamCreateWithFlags(&d2h_, cudaStreamNonBlocking));
@@ -299,6 +300,7 @@ Executor::~Executor() {
     for (auto* p : v) cudaFree(p);
   if (grads_) cudaFree(grads_);
   if (d_checksums_) cudaFree(d_checksums_);
+  if (d_span_) cudaFree(d_span_);
   if (h2d_) cudaStreamDestroy(h2d_);
   if (d2h_) cudaStreamDestroy(d2h_);
   if (opt_) cudaStreamDestroy(opt_);
@@ -792,8 +794,15 @@ void Executor::optimizer_work(TensorRec& s, TensorRec& p) {
   TCB_CK(cudaEventRecord(a0, opt_));
   auto* st = reinterpret_cast<float*>(stg);
   const AdamScalars sc = adam_scalars(so_.lr, so_.beta1, so_.beta2, so_.eps, so_.weight_decay, adam_step_);
+  unsigned long long *smin = nullptr, *smax = nullptr;
+  const std::size_t cap = std::max<std::size_t>(recs_.size(), 1);
+  if (span_cursor_ < cap && adamw_variant() >= 2) {  // in-kernel resident span (TMA variants)
+    smin = span_base_ + span_cursor_;
+    smax = span_base_ + cap + span_cursor_;
+    ++span_cursor_;
+  }
   TCB_CK(launch_adamw(st, st + n, st + 2 * n, reinterpret_cast<const std::uint16_t*>(p.grad),
-                      reinterpret_cast<std::uint16_t*>(pout), n, sc, so_.grad_scale, opt_));
+                      reinterpret_cast<std::uint16_t*>(pout), n, sc, so_.grad_scale, opt_, smin, smax));
   TCB_CK(cudaEventRecord(a1, opt_));
   adam_.emplace_back(a0, a1);
   ++stats_.kernel_launches;
@@ -959,6 +968,13 @@ void Executor::iteration(const StepOptions& so, cudaStream_t compute) {
   access_cursor_ = 0;
   events_.next_generation();
   cks_base_ = d_checksums_ + (events_.generation() % 2) * std::max<std::size_t>(n_accesses_, 1);
+  {  // per-launch AdamW spans: mins start at UINT64_MAX (0xff bytes), maxes at 0
+    const std::size_t cap = std::max<std::size_t>(recs_.size(), 1);
+    span_base_ = d_span_ + (events_.generation() % 2) * 2 * cap;
+    span_cursor_ = 0;
+    TCB_CK(cudaMemsetAsync(span_base_, 0xff, cap * sizeof(unsigned long long), opt_));
+    TCB_CK(cudaMemsetAsync(span_base_ + cap, 0, cap * sizeof(unsigned long long), opt_));
+  }
   TCB_CK(cudaMemsetAsync(cks_base_, 0, std::max<std::size_t>(n_accesses_, 1) * sizeof(std::uint64_t), compute));
   nvtxRangePushA("tencache.decide");
   const std::vector<Hook> hooks = decide_iteration();
@@ -1036,6 +1052,7 @@ void Executor::finish_iteration() {
   }
   rec.cks_buf = static_cast<std::size_t>(events_.generation() % 2);
   rec.io_seq = io_ ? io_->submitted() : 0;
+  rec.spans = span_cursor_;
   copies_.clear();
   stalls_.clear();
   ontime_.clear();
@@ -1105,6 +1122,17 @@ void Executor::harvest_front() {
   }
   TCB_CK(cudaMemcpy(h_checksums_.data(), d_checksums_ + rec.cks_buf * std::max<std::size_t>(n_accesses_, 1),
                     n_accesses_ * sizeof(std::uint64_t), cudaMemcpyDeviceToHost));
+  if (rec.spans) {
+    const std::size_t cap = std::max<std::size_t>(recs_.size(), 1);
+    std::vector<unsigned long long> sp(2 * cap);
+    TCB_CK(cudaMemcpy(sp.data(), d_span_ + rec.cks_buf * 2 * cap, sp.size() * sizeof(unsigned long long),
+                      cudaMemcpyDeviceToHost));
+    for (std::size_t k = 0; k < rec.spans; ++k)
+      if (sp[cap + k] > sp[k]) {
+        stats_.adam_span_ms += static_cast<double>(sp[cap + k] - sp[k]) * 1e-6;
+        ++stats_.adam_spans;
+      }
+  }
   scrub(rec.gen);
   events_.recycle_upto(rec.gen);
 }

@@ -262,6 +262,7 @@ class Executor {
     std::vector<cudaEvent_t> marks, fences;
     std::size_t cks_buf = 0;
     std::uint64_t io_seq = 0;  // last NVMe job submitted in the iteration
+    std::size_t spans = 0;     // AdamW launches with a recorded span
   };
   void harvest_front();
   void drain();
@@ -296,6 +297,9 @@ class Executor {
   std::uint64_t* d_checksums_ = nullptr;  // two buffers of n_accesses_ (iteration parity)
   std::vector<std::uint64_t> h_checksums_;
   std::uint64_t* cks_base_ = nullptr;
+  unsigned long long* d_span_ = nullptr;  // 2 parities x n_params x (min, max) AdamW kernel spans
+  unsigned long long* span_base_ = nullptr;
+  std::size_t span_cursor_ = 0;
   int checksum_ctas_ = 0;
   bool opt_yield_ = false;                 // optimizer copies queue behind earlier decision copies (env TC_OPT_YIELD)
   cudaEvent_t last_h2d_ = nullptr, last_d2h_ = nullptr;  // most recent decision copy per direction  // grid cap of the stand-in's checksum (env TC_CHECKSUM_CTAS; 0 = full)

@@ -41,7 +41,7 @@ for mib in (1, 4, 16, 64, 256, 1024):
     out["d2h_GBps"].append(round(res["d2h"], 2))
     out["bidir_total_GBps"].append(round(res["bidir"], 2))
     del h1, h2, d1, d2
-out["async_engine_count"] = torch.cuda.get_device_properties(0).__dict__.get("async_engine_count", None)
+out["note"] = "best of REPS per size; bidir = one H2D and one D2H copy of the size running concurrently"
 os.makedirs("gpurun_out", exist_ok=True)
 json.dump(out, open("gpurun_out/pcie_sweep.json", "w"), indent=1)
 print(json.dumps(out))
