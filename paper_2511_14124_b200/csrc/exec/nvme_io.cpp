@@ -3,6 +3,9 @@
 #include <cuda.h>
 #include <unistd.h>
 
+#include <algorithm>
+#include <cstdlib>
+
 #include "capi_common.hpp"
 
 namespace tcb {
@@ -52,7 +55,10 @@ NvmeQueue::NvmeQueue(int device, int fd) : device_(device), fd_(fd) {
     cudaFreeHost(h);
     throw DeviceError(TC_ECUDA, "stream memory operations unsupported");
   }
-  worker_ = std::thread([this] { run(); });
+  dispatcher_ = std::thread([this] { dispatch(); });
+  const char* env = std::getenv("TC_NVME_THREADS");
+  const int nw = env ? std::max(1, std::atoi(env)) : 8;
+  for (int i = 0; i < nw; ++i) workers_.emplace_back([this] { work(); });
 }
 
 NvmeQueue::~NvmeQueue() {
@@ -61,7 +67,10 @@ NvmeQueue::~NvmeQueue() {
     stop_ = true;
   }
   cv_.notify_all();
-  if (worker_.joinable()) worker_.join();
+  piece_cv_.notify_all();
+  if (dispatcher_.joinable()) dispatcher_.join();
+  for (auto& w : workers_)
+    if (w.joinable()) w.join();
   if (flag_) cudaFreeHost(const_cast<std::uint32_t*>(flag_));
 }
 
@@ -103,8 +112,10 @@ std::uint64_t NvmeQueue::done() const {
   return done_;
 }
 
-void NvmeQueue::run() {
+// Jobs in FIFO order: await their events, then fan out pieces of <= 16 MiB.
+void NvmeQueue::dispatch() {
   cudaSetDevice(device_);
+  constexpr std::uint64_t kPiece = 16ull << 20;
   for (;;) {
     Job j;
     {
@@ -113,25 +124,62 @@ void NvmeQueue::run() {
       if (q_.empty()) return;
       j = std::move(q_.front());
       q_.pop_front();
+      remaining_[j.seq] = ~0u;  // open (not yet split) until its pieces are queued
     }
-    std::string err;
+    bool ok = true;
     for (cudaEvent_t e : j.waits)
-      if (e && cudaEventSynchronize(e) != cudaSuccess) err = "event wait failed before NVMe I/O";
-    auto* p = static_cast<std::uint8_t*>(j.buf);
-    for (std::uint64_t done = 0; err.empty() && done < j.bytes;) {
-      const ssize_t k = j.write ? pwrite(fd_, p + done, j.bytes - done, static_cast<off_t>(j.off + done))
-                                : pread(fd_, p + done, j.bytes - done, static_cast<off_t>(j.off + done));
-      if (k <= 0) err = j.write ? "NVMe tier write failed" : "NVMe tier read failed";
+      if (e && cudaEventSynchronize(e) != cudaSuccess) ok = false;
+    std::lock_guard<std::mutex> g(mu_);
+    if (!ok) error_ = "event wait failed before NVMe I/O";
+    const std::uint64_t n = std::max<std::uint64_t>(1, (j.bytes + kPiece - 1) / kPiece);
+    remaining_[j.seq] = static_cast<std::uint32_t>(n);
+    for (std::uint64_t k = 0; k < n; ++k) {
+      const std::uint64_t o = k * kPiece;
+      pieces_.push_back(Piece{j.write, static_cast<std::uint8_t*>(j.buf) + o, std::min(kPiece, j.bytes - o),
+                              j.off + o, j.seq});
+    }
+    piece_cv_.notify_all();
+  }
+}
+
+void NvmeQueue::work() {
+  for (;;) {
+    Piece p;
+    {
+      std::unique_lock<std::mutex> g(mu_);
+      piece_cv_.wait(g, [&] { return stop_ || !pieces_.empty(); });
+      if (pieces_.empty()) return;
+      p = pieces_.front();
+      pieces_.pop_front();
+    }
+    bool ok = true;
+    for (std::uint64_t done = 0; ok && done < p.bytes;) {
+      const ssize_t k = p.write ? pwrite(fd_, p.buf + done, p.bytes - done, static_cast<off_t>(p.off + done))
+                                : pread(fd_, p.buf + done, p.bytes - done, static_cast<off_t>(p.off + done));
+      if (k <= 0) ok = false;
       else done += static_cast<std::uint64_t>(k);
     }
-    {
-      std::lock_guard<std::mutex> g(mu_);
-      if (!err.empty()) error_ = err;
-      done_ = j.seq;
-    }
-    __atomic_store_n(const_cast<std::uint32_t*>(flag_), static_cast<std::uint32_t>(j.seq), __ATOMIC_RELEASE);
-    done_cv_.notify_all();
+    piece_done(p.seq, ok);
   }
+}
+
+// A job is complete when its last piece lands; the published watermark is
+// the highest seq below which every job is complete.
+void NvmeQueue::piece_done(std::uint64_t seq, bool ok) {
+  std::uint64_t mark = 0;
+  {
+    std::lock_guard<std::mutex> g(mu_);
+    if (!ok) error_ = "NVMe tier I/O failed";
+    if (--remaining_[seq] == 0) remaining_.erase(seq);
+    // open = being dispatched or with pieces in flight (remaining_), or still queued (q_)
+    const std::uint64_t oldest_open = remaining_.empty() ? submitted_ + 1 : remaining_.begin()->first;
+    const std::uint64_t first_queued = q_.empty() ? submitted_ + 1 : q_.front().seq;
+    mark = std::min(oldest_open, first_queued) - 1;
+    if (mark <= done_) return;
+    done_ = mark;
+  }
+  __atomic_store_n(const_cast<std::uint32_t*>(flag_), static_cast<std::uint32_t>(mark), __ATOMIC_RELEASE);
+  done_cv_.notify_all();
 }
 
 }  // namespace tcb

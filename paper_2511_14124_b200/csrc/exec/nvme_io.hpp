@@ -1,15 +1,19 @@
-// Asynchronous NVMe tier I/O. One worker thread executes jobs in FIFO order:
-// wait for the CUDA events the job depends on (the copy that filled a pinned
-// buffer, or the copies that last read it), then pread/pwrite between the
-// pinned buffer and the tier file, then publish the job's sequence number in
-// a mapped host word. GPU streams that consume the bytes wait on that word
-// with cuStreamWaitValue32 (no host thread blocks in the iteration, no CUDA
-// host callbacks); host code waits on a condition variable.
+// Asynchronous NVMe tier I/O. A dispatcher thread takes jobs in FIFO order,
+// waits for the CUDA events each depends on (the copy that filled a pinned
+// buffer, or the copies that last read it) and splits it into pieces that a
+// pool of worker threads pread/pwrite concurrently (queue depth for real
+// NVMe, parallel copies for the page cache). Jobs complete in any order; the
+// in-order completion watermark is published in a mapped host word. GPU
+// streams that consume the bytes wait on that word with cuStreamWaitValue32
+// (no host thread blocks in the iteration, no CUDA host callbacks); host
+// code waits on a condition variable.
 #pragma once
 
 #include <condition_variable>
 #include <cstdint>
 #include <deque>
+#include <map>
+#include <string>
 #include <mutex>
 #include <thread>
 #include <vector>
@@ -46,10 +50,21 @@ class NvmeQueue {
     std::uint64_t bytes, off, seq;
     std::vector<cudaEvent_t> waits;
   };
+  struct Piece {
+    bool write;
+    std::uint8_t* buf;
+    std::uint64_t bytes, off, seq;
+  };
   std::uint64_t submit(Job j);
-  void run();
+  void dispatch();
+  void work();
+  void piece_done(std::uint64_t seq, bool ok);
 
   int device_, fd_;
+  std::deque<Piece> pieces_;
+  std::map<std::uint64_t, std::uint32_t> remaining_;  // seq -> pieces left
+  std::condition_variable piece_cv_;
+  std::vector<std::thread> workers_;
   volatile std::uint32_t* flag_ = nullptr;  // mapped pinned word: last completed seq
   void* flag_dev_ = nullptr;
   void* wait_fn_ = nullptr;                 // cuStreamWaitValue32
@@ -59,7 +74,7 @@ class NvmeQueue {
   std::uint64_t submitted_ = 0, done_ = 0, bytes_read_ = 0, bytes_written_ = 0;
   bool stop_ = false;
   std::string error_;
-  std::thread worker_;
+  std::thread dispatcher_;
 };
 
 }  // namespace tcb
