@@ -435,7 +435,8 @@ void Executor::host_wait_all(const SlotSync& y) {
 std::uint64_t Executor::nvme_read_async(TensorRec& r, void* dst, SlotSync& target) {
   std::vector<cudaEvent_t> waits(target.readers.begin(), target.readers.end());
   if (target.writer) waits.push_back(target.writer);
-  const std::uint64_t k = io_->submit_read(dst, r.bytes, r.nvme_off, std::move(waits));
+  const std::uint64_t k =
+      io_->submit_read(dst, r.bytes, r.nvme_off, std::move(waits), std::max(target.io_read, target.io_write));
   target = SlotSync{};
   target.io_write = k;
   stats_.nvme_read_bytes += r.bytes;
@@ -447,7 +448,7 @@ std::uint64_t Executor::nvme_read_async(TensorRec& r, void* dst, SlotSync& targe
 std::uint64_t Executor::nvme_write_async(TensorRec& r, const void* src, SlotSync& source) {
   std::vector<cudaEvent_t> waits;
   if (source.writer) waits.push_back(source.writer);
-  const std::uint64_t k = io_->submit_write(src, r.bytes, r.nvme_off, std::move(waits));
+  const std::uint64_t k = io_->submit_write(src, r.bytes, r.nvme_off, std::move(waits), source.io_write);
   source.io_read = k;
   r.nvme_valid = true;
   stats_.nvme_write_bytes += r.bytes;

@@ -4,6 +4,7 @@
 #include <unistd.h>
 
 #include <algorithm>
+#include <cstdio>
 #include <cstdlib>
 
 #include "capi_common.hpp"
@@ -74,23 +75,30 @@ NvmeQueue::~NvmeQueue() {
   if (flag_) cudaFreeHost(const_cast<std::uint32_t*>(flag_));
 }
 
+static const bool kDebug = std::getenv("TC_NVME_DEBUG") != nullptr;
+
 std::uint64_t NvmeQueue::submit(Job j) {
   std::lock_guard<std::mutex> g(mu_);
   if (!error_.empty()) throw DeviceError(TC_EIO, error_);
   j.seq = ++submitted_;
+  if (kDebug)
+    std::fprintf(stderr, "[nvme] submit %llu %s %llu B @%llu waits=%zu\n", static_cast<unsigned long long>(j.seq),
+                 j.write ? "W" : "R", static_cast<unsigned long long>(j.bytes), static_cast<unsigned long long>(j.off),
+                 j.waits.size());
   (j.write ? bytes_written_ : bytes_read_) += j.bytes;
   q_.push_back(std::move(j));
   cv_.notify_one();
   return submitted_;
 }
 
-std::uint64_t NvmeQueue::submit_read(void* dst, std::uint64_t bytes, std::uint64_t off, std::vector<cudaEvent_t> w) {
-  return submit(Job{false, dst, bytes, off, 0, std::move(w)});
+std::uint64_t NvmeQueue::submit_read(void* dst, std::uint64_t bytes, std::uint64_t off, std::vector<cudaEvent_t> w,
+                                     std::uint64_t after) {
+  return submit(Job{false, dst, bytes, off, 0, std::move(w), after});
 }
 
 std::uint64_t NvmeQueue::submit_write(const void* src, std::uint64_t bytes, std::uint64_t off,
-                                      std::vector<cudaEvent_t> w) {
-  return submit(Job{true, const_cast<void*>(src), bytes, off, 0, std::move(w)});
+                                      std::vector<cudaEvent_t> w, std::uint64_t after) {
+  return submit(Job{true, const_cast<void*>(src), bytes, off, 0, std::move(w), after});
 }
 
 void NvmeQueue::stream_wait(cudaStream_t s, std::uint64_t seq) {
@@ -102,6 +110,7 @@ void NvmeQueue::stream_wait(cudaStream_t s, std::uint64_t seq) {
 }
 
 void NvmeQueue::wait(std::uint64_t seq) {
+  if (kDebug) std::fprintf(stderr, "[nvme] host wait %llu\n", static_cast<unsigned long long>(seq));
   std::unique_lock<std::mutex> g(mu_);
   done_cv_.wait(g, [&] { return done_ >= seq || !error_.empty(); });
   if (!error_.empty()) throw DeviceError(TC_EIO, error_);
@@ -129,7 +138,8 @@ void NvmeQueue::dispatch() {
     bool ok = true;
     for (cudaEvent_t e : j.waits)
       if (e && cudaEventSynchronize(e) != cudaSuccess) ok = false;
-    std::lock_guard<std::mutex> g(mu_);
+    std::unique_lock<std::mutex> g(mu_);
+    if (j.after) done_cv_.wait(g, [&] { return done_ >= j.after || !error_.empty(); });  // same-buffer order
     if (!ok) error_ = "event wait failed before NVMe I/O";
     const std::uint64_t n = std::max<std::uint64_t>(1, (j.bytes + kPiece - 1) / kPiece);
     remaining_[j.seq] = static_cast<std::uint32_t>(n);
@@ -175,6 +185,9 @@ void NvmeQueue::piece_done(std::uint64_t seq, bool ok) {
     const std::uint64_t oldest_open = remaining_.empty() ? submitted_ + 1 : remaining_.begin()->first;
     const std::uint64_t first_queued = q_.empty() ? submitted_ + 1 : q_.front().seq;
     mark = std::min(oldest_open, first_queued) - 1;
+    if (kDebug)
+      std::fprintf(stderr, "[nvme] piece of %llu done; mark %llu (done %llu)\n", static_cast<unsigned long long>(seq),
+                   static_cast<unsigned long long>(mark), static_cast<unsigned long long>(done_));
     if (mark <= done_) return;
     done_ = mark;
   }

@@ -32,9 +32,12 @@ class NvmeQueue {
   NvmeQueue(int device, int fd);
   ~NvmeQueue();
 
-  std::uint64_t submit_read(void* dst, std::uint64_t bytes, std::uint64_t file_off, std::vector<cudaEvent_t> waits);
+  // `after`: an earlier job on the same host buffer that must be complete
+  // before this one starts (jobs otherwise run concurrently in the pool).
+  std::uint64_t submit_read(void* dst, std::uint64_t bytes, std::uint64_t file_off, std::vector<cudaEvent_t> waits,
+                            std::uint64_t after = 0);
   std::uint64_t submit_write(const void* src, std::uint64_t bytes, std::uint64_t file_off,
-                             std::vector<cudaEvent_t> waits);
+                             std::vector<cudaEvent_t> waits, std::uint64_t after = 0);
   void stream_wait(cudaStream_t s, std::uint64_t seq);  // GPU-side wait for job `seq`
   void wait(std::uint64_t seq);                         // host-side wait
   void wait_all() { wait(submitted_); }
@@ -49,6 +52,7 @@ class NvmeQueue {
     void* buf;
     std::uint64_t bytes, off, seq;
     std::vector<cudaEvent_t> waits;
+    std::uint64_t after = 0;
   };
   struct Piece {
     bool write;

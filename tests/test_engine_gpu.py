@@ -323,3 +323,17 @@ def test_zero3_p2p_fused_exchange_equals_nccl_world1(tmpd):
     for x, y in zip(a, b):
         for u, v in zip(x, y):
             assert np.array_equal(u, v)
+
+
+def test_many_iterations_pipelined(tmpd):
+    """Eight pipelined iterations (events recycled by generation, NVMe jobs and
+    optimizer stages reused across iterations): bytes and updates stay exact."""
+    rng = random.Random(77)
+    p = [(i + 1, rng.choice([4096, 8192]), "p16", i) for i in range(8)]
+    s, o = cases.with_states(p, order=[x[0] for x in p][::-1])
+    tr = cases.write_trace(os.path.join(tmpd, "long.jsonl"), p + s, cases.fwd_bwd([x[0] for x in p], 5.0) + o, 8)
+    total = sum(x[1] for x in p)
+    m = cases.write_machine(os.path.join(tmpd, "long_m.json"), int(0.6 * total), int(0.5 * total) + 3 * total)
+    for pol in ("tencache", "tencache+opt"):
+        st = check_engine(tr, m, {"policy": pol}, iters=8, nvme_dir=tmpd, stages=3)
+        assert st["param_hits"] == P.run(tr, m, {"policy": pol})["param_hits"]
