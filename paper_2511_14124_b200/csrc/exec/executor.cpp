@@ -210,6 +210,7 @@ Executor::Executor(const std::string& trace_path, const std::string& machine_pat
   if (!std::getenv("TC_SYNC_NVME")) {
     try {
       io_ = std::make_unique<NvmeQueue>(device_, nvme_fd_);
+      TCB_CK(cudaStreamCreateWithFlags(&io_join_, cudaStreamNonBlocking));
     } catch (const std::exception&) {
       io_.reset();  // no stream memory operations: synchronous NVMe I/O
     }
@@ -306,6 +307,7 @@ Executor::~Executor() {
   if (opt_) cudaStreamDestroy(opt_);
   if (h2d_opt_) cudaStreamDestroy(h2d_opt_);
   if (d2h_opt_) cudaStreamDestroy(d2h_opt_);
+  if (io_join_) cudaStreamDestroy(io_join_);
   if (compute_owned_) cudaStreamDestroy(compute_owned_);
   if (nvme_fd_ >= 0) close(nvme_fd_);
   if (z3_) {
@@ -430,13 +432,27 @@ void Executor::host_wait_all(const SlotSync& y) {
   if (io_) io_->wait(std::max(y.io_read, y.io_write));
 }
 
+// The I/O worker waits on events later, on its own thread; an event it names
+// could meanwhile be recycled and re-recorded behind GPU work that waits on
+// that very job. So a job never names slot events directly: they are joined
+// on a side stream into ONE fresh event of the current generation, which is
+// harvested only after all of that generation's jobs completed.
+std::vector<cudaEvent_t> Executor::io_deps(std::vector<cudaEvent_t> deps) {
+  std::erase(deps, nullptr);
+  if (deps.empty()) return {};
+  for (cudaEvent_t e : deps) TCB_CK(cudaStreamWaitEvent(io_join_, e, 0));
+  cudaEvent_t j = events_.get(false);
+  TCB_CK(cudaEventRecord(j, io_join_));
+  return {j};
+}
+
 // NVMe -> host buffer once every GPU op touching `target` is done; returns the
 // job (GPU consumers wait on it through target.io_write).
 std::uint64_t Executor::nvme_read_async(TensorRec& r, void* dst, SlotSync& target) {
   std::vector<cudaEvent_t> waits(target.readers.begin(), target.readers.end());
   if (target.writer) waits.push_back(target.writer);
-  const std::uint64_t k =
-      io_->submit_read(dst, r.bytes, r.nvme_off, std::move(waits), std::max(target.io_read, target.io_write));
+  const std::uint64_t k = io_->submit_read(dst, r.bytes, r.nvme_off, io_deps(std::move(waits)),
+                                           std::max(target.io_read, target.io_write));
   target = SlotSync{};
   target.io_write = k;
   stats_.nvme_read_bytes += r.bytes;
@@ -448,7 +464,7 @@ std::uint64_t Executor::nvme_read_async(TensorRec& r, void* dst, SlotSync& targe
 std::uint64_t Executor::nvme_write_async(TensorRec& r, const void* src, SlotSync& source) {
   std::vector<cudaEvent_t> waits;
   if (source.writer) waits.push_back(source.writer);
-  const std::uint64_t k = io_->submit_write(src, r.bytes, r.nvme_off, std::move(waits), source.io_write);
+  const std::uint64_t k = io_->submit_write(src, r.bytes, r.nvme_off, io_deps(std::move(waits)), source.io_write);
   source.io_read = k;
   r.nvme_valid = true;
   stats_.nvme_write_bytes += r.bytes;

@@ -306,6 +306,8 @@ class Executor {
   std::size_t n_accesses_ = 0, access_cursor_ = 0;
   int nvme_fd_ = -1;
   std::unique_ptr<NvmeQueue> io_;  // async NVMe tier I/O (null: synchronous fallback)
+  cudaStream_t io_join_ = nullptr;  // joins a job's dependencies into one event of the submitting generation
+  std::vector<cudaEvent_t> io_deps(std::vector<cudaEvent_t> deps);
   std::uint64_t nvme_read_async(TensorRec& r, void* dst, SlotSync& target);
   std::uint64_t nvme_write_async(TensorRec& r, const void* src, SlotSync& source);
   std::string nvme_path_;
