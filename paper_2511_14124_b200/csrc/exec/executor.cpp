@@ -7,8 +7,11 @@
 #include <unistd.h>
 
 #include <algorithm>
+#include <chrono>
+#include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <thread>
 
 namespace tcb {
 
@@ -451,8 +454,11 @@ std::vector<cudaEvent_t> Executor::io_deps(std::vector<cudaEvent_t> deps) {
 std::uint64_t Executor::nvme_read_async(TensorRec& r, void* dst, SlotSync& target) {
   std::vector<cudaEvent_t> waits(target.readers.begin(), target.readers.end());
   if (target.writer) waits.push_back(target.writer);
+  // after: the buffer's previous job and the extent's previous job (a pending
+  // write of the same tensor must land before it is read back)
   const std::uint64_t k = io_->submit_read(dst, r.bytes, r.nvme_off, io_deps(std::move(waits)),
-                                           std::max(target.io_read, target.io_write));
+                                           std::max({target.io_read, target.io_write, r.nvme_job}));
+  r.nvme_job = k;
   target = SlotSync{};
   target.io_write = k;
   stats_.nvme_read_bytes += r.bytes;
@@ -464,7 +470,9 @@ std::uint64_t Executor::nvme_read_async(TensorRec& r, void* dst, SlotSync& targe
 std::uint64_t Executor::nvme_write_async(TensorRec& r, const void* src, SlotSync& source) {
   std::vector<cudaEvent_t> waits;
   if (source.writer) waits.push_back(source.writer);
-  const std::uint64_t k = io_->submit_write(src, r.bytes, r.nvme_off, io_deps(std::move(waits)), source.io_write);
+  const std::uint64_t k =
+      io_->submit_write(src, r.bytes, r.nvme_off, io_deps(std::move(waits)), std::max(source.io_write, r.nvme_job));
+  r.nvme_job = k;
   source.io_read = k;
   r.nvme_valid = true;
   stats_.nvme_write_bytes += r.bytes;
@@ -1086,7 +1094,31 @@ void Executor::finish_iteration() {
 void Executor::harvest_front() {
   IterRecord rec = std::move(pending_.front());
   pending_.pop_front();
-  for (cudaEvent_t f : rec.fences) TCB_CK(cudaEventSynchronize(f));
+  {  // fences, with a diagnostic if an iteration does not drain
+    static const char* const kStreams[] = {"h2d", "d2h", "opt", "h2d_opt", "d2h_opt", "compute"};
+    const auto t0 = std::chrono::steady_clock::now();
+    for (bool reported = false;;) {
+      bool all = true;
+      std::string pending;
+      for (std::size_t i = 0; i < rec.fences.size(); ++i) {
+        const cudaError_t q = cudaEventQuery(rec.fences[i]);
+        if (q == cudaErrorNotReady) {
+          all = false;
+          pending += std::string(" ") + (i < 6 ? kStreams[i] : "?");
+        } else if (q != cudaSuccess) {
+          TCB_CK(q);
+        }
+      }
+      if (all) break;
+      if (!reported && std::chrono::steady_clock::now() - t0 > std::chrono::seconds(30)) {
+        reported = true;
+        std::fprintf(stderr, "[executor] iteration %llu not drained after 30 s; streams pending:%s; %s\n",
+                     static_cast<unsigned long long>(rec.gen), pending.c_str(),
+                     io_ ? io_->describe().c_str() : "no nvme queue");
+      }
+      std::this_thread::sleep_for(std::chrono::microseconds(50));
+    }
+  }
   if (io_) io_->wait(rec.io_seq);  // no queued job may still name an event we recycle
   float ms = 0;
   phase_ms_.clear();

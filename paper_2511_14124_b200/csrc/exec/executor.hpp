@@ -121,6 +121,7 @@ struct TensorRec {
   std::uint32_t slot = 0;          // physical slot index within its class
   std::uint64_t nvme_off = 0;
   bool nvme_valid = false;         // NVMe extent holds the current bytes
+  std::uint64_t nvme_job = 0;      // last async job on its NVMe extent (file-side ordering)
   std::uint8_t* grad = nullptr;    // params: bf16 gradient in HBM
   int issued_since_access = 0;     // P7b hit definition
   cudaEvent_t arrival = nullptr;   // last H2D into its GPU slot (for on-time)

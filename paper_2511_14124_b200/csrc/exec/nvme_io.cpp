@@ -4,6 +4,7 @@
 #include <unistd.h>
 
 #include <algorithm>
+#include <chrono>
 #include <cstdio>
 #include <cstdlib>
 
@@ -109,10 +110,29 @@ void NvmeQueue::stream_wait(cudaStream_t s, std::uint64_t seq) {
   if (r != CUDA_SUCCESS) throw DeviceError(TC_ECUDA, "cuStreamWaitValue32 failed");
 }
 
+std::string NvmeQueue::describe() {
+  std::lock_guard<std::mutex> g(mu_);
+  std::string s = "nvme queue: submitted " + std::to_string(submitted_) + " done " + std::to_string(done_) +
+                  " flag " + std::to_string(*flag_) + " queued " + std::to_string(q_.size()) + " pieces " +
+                  std::to_string(pieces_.size()) + " dispatching " + std::to_string(dispatching_) + " phase " +
+                  std::to_string(dispatch_phase_) + " open:";
+  int k = 0;
+  for (const auto& [seq, left] : remaining_) {
+    if (k++ > 8) break;
+    s += " " + std::to_string(seq) + "(" + std::to_string(static_cast<int>(left)) + ")";
+  }
+  return s;
+}
+
 void NvmeQueue::wait(std::uint64_t seq) {
   if (kDebug) std::fprintf(stderr, "[nvme] host wait %llu\n", static_cast<unsigned long long>(seq));
   std::unique_lock<std::mutex> g(mu_);
-  done_cv_.wait(g, [&] { return done_ >= seq || !error_.empty(); });
+  while (!done_cv_.wait_for(g, std::chrono::seconds(30), [&] { return done_ >= seq || !error_.empty(); })) {
+    g.unlock();
+    std::fprintf(stderr, "[nvme] still waiting for job %llu: %s\n", static_cast<unsigned long long>(seq),
+                 describe().c_str());
+    g.lock();
+  }
   if (!error_.empty()) throw DeviceError(TC_EIO, error_);
 }
 
@@ -134,12 +154,16 @@ void NvmeQueue::dispatch() {
       j = std::move(q_.front());
       q_.pop_front();
       remaining_[j.seq] = ~0u;  // open (not yet split) until its pieces are queued
+      dispatching_ = j.seq;
+      dispatch_phase_ = 1;
     }
     bool ok = true;
     for (cudaEvent_t e : j.waits)
       if (e && cudaEventSynchronize(e) != cudaSuccess) ok = false;
     std::unique_lock<std::mutex> g(mu_);
+    dispatch_phase_ = 2;
     if (j.after) done_cv_.wait(g, [&] { return done_ >= j.after || !error_.empty(); });  // same-buffer order
+    dispatch_phase_ = 3;
     if (!ok) error_ = "event wait failed before NVMe I/O";
     const std::uint64_t n = std::max<std::uint64_t>(1, (j.bytes + kPiece - 1) / kPiece);
     remaining_[j.seq] = static_cast<std::uint32_t>(n);
@@ -176,21 +200,20 @@ void NvmeQueue::work() {
 // A job is complete when its last piece lands; the published watermark is
 // the highest seq below which every job is complete.
 void NvmeQueue::piece_done(std::uint64_t seq, bool ok) {
-  std::uint64_t mark = 0;
-  {
-    std::lock_guard<std::mutex> g(mu_);
-    if (!ok) error_ = "NVMe tier I/O failed";
-    if (--remaining_[seq] == 0) remaining_.erase(seq);
-    // open = being dispatched or with pieces in flight (remaining_), or still queued (q_)
-    const std::uint64_t oldest_open = remaining_.empty() ? submitted_ + 1 : remaining_.begin()->first;
-    const std::uint64_t first_queued = q_.empty() ? submitted_ + 1 : q_.front().seq;
-    mark = std::min(oldest_open, first_queued) - 1;
-    if (kDebug)
-      std::fprintf(stderr, "[nvme] piece of %llu done; mark %llu (done %llu)\n", static_cast<unsigned long long>(seq),
-                   static_cast<unsigned long long>(mark), static_cast<unsigned long long>(done_));
-    if (mark <= done_) return;
-    done_ = mark;
-  }
+  std::lock_guard<std::mutex> g(mu_);
+  if (!ok) error_ = "NVMe tier I/O failed";
+  if (--remaining_[seq] == 0) remaining_.erase(seq);
+  // open = being dispatched or with pieces in flight (remaining_), or still queued (q_)
+  const std::uint64_t oldest_open = remaining_.empty() ? submitted_ + 1 : remaining_.begin()->first;
+  const std::uint64_t first_queued = q_.empty() ? submitted_ + 1 : q_.front().seq;
+  const std::uint64_t mark = std::min(oldest_open, first_queued) - 1;
+  if (kDebug)
+    std::fprintf(stderr, "[nvme] piece of %llu done; mark %llu (done %llu)\n", static_cast<unsigned long long>(seq),
+                 static_cast<unsigned long long>(mark), static_cast<unsigned long long>(done_));
+  if (mark <= done_) return;
+  done_ = mark;
+  // published under the lock: two workers must never store the watermark out
+  // of order (a GPU stream waiting for a value above a regressed word hangs)
   __atomic_store_n(const_cast<std::uint32_t*>(flag_), static_cast<std::uint32_t>(mark), __ATOMIC_RELEASE);
   done_cv_.notify_all();
 }

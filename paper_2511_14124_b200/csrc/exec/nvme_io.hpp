@@ -44,6 +44,7 @@ class NvmeQueue {
   std::uint64_t done() const;
   std::uint64_t submitted() const { return submitted_; }
   std::uint64_t bytes_read() const { return bytes_read_; }
+  std::string describe();  // state dump for hang diagnostics
   std::uint64_t bytes_written() const { return bytes_written_; }
 
  private:
@@ -76,6 +77,8 @@ class NvmeQueue {
   std::condition_variable cv_, done_cv_;
   std::deque<Job> q_;
   std::uint64_t submitted_ = 0, done_ = 0, bytes_read_ = 0, bytes_written_ = 0;
+  std::uint64_t dispatching_ = 0;  // job the dispatcher is on
+  int dispatch_phase_ = 0;         // 0 idle, 1 events, 2 after, 3 split
   bool stop_ = false;
   std::string error_;
   std::thread dispatcher_;
