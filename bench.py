@@ -93,6 +93,66 @@ class ClockSampler:
                 "samples": len(self.rows)}
 
 
+def hbm_context(chunk_bytes, reps=8):
+    """Context for the in-step AdamW roofline, measured live on this GPU
+    (tools/adamw_contention.py has the full matrix): the same 28 B/elem launch
+    timed alone, and a torch HBM copy of the same bytes alone and while pinned
+    H2D + D2H copies run on other streams, as in every step. Concurrent PCIe
+    DMA lowers what any HBM-bound kernel can reach by ~20-25 % on B200."""
+    import torch
+    from paper_2511_14124_b200 import kernels as K
+    n = chunk_bytes // 2
+    st = torch.zeros(3 * n, dtype=torch.float32, device="cuda")
+    g = torch.zeros(n, dtype=torch.bfloat16, device="cuda")
+    po = torch.empty(n, dtype=torch.bfloat16, device="cuda")
+    a = torch.empty(ADAM_BYTES_PER_ELEM * n // 2, dtype=torch.uint8, device="cuda")
+    b = torch.empty_like(a)
+    ha = torch.empty(256 << 20, dtype=torch.uint8).pin_memory()
+    hb = torch.empty_like(ha).pin_memory()
+    da = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
+    db = torch.empty_like(da)
+    s_main, s_up, s_down = torch.cuda.Stream(), torch.cuda.Stream(), torch.cuda.Stream()
+
+    def pcie():
+        with torch.cuda.stream(s_up):
+            for _ in range(2):
+                da.copy_(ha, non_blocking=True)
+        with torch.cuda.stream(s_down):
+            for _ in range(2):
+                hb.copy_(db, non_blocking=True)
+
+    def timed(fn, load):
+        out = []
+        for i in range(reps):
+            torch.cuda.synchronize()
+            if load:
+                pcie()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(s_main)
+            fn(i)
+            e1.record(s_main)
+            torch.cuda.synchronize()
+            out.append(e0.elapsed_time(e1) * 1e-3)
+        return sorted(out)[len(out) // 2]
+
+    def copy(i):
+        with torch.cuda.stream(s_main):
+            b.copy_(a)
+
+    byt = ADAM_BYTES_PER_ELEM * n
+    adam_alone = timed(lambda i: K.adamw(st, g, po, 1e-4, 0.9, 0.999, 1e-8, 0.01, i + 1, stream=s_main), False)
+    adam_load = timed(lambda i: K.adamw(st, g, po, 1e-4, 0.9, 0.999, 1e-8, 0.01, i + 1, stream=s_main), True)
+    copy_alone = timed(copy, False)
+    copy_load = timed(copy, True)
+    torch.cuda.synchronize()
+    return {"adamw_alone_GBps": round(byt / adam_alone / 1e9, 1),
+            "adamw_under_pcie_GBps": round(byt / adam_load / 1e9, 1),
+            "hbm_copy_alone_GBps": round(byt / copy_alone / 1e9, 1),
+            "hbm_copy_under_pcie_GBps": round(byt / copy_load / 1e9, 1),
+            "how": "median of %d event-timed launches of the same byte count; 'under_pcie' = while 2 x 256 MiB "
+                   "pinned H2D and D2H copies run on two other streams" % reps}
+
+
 def build_c2(workdir, tokens, tflops, iters=1):
     from paper_2511_14124_b200 import traces as T
     info = T.config_c2(workdir, iterations=iters, tokens=tokens, effective_tflops=tflops)
@@ -121,6 +181,11 @@ def run_ours(args):
     if args.config == "c3":
         from paper_2511_14124_b200 import traces as T
         info = T.config_c3_rank(wd, tokens=args.tokens, effective_tflops=args.tflops)
+        cfg = {"policy": "tencache"}
+        nvme_dir = wd
+    elif args.config == "c5":
+        from paper_2511_14124_b200 import traces as T
+        info = T.config_c5_rank(wd, tokens=args.tokens, effective_tflops=args.tflops)
         cfg = {"policy": "tencache"}
         nvme_dir = wd
     elif args.config == "c4":
@@ -168,19 +233,20 @@ def run_ours(args):
     B, S = 8, args.tokens // 8
     tokens_h = torch.randint(0, 50272, (B, S), dtype=torch.int32).pin_memory()
     tokens_d = torch.empty_like(tokens_h, device="cuda")
-    e2e_steps = max(2, K // 2)
+    e2e_steps = K
     torch.cuda.synchronize()
     t0 = time.perf_counter()
     for _ in range(e2e_steps):
         tokens_d.copy_(tokens_h, non_blocking=True)
         eng.iteration(**step_kw)
-        cks = eng.access_checksums()
+        cks = eng.step_result()
     torch.cuda.synchronize()
     e2e_ms = (time.perf_counter() - t0) * 1e3 / e2e_steps
     eng.reset_stats()
 
     pk = peaks()
     hbm = pk.get("hbm_gbs", 6650.0)
+    ctx = hbm_context(info["chunk_bytes"])
     launches_per_iter = info["params"]
     elems_per_launch = st["adam_elems"] / max(1, K * launches_per_iter)
     avg_launch_ms = st["adam_ms"] / max(1, K * launches_per_iter)
@@ -200,9 +266,10 @@ def run_ours(args):
     copy_busy = st["h2d_busy_ms"] + st["d2h_busy_ms"]
     hidden = 1.0 - st["stall_ms"] / copy_busy if copy_busy else None
     prefetched = st["param_accesses"] - st["param_hits"]
-    if args.config == "c3":  # the whole shard is GPU-resident: no cache decisions, only optimizer streaming
+    if args.config in ("c3", "c5"):  # whole shard GPU-resident: no cache decisions, only optimizer streaming
         value_bytes = (st["opt_h2d_bytes"] + st["opt_d2h_bytes"]) / K
-        value_def = "optimizer-state PCIe bytes (both directions) per step / step time (C3 has no cache moves)"
+        value_def = ("optimizer-state PCIe bytes (both directions) per step / step time (the plan caches the whole "
+                     "parameter shard on the GPU: no cache moves)")
     else:
         value_bytes = dec_bytes
         value_def = ("cache-decision bytes per step (sum of non-instant TransferRequest bytes = the reference's "
@@ -220,8 +287,11 @@ def run_ours(args):
                                 "host memory (BASELINE.json configs[2])") if args.config == "c3" else
                                ("C4 rank 0 of 8: GPT-3 13B ZeRO-3 shard with GPU/CPU/NVMe tiers, NVMe via pinned "
                                 "bounce buffers (BASELINE.json configs[3]), " +
-                                ("O_DIRECT" if args.direct_io else "buffered") + f" file I/O in {args.nvme_dir}"),
-                   "model": {"c2": "opt-1.3b", "c3": "llama2-7b", "c4": "gpt3-13b"}[args.config],
+                                ("O_DIRECT" if args.direct_io else "buffered") + f" file I/O in {args.nvme_dir}")
+                               if args.config == "c4" else
+                               ("C5 rank 0 of 8: Llama-3 70B ZeRO-3 shard, parameters and optimizer states homed in "
+                                "pinned host memory, GPU cache sized from 180 GB HBM (BASELINE.json configs[4])"),
+                   "model": {"c2": "opt-1.3b", "c3": "llama2-7b", "c4": "gpt3-13b", "c5": "llama3-70b"}[args.config],
                    "chunks": info["params"], "chunk_bytes": info["chunk_bytes"],
                    "gpu_param_chunks": info["gpu_chunks"], "policy": cfg["policy"],
                    "tokens_per_step": args.tokens, "compute": args.compute,
@@ -247,7 +317,7 @@ def run_ours(args):
         "phase_ms_last_step": {k: round(v, 2) for k, v in zip(("forward", "backward", "optimizer_compute_stream",
                                                                 "iteration_all_streams"), phases)},
         "optimizer_hoisted": not args.no_hoist, "optimizer_prestaged": not args.no_prestage,
-        "roofline": {"kernel": "fused AdamW (adamw_kernel<2>)", "bound": "hbm", "achieved": round(achieved, 1),
+        "roofline": {"kernel": "fused AdamW (adamw_tma_kernel<256,3>, TMA bulk pipeline)", "bound": "hbm", "achieved": round(achieved, 1),
                      "peak": hbm, "unit": "GB/s", "frac": round(achieved / hbm, 4), "traffic": traffic,
                      "algorithmic_bytes_per_launch": int(ADAM_BYTES_PER_ELEM * elems_per_launch),
                      "avg_launch_us": round(avg_launch_ms * 1e3, 2),
@@ -257,7 +327,9 @@ def run_ours(args):
                                         "note": "first CTA start to last CTA end (%globaltimer) of the same launches; "
                                                 "the event-timed avg_launch_us adds queueing behind other streams"}
                                        if st["adam_spans"] else None),
-                     "peak_source": "MEASURED_PEAKS.json hbm_gbs (burst copy)"},
+                     "peak_source": "MEASURED_PEAKS.json hbm_gbs (burst copy)",
+                     "context": dict(ctx, frac_alone=round(ctx["adamw_alone_GBps"] / hbm, 4),
+                                     frac_in_step_vs_copy_under_pcie=round(achieved / ctx["hbm_copy_under_pcie_GBps"], 4))},
         "e2e": {"value": round(value_bytes / (e2e_ms * 1e-3) / 1e9, 4), "unit": "GB/s", "ms_per_step": round(e2e_ms, 3),
                 "h2d_bytes_per_step": int(tokens_h.numel() * 4), "d2h_bytes_per_step": int(len(cks) * 8),
                 "path": "Engine.iteration (ctypes C-ABI tc_engine_iteration), host wall clock"},
@@ -445,11 +517,13 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-hoist", action="store_true", help="run optimizer updates in place (after backward)")
     ap.add_argument("--no-prestage", action="store_true", help="no staging of optimizer states ahead of updates")
-    ap.add_argument("--config", default="c2", choices=["c2", "c3", "c4"])
+    ap.add_argument("--config", default="c2", choices=["c2", "c3", "c4", "c5"])
     ap.add_argument("--zero3", action="store_true", help="the torchrun ZeRO-3 path even at world size 1")
     ap.add_argument("--exchange", default="p2p", choices=["p2p", "nccl"],
                     help="ZeRO-3 exchange: fused peer-memory kernels (default) or NCCL + pack kernels")
-    ap.add_argument("--stages", type=int, default=12, help="HBM optimizer-state stages")
+    ap.add_argument("--stages", type=int, default=None,
+                    help="HBM optimizer-state stages (default: 128 for c3/c5, whose forward pass has no cache "
+                         "prefetches to compete with state pre-staging; 12 otherwise; profiles/r01_stage_sweep.json)")
     ap.add_argument("--gpu-spares", type=int, default=4, help="spare HBM slots per parameter class")
     ap.add_argument("--policy", default="tencache",
                     choices=["tencache", "tencache+opt", "zero-infinity", "l2l", "no-offload"],
@@ -457,20 +531,33 @@ def main():
     ap.add_argument("--nvme-dir", default="/tmp", help="directory of the NVMe tier file (c4)")
     ap.add_argument("--direct-io", action="store_true", help="O_DIRECT NVMe tier I/O")
     args = ap.parse_args()
+    if args.stages is None:
+        args.stages = 128 if args.config in ("c3", "c5") else 12
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", "1"))
+    # stdout carries exactly one JSON line: anything a library prints there
+    # (e.g. NCCL's version banner) is sent to stderr instead
+    sys.stdout.flush()
+    json_fd = os.dup(1)
+    os.dup2(2, 1)
+    out = os.fdopen(json_fd, "w")
+
+    def emit(line):
+        out.write(json.dumps(line) + "\n")
+        out.flush()
+
     if args.impl == "reference":
         if rank != 0:
             return
-        print(json.dumps(run_reference_arm(args)))
+        emit(run_reference_arm(args))
         return
     if world > 1 or args.zero3:
         from paper_2511_14124_b200 import zero3
         line = zero3.bench_rank(args)
         if rank == 0 and line:
-            print(json.dumps(line))
+            emit(line)
         return
-    print(json.dumps(run_ours(args)))
+    emit(run_ours(args))
 
 
 if __name__ == "__main__":

@@ -241,6 +241,13 @@ int tc_engine_phase_ms(tc_engine* e, double* out, size_t cap, size_t* n);
 /* checksum the fwd/bwd stand-in computed for each parameter access of the
  * last iteration (device -> host copy), in access order. */
 int tc_engine_access_checksums(tc_engine* e, uint64_t* out, size_t cap, size_t* n);
+/* The step's result without draining: the per-access checksums of the most
+ * recently enqueued iteration, copied to pinned host memory at the end of its
+ * compute stream. Waits only for that iteration's forward/backward, so its
+ * optimizer write-back tail keeps overlapping the next iteration (what a
+ * training loop's loss.item() waits for). out == NULL or cap == 0: only
+ * sets *n (no wait). TC_EARG before any iteration. */
+int tc_engine_step_result(tc_engine* e, uint64_t* out, size_t cap, size_t* n);
 
 /* ===================== ZeRO-3 exchange ================= */
 /* NCCL (libnccl.so.2 loaded at run time) unique id, to be broadcast by the

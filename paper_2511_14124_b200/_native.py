@@ -144,6 +144,7 @@ _SIGS = {
     "tc_engine_p2p_handles": ([C.c_void_p, C.c_void_p, C.c_size_t, C.POINTER(C.c_size_t)], C.c_int),
     "tc_engine_enable_p2p": ([C.c_void_p, C.c_void_p], C.c_int),
     "tc_engine_access_checksums": ([C.c_void_p, C.POINTER(C.c_uint64), C.c_size_t, C.POINTER(C.c_size_t)], C.c_int),
+    "tc_engine_step_result": ([C.c_void_p, C.POINTER(C.c_uint64), C.c_size_t, C.POINTER(C.c_size_t)], C.c_int),
 }
 
 

@@ -261,6 +261,9 @@ Executor::Executor(const std::string& trace_path, const std::string& machine_pat
   TCB_CK(cudaMalloc(&d_checksums_, 2 * std::max<std::size_t>(n_accesses_, 1) * sizeof(std::uint64_t)));
   TCB_CK(cudaMalloc(&d_span_, 2 * 2 * std::max<std::size_t>(recs_.size(), 1) * sizeof(unsigned long long)));
   h_checksums_.assign(n_accesses_, 0);
+  TCB_CK(cudaHostAlloc(&h_result_, 2 * std::max<std::size_t>(n_accesses_, 1) * sizeof(std::uint64_t),
+                       cudaHostAllocDefault));
+  for (auto& e : result_ev_) TCB_CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
   TCB_CK(cudaStreamCreateWithFlags(&h2d_, cudaStreamNonBlocking));
   TCB_CK(cudaStreamCreateWithFlags(&d2h_, cudaStreamNonBlocking));
   int lo_prio = 0, hi_prio = 0;  // the fused AdamW gets the highest stream priority
@@ -304,6 +307,9 @@ Executor::~Executor() {
     for (auto* p : v) cudaFree(p);
   if (grads_) cudaFree(grads_);
   if (d_checksums_) cudaFree(d_checksums_);
+  if (h_result_) cudaFreeHost(h_result_);
+  for (auto& e : result_ev_)
+    if (e) cudaEventDestroy(e);
   if (d_span_) cudaFree(d_span_);
   if (h2d_) cudaStreamDestroy(h2d_);
   if (d2h_) cudaStreamDestroy(d2h_);
@@ -1063,6 +1069,15 @@ void Executor::iteration(const StepOptions& so, cudaStream_t compute) {
 // (fences awaited, timings summed, its events recycled) so that iteration
 // t+1's forward pass overlaps iteration t's optimizer write-back tail.
 void Executor::finish_iteration() {
+  {  // the step's result (per-access checksums) to pinned host memory, on the
+     // compute stream: step_result() waits for this, not for the optimizer tail
+    const std::size_t k = static_cast<std::size_t>(events_.generation() % 2), na = std::max<std::size_t>(n_accesses_, 1);
+    TCB_CK(cudaMemcpyAsync(h_result_ + k * na, cks_base_, n_accesses_ * sizeof(std::uint64_t),
+                           cudaMemcpyDeviceToHost, compute_));
+    TCB_CK(cudaEventRecord(result_ev_[k], compute_));
+    result_gen_ = events_.generation();
+    have_result_ = true;
+  }
   IterRecord rec;
   rec.gen = events_.generation();
   rec.copies = std::move(copies_);
@@ -1425,6 +1440,15 @@ const std::vector<std::uint64_t>& Executor::access_checksums() {
   return h_checksums_;
 }
 
+std::vector<std::uint64_t> Executor::step_result() {
+  TCB_CK(cudaSetDevice(device_));
+  if (!have_result_) throw DeviceError(TC_EARG, "no iteration has been run");
+  const std::size_t k = static_cast<std::size_t>(result_gen_ % 2);
+  TCB_CK(cudaEventSynchronize(result_ev_[k]));
+  const std::uint64_t* r = h_result_ + k * std::max<std::size_t>(n_accesses_, 1);
+  return std::vector<std::uint64_t>(r, r + n_accesses_);
+}
+
 void Executor::seed(std::uint64_t seed) {
   TCB_CK(cudaSetDevice(device_));
   sync();
@@ -1703,6 +1727,20 @@ int tc_engine_stats_reset(tc_engine* e) {
     if (!e) return set_error(TC_EARG, "null argument");
     e->ex->sync();
     e->ex->reset_stats();
+    return TC_OK;
+  })
+}
+
+int tc_engine_step_result(tc_engine* e, uint64_t* out, size_t cap, size_t* n) {
+  TC_GUARD({
+    if (!e) return set_error(TC_EARG, "null argument");
+    if (out == nullptr || cap == 0) {  // size query: no wait
+      if (n) *n = e->ex->n_accesses();
+      return TC_OK;
+    }
+    const auto v = e->ex->step_result();
+    for (std::size_t i = 0; i < v.size() && i < cap; ++i) out[i] = v[i];
+    if (n) *n = v.size();
     return TC_OK;
   })
 }

@@ -196,6 +196,10 @@ class Executor {
   tc_engine_stats stats() const { return stats_; }
   void reset_stats() { stats_ = tc_engine_stats{}; }
   const std::vector<std::uint64_t>& access_checksums();
+  // The last enqueued iteration's per-access checksums; waits only for its
+  // compute stream (forward/backward), not its optimizer write-back tail.
+  std::vector<std::uint64_t> step_result();
+  std::size_t n_accesses() const { return n_accesses_; }
   const std::vector<double>& phase_ms() const { return phase_ms_; }
   const tencache::IPolicy& policy() const { return *policy_; }
 
@@ -297,6 +301,10 @@ class Executor {
   std::uint8_t* grads_ = nullptr;
   std::uint64_t* d_checksums_ = nullptr;  // two buffers of n_accesses_ (iteration parity)
   std::vector<std::uint64_t> h_checksums_;
+  std::uint64_t* h_result_ = nullptr;  // pinned, two buffers of n_accesses_ (iteration parity)
+  cudaEvent_t result_ev_[2] = {nullptr, nullptr};
+  std::uint64_t result_gen_ = 0;
+  bool have_result_ = false;
   std::uint64_t* cks_base_ = nullptr;
   unsigned long long* d_span_ = nullptr;  // 2 parities x n_params x (min, max) AdamW kernel spans
   unsigned long long* span_base_ = nullptr;

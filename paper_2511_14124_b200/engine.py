@@ -88,6 +88,15 @@ class Engine:
         N.check(N.lib().tc_engine_access_checksums(self._h, out, n.value, C.byref(n)))
         return np.array(out[: n.value], dtype=np.uint64)
 
+    def step_result(self):
+        """The last enqueued iteration's per-access checksums (its result);
+        waits for its forward/backward only, not the optimizer write-back."""
+        n = C.c_size_t()
+        N.check(N.lib().tc_engine_step_result(self._h, None, 0, C.byref(n)))
+        out = (C.c_uint64 * max(n.value, 1))()
+        N.check(N.lib().tc_engine_step_result(self._h, out, n.value, C.byref(n)))
+        return np.array(out[: n.value], dtype=np.uint64)
+
     def close(self):
         if self._h:
             N.lib().tc_engine_destroy(self._h)

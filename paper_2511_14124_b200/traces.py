@@ -226,3 +226,30 @@ def config_c3_rank(workdir: str, world: int = 1, rank: int = 0, iterations: int 
     write_machine(mp, n * S, n * 6 * S + 1, pinned_overrides=links)
     info.update({"trace": tp, "machine": mp, "gpu_chunks": n, "params": n, "chunk_bytes": S, "layout": lay})
     return info
+
+
+def config_c5_rank(workdir: str, world: int = 8, rank: int = 0, iterations: int = 1, tokens: int = 16384,
+                   effective_tflops: float = 700.0, hbm_cache_bytes: int | None = None, links: dict | None = None):
+    """BASELINE configs[4] (Llama-3 70B ZeRO-3, full parameter + optimizer
+    offload on 8xB200), one rank's shard: parameters and optimizer states both
+    have their home in pinned host memory; the GPU parameter cache is sized
+    from the 180 GB of HBM per GPU (minus activations/workspace, stated below),
+    so the TenCache plan (Alg. 2) caches the whole 17.6 GB parameter shard on
+    the GPU and the 105.9 GB of optimizer states stream through pinned host
+    memory every step."""
+    import os
+    from . import zero3 as Z
+    lay = Z.shard_layout("llama3-70b", world)
+    tp = os.path.join(workdir, f"c5_w{world}_r{rank}.jsonl")
+    info = Z.write_rank_trace(tp, lay, rank, iterations, tokens, effective_tflops)
+    S, n = lay.chunk_bytes, lay.chunks_per_rank
+    # 180 GB HBM - gradients of the shard (n*S) - 12 optimizer stages (72 S)
+    # - 40 GB activations/workspace headroom
+    gpu_cap = hbm_cache_bytes if hbm_cache_bytes is not None else 180_000_000_000 - n * S - 72 * S - 40_000_000_000
+    gpu_chunks = min(n, gpu_cap // S)
+    mp = os.path.join(workdir, "c5_machine.json")
+    links = links or {"cpu->gpu": 55.3, "gpu->cpu": 57.0}
+    write_machine(mp, gpu_chunks * S, (n - gpu_chunks) * S + n * 6 * S + 1, pinned_overrides=links)
+    info.update({"trace": tp, "machine": mp, "gpu_chunks": gpu_chunks, "params": n, "chunk_bytes": S,
+                 "layout": lay, "hbm_cache_bytes": gpu_cap})
+    return info

@@ -50,10 +50,15 @@ def check_engine(tr, m, cfg, iters=2, nvme_dir="", hoist=True, prestage=True, st
     accesses = [i for s in steps if s["phase"] != "o" for i in s["ids"]]
     opt_steps = [s["ids"] for s in steps if s["phase"] == "o"]
     for it in range(1, iters + 1):
+        if it == 1:
+            with pytest.raises(RuntimeError):
+                e.step_result()  # no iteration yet
         e.iteration(hoist=hoist, prestage=prestage, **HP)
+        early = e.step_result()  # waits for the compute stream only
         got = e.access_checksums()
         want = np.array([ref.checksum(params[i]) for i in accesses], dtype=np.uint64)
         assert np.array_equal(got, want), f"iteration {it}: access checksum mismatch"
+        assert np.array_equal(early, want), f"iteration {it}: step_result mismatch"
         for sid, pid in opt_steps:
             n = tensors[pid]["size"] // 2
             st = states[sid]
