@@ -84,6 +84,12 @@ def build(verbose=False, jobs=None):
         if r.returncode != 0:
             raise RuntimeError(f"link failed:\n{r.stderr}")
         os.replace(LIB + ".tmp", LIB)
+    cli = os.path.join(OUT, "tencache_sim")
+    cli_src = os.path.join(CSRC, "cli", "tencache_sim.cpp")
+    if not os.path.exists(cli) or os.path.getmtime(cli) < max(os.path.getmtime(cli_src), os.path.getmtime(LIB)):
+        _compile(["g++"] + CXXFLAGS + INCS + [cli_src, "-o", cli + ".tmp", f"-L{OUT}", "-l:libtencache_b200.so",
+                                             "-Wl,-rpath,$ORIGIN", "-pthread"], cli_src)
+        os.replace(cli + ".tmp", cli)
     if verbose:
         for l in logs:
             if l.strip():

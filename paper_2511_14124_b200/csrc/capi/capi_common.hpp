@@ -13,6 +13,9 @@ namespace tcb {
 int set_error(int code, const std::string& msg);
 tencache::RunConfig parse_run_config(const char* cfg_json);
 tencache::MachineConfig machine_from(const char* path);
+// SimReport as JSON text (exact rationals as "n/d" strings); shared by tc_run,
+// tc_sweep and the tencache_sim CLI.
+std::string report_json_text(const tencache::SimReport& r);
 
 // Runtime failures of the data plane (CUDA / NCCL / file I/O).
 struct DeviceError : std::runtime_error {

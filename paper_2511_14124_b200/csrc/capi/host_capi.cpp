@@ -133,6 +133,8 @@ json report_json(const SimReport& r) {
 
 }  // namespace
 
+std::string tcb::report_json_text(const SimReport& r) { return report_json(r).dump(); }
+
 extern "C" {
 
 const char* tc_last_error(void) { return g_last_error.c_str(); }
