@@ -524,7 +524,10 @@ def main():
     ap.add_argument("--stages", type=int, default=None,
                     help="HBM optimizer-state stages (default: 128 for c3/c5, whose forward pass has no cache "
                          "prefetches to compete with state pre-staging; 12 otherwise; profiles/r01_stage_sweep.json)")
-    ap.add_argument("--gpu-spares", type=int, default=4, help="spare HBM slots per parameter class")
+    ap.add_argument("--gpu-spares", type=int, default=16,
+                    help="spare HBM slots per parameter class beyond the policy's logical GPU tier: a prefetch "
+                         "lands in a free slot while the slot's previous occupant is still waiting for its "
+                         "update and eviction (profiles/r01_ring_sweep.json)")
     ap.add_argument("--policy", default="tencache",
                     choices=["tencache", "tencache+opt", "zero-infinity", "l2l", "no-offload"],
                     help="C2 cache policy on the same executor (the paper's baselines for comparison)")

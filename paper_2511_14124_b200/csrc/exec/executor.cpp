@@ -210,6 +210,9 @@ Executor::Executor(const std::string& trace_path, const std::string& machine_pat
   if (ftruncate(nvme_fd_, static_cast<off_t>(off)) != 0) throw DeviceError(TC_EIO, "ftruncate NVMe tier file");
   if (const char* c = std::getenv("TC_CHECKSUM_CTAS")) checksum_ctas_ = std::atoi(c);
   if (const char* c = std::getenv("TC_OPT_YIELD")) opt_yield_ = std::atoi(c) != 0;
+  if (const char* c = std::getenv("TC_PRESTAGE_FWD")) prestage_fwd_override_ = std::atoi(c);
+  if (const char* c = std::getenv("TC_PRESTAGE_GATE")) prestage_gate_ = std::atoi(c) != 0;
+  if (const char* c = std::getenv("TC_EDGE_FILL")) edge_fill_ = std::atoi(c) != 0;
   if (!std::getenv("TC_SYNC_NVME")) {
     try {
       io_ = std::make_unique<NvmeQueue>(device_, nvme_fd_);
@@ -1022,7 +1025,14 @@ void Executor::iteration(const StepOptions& so, cudaStream_t compute) {
   staged_.clear();
   for (std::size_t i = 0; i < n; ++i)
     for (std::size_t j : after[i]) prestage_order_.push_back(index_of(trace_.steps[j].tensor_ids.front()));
-  if (so_.prestage) refill_stages(forward_prestage_budget(hooks));
+  if (so_.prestage) {
+    // The forward refill of iteration t+1 is issued while iteration t's tail
+    // may still be moving; gated, it starts only after t's last cache
+    // prefetch so it never competes with t's critical H2D traffic.
+    if (prestage_gate_ && last_h2d_) TCB_CK(cudaStreamWaitEvent(h2d_opt_, last_h2d_, 0));
+    refill_stages(prestage_fwd_override_ >= 0 ? static_cast<std::size_t>(prestage_fwd_override_)
+                                              : forward_prestage_budget(hooks));
+  }
   auto mark = [&] {
     cudaEvent_t e = events_.get(true);
     TCB_CK(cudaEventRecord(e, compute));
@@ -1035,6 +1045,14 @@ void Executor::iteration(const StepOptions& so, cudaStream_t compute) {
       const TraceStep& step = trace_.steps[h.step];
       if (step.phase != prev) {
         mark();
+        if (prev == Phase::Forward && so_.prestage && edge_fill_) {
+          // Forward -> backward edge: the forward's cache prefetches are all
+          // issued and no backward prefetch exists yet, so the H2D link
+          // would idle until the first update frees a stage. Fill the rest
+          // of the ring, starting when the forward's last prefetch lands.
+          if (last_h2d_) TCB_CK(cudaStreamWaitEvent(h2d_opt_, last_h2d_, 0));
+          refill_stages(stage_.size());
+        }
         prev = step.phase;
       }
       nvtxRangePushA(step.phase == Phase::Forward ? "tencache.fwd" : step.phase == Phase::Backward ? "tencache.bwd"

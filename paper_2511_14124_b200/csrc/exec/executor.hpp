@@ -294,6 +294,9 @@ class Executor {
   std::vector<std::int32_t> prestage_order_;              // states in update (hoist) order
   std::size_t prestage_next_ = 0;
   std::size_t prestage_lookahead_ = 2;
+  int prestage_fwd_override_ = -1;  // TC_PRESTAGE_FWD: states staged for the forward (-1: bandwidth model)
+  bool prestage_gate_ = false;      // TC_PRESTAGE_GATE: forward refill waits for the last cache prefetch
+  bool edge_fill_ = false;          // TC_EDGE_FILL: fill the stage ring at the forward->backward edge (neutral on C2)
   std::uint64_t stage_bytes_ = 0;
   std::map<std::uint64_t, std::vector<std::uint8_t*>> pout_scratch_;  // HBM updated-param scratch
   std::map<std::uint64_t, std::vector<SlotSync>> pout_sync_;
