@@ -92,6 +92,8 @@ int tc_adamw_split(float* p32, float* m, float* v, const void* grad, void* param
                    double beta1, double beta2, double eps, double weight_decay, int64_t step, float grad_scale,
                    void* stream) {
   if (step < 1) return set_error(TC_EARG, "tc_adamw: step must be >= 1");
+  if (n == 0) return TC_OK;
+  if (!p32 || !m || !v || !grad) return set_error(TC_EARG, "tc_adamw: null buffer");
   const AdamScalars s = adam_scalars(lr, beta1, beta2, eps, weight_decay, step);
   return cuda_status(launch_adamw(p32, m, v, static_cast<const std::uint16_t*>(grad),
                                   static_cast<std::uint16_t*>(param_out), n, s, grad_scale, as_stream(stream)),
