@@ -205,7 +205,9 @@ typedef struct {
   int compute_mode;    /* 0: checksum only, 1: checksum + spin for compute_us*batch_scale */
   int spin_ctas;
   int flags;           /* bit 0: run optimizer updates in place (no hoisting after the last access);
-                          bit 1: no pre-staging of optimizer states ahead of their updates */
+                          bit 1: no pre-staging of optimizer states ahead of their updates;
+                          bit 2: last iteration: no prologue of the next one (its decisions and
+                                 first state loads are otherwise enqueued at the end of this call) */
 } tc_step_options;
 
 /* One training iteration: every trace step in order, policy decisions at the

@@ -213,6 +213,7 @@ Executor::Executor(const std::string& trace_path, const std::string& machine_pat
   if (const char* c = std::getenv("TC_PRESTAGE_FWD")) prestage_fwd_override_ = std::atoi(c);
   if (const char* c = std::getenv("TC_PRESTAGE_GATE")) prestage_gate_ = std::atoi(c) != 0;
   if (const char* c = std::getenv("TC_EDGE_FILL")) edge_fill_ = std::atoi(c) != 0;
+  if (const char* c = std::getenv("TC_LOOKAHEAD")) lookahead_ = std::atoi(c) != 0;
   if (!std::getenv("TC_SYNC_NVME")) {
     try {
       io_ = std::make_unique<NvmeQueue>(device_, nvme_fd_);
@@ -807,7 +808,8 @@ void Executor::optimizer_work(TensorRec& s, TensorRec& p) {
     b = it != staged_.end() ? it->second : stage_state(s);
     staged_.erase(index_of(s.id));
     stg = stage_[b];
-    TCB_CK(cudaStreamWaitEvent(opt_, stage_sync_[b].writer, 0));
+    // (null once a drain between the prologue's staging and this update completed it)
+    if (stage_sync_[b].writer) TCB_CK(cudaStreamWaitEvent(opt_, stage_sync_[b].writer, 0));
   }
   if (p.grad_ready) TCB_CK(cudaStreamWaitEvent(opt_, p.grad_ready, 0));
   std::uint8_t* pout;
@@ -1000,7 +1002,7 @@ void Executor::iteration(const StepOptions& so, cudaStream_t compute) {
   so_ = so;
   ++adam_step_;
   access_cursor_ = 0;
-  events_.next_generation();
+  if (!ahead_) events_.next_generation();  // else the prologue already opened this generation
   cks_base_ = d_checksums_ + (events_.generation() % 2) * std::max<std::size_t>(n_accesses_, 1);
   {  // per-launch AdamW spans: mins start at UINT64_MAX (0xff bytes), maxes at 0
     const std::size_t cap = std::max<std::size_t>(recs_.size(), 1);
@@ -1010,21 +1012,27 @@ void Executor::iteration(const StepOptions& so, cudaStream_t compute) {
     TCB_CK(cudaMemsetAsync(span_base_ + cap, 0, cap * sizeof(unsigned long long), opt_));
   }
   TCB_CK(cudaMemsetAsync(cks_base_, 0, std::max<std::size_t>(n_accesses_, 1) * sizeof(std::uint64_t), compute));
-  nvtxRangePushA("tencache.decide");
-  const std::vector<Hook> hooks = decide_iteration();
-  nvtxRangePop();
+  std::vector<Hook> hooks;
+  if (ahead_) {  // decided (and its first states staged) at the end of the previous iteration
+    hooks = std::move(*ahead_);
+    ahead_.reset();
+  } else {
+    nvtxRangePushA("tencache.decide");
+    hooks = decide_iteration();
+    nvtxRangePop();
+    drop_staged();
+  }
   const std::vector<std::size_t> hoist = plan_hoisting(hooks);
   const std::size_t n = trace_.steps.size();
   std::vector<std::vector<std::size_t>> after(n);
   for (std::size_t j = 0; j < n; ++j)
     if (hoist[j] < n) after[hoist[j]].push_back(j);
   // Hoisted updates in execution order; their states can be staged any time
-  // (no decision touches them before their update, plan_hoisting).
-  prestage_order_.clear();
-  prestage_next_ = 0;
-  staged_.clear();
-  for (std::size_t i = 0; i < n; ++i)
-    for (std::size_t j : after[i]) prestage_order_.push_back(index_of(trace_.steps[j].tensor_ids.front()));
+  // (no decision touches them before their update, plan_hoisting). States
+  // staged by the prologue are skipped by refill_stages.
+  set_prestage_order(hooks, hoist);
+  // states the prologue staged come first in the order: continue after them
+  while (prestage_next_ < prestage_order_.size() && staged_.count(prestage_order_[prestage_next_])) ++prestage_next_;
   if (so_.prestage) {
     // The forward refill of iteration t+1 is issued while iteration t's tail
     // may still be moving; gated, it starts only after t's last cache
@@ -1080,6 +1088,45 @@ void Executor::iteration(const StepOptions& so, cudaStream_t compute) {
   }
   mark();
   finish_iteration();
+  if (lookahead_ && so_.prestage && so_.prologue) prologue_next();
+}
+
+// Hoisted updates of an iteration in execution order = the order their
+// states are staged.
+void Executor::set_prestage_order(const std::vector<Hook>& hooks, const std::vector<std::size_t>& hoist) {
+  const std::size_t n = trace_.steps.size();
+  std::vector<std::vector<std::size_t>> after(n);
+  for (std::size_t j = 0; j < n; ++j)
+    if (hoist[j] < n) after[hoist[j]].push_back(j);
+  prestage_order_.clear();
+  prestage_next_ = 0;
+  for (std::size_t i = 0; i < n; ++i)
+    for (std::size_t j : after[i]) prestage_order_.push_back(index_of(trace_.steps[j].tensor_ids.front()));
+}
+
+// Release stages holding pre-staged states (their bytes may be stale: the
+// caller wrote or re-seeded tensors); the decisions made ahead stay valid.
+void Executor::drop_staged() {
+  for (auto& [idx, b] : staged_) stage_free_.push_back(b);
+  staged_.clear();
+}
+
+// Prologue of iteration t+1, run at the end of iteration t's enqueue: its
+// decisions are made now (the request stream is timing-independent,
+// engine.hpp:49-51) and its first optimizer states are staged right behind
+// t's last state loads, so the H2D link works through t's write-back tail
+// whether or not the caller waits for t's result before calling iteration()
+// again (tc_engine_step_result waits for t's compute stream).
+void Executor::prologue_next() {
+  events_.next_generation();
+  nvtxRangePushA("tencache.decide");
+  std::vector<Hook> hooks = decide_iteration();
+  nvtxRangePop();
+  set_prestage_order(hooks, plan_hoisting(hooks));
+  if (prestage_gate_ && last_h2d_) TCB_CK(cudaStreamWaitEvent(h2d_opt_, last_h2d_, 0));
+  refill_stages(prestage_fwd_override_ >= 0 ? static_cast<std::size_t>(prestage_fwd_override_)
+                                            : forward_prestage_budget(hooks));
+  ahead_ = std::move(hooks);
 }
 
 // The iteration is enqueued; nothing waits for it here. Its timing records
@@ -1470,6 +1517,7 @@ std::vector<std::uint64_t> Executor::step_result() {
 void Executor::seed(std::uint64_t seed) {
   TCB_CK(cudaSetDevice(device_));
   sync();
+  drop_staged();  // stages 0/1 are scratch below, and every state changes
   std::uint8_t* tmp = stage_[0];  // >= 6x the largest parameter
   for (auto& p : recs_) {
     if (p.is_state) continue;
@@ -1544,6 +1592,7 @@ void Executor::write_tensor(TensorId id, const void* src, std::uint64_t bytes) {
   sync();
   TensorRec& r = rec(id);
   if (bytes != r.bytes) throw std::invalid_argument("write_tensor: size mismatch");
+  if (r.is_state) drop_staged();
   if (r.tier == PTier::Gpu) {
     TCB_CK(cudaMemcpy(where(r), src, bytes, cudaMemcpyHostToDevice));
     r.nvme_valid = false;
@@ -1657,6 +1706,7 @@ int tc_engine_iteration(tc_engine* e, const tc_step_options* so, void* compute_s
       o.spin_ctas = so->spin_ctas;
       o.hoist_optimizer = (so->flags & 1) == 0;
       o.prestage = (so->flags & 2) == 0;
+      o.prologue = (so->flags & 4) == 0;
     }
     e->ex->iteration(o, static_cast<cudaStream_t>(compute_stream));
     return TC_OK;

@@ -25,6 +25,7 @@
 #include <deque>
 #include <map>
 #include <memory>
+#include <optional>
 #include <string>
 #include <fstream>
 #include <unordered_map>
@@ -173,6 +174,7 @@ struct StepOptions {
   int spin_ctas = 1;
   bool hoist_optimizer = true;  // run each update right after its parameter's last fwd/bwd access
   bool prestage = true;         // stage optimizer states into HBM ahead of their updates
+  bool prologue = true;         // enqueue the next iteration's decisions + first state loads at the end
 };
 
 class Executor {
@@ -257,6 +259,9 @@ class Executor {
   std::size_t stage_state(TensorRec& s);
   void refill_stages(std::size_t want_staged);
   std::size_t forward_prestage_budget(const std::vector<Hook>& hooks) const;
+  void set_prestage_order(const std::vector<Hook>& hooks, const std::vector<std::size_t>& hoist);
+  void drop_staged();
+  void prologue_next();
   void wait_barriers(cudaStream_t cs);
   void finish_iteration();
   struct IterRecord {
@@ -296,6 +301,8 @@ class Executor {
   std::size_t prestage_lookahead_ = 2;
   int prestage_fwd_override_ = -1;  // TC_PRESTAGE_FWD: states staged for the forward (-1: bandwidth model)
   bool prestage_gate_ = false;      // TC_PRESTAGE_GATE: forward refill waits for the last cache prefetch
+  bool lookahead_ = true;           // TC_LOOKAHEAD: decide + pre-stage iteration t+1 at the end of t
+  std::optional<std::vector<Hook>> ahead_;
   bool edge_fill_ = false;          // TC_EDGE_FILL: fill the stage ring at the forward->backward edge (neutral on C2)
   std::uint64_t stage_bytes_ = 0;
   std::map<std::uint64_t, std::vector<std::uint8_t*>> pout_scratch_;  // HBM updated-param scratch

@@ -53,8 +53,11 @@ class Engine:
 
     # -- execution --------------------------------------------------------
     def iteration(self, lr=1e-4, beta1=0.9, beta2=0.999, eps=1e-8, weight_decay=0.01, grad_scale=1.0,
-                  compute_mode=0, spin_ctas=1, stream=None, hoist=True, prestage=True):
-        flags = (0 if hoist else 1) | (0 if prestage else 2)
+                  compute_mode=0, spin_ctas=1, stream=None, hoist=True, prestage=True, last=False):
+        """One training iteration (enqueued). last=True: no prologue of the
+        next iteration (its decisions and first optimizer-state loads are
+        otherwise enqueued behind this one)."""
+        flags = (0 if hoist else 1) | (0 if prestage else 2) | (4 if last else 0)
         so = N.tc_step_options(lr, beta1, beta2, eps, weight_decay, grad_scale, compute_mode, spin_ctas, flags)
         N.check(N.lib().tc_engine_iteration(self._h, C.byref(so), C.c_void_p(stream or 0)))
 

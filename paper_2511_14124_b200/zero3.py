@@ -185,7 +185,8 @@ def bench_rank(args):
     cfg = {"policy": "tencache"}
     rep = P.run(tp, mp, cfg)
     dec_bytes = sum(rep["transfer_bytes"].values())
-    eng = Engine(tp, mp, cfg, device=local, nvme_dir=wd)
+    eng = Engine(tp, mp, cfg, device=local, nvme_dir=wd, opt_stage_slots=args.stages,
+                 gpu_spare_slots=args.gpu_spares)
     eng.seed(rank)
     enable(eng, layout, rank, world, exchange=args.exchange)
     stream = torch.cuda.current_stream()
@@ -198,8 +199,8 @@ def bench_rank(args):
     torch.cuda.synchronize()
     s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     s.record(stream)
-    for _ in range(args.steps):
-        eng.iteration(**kw)
+    for k in range(args.steps):
+        eng.iteration(last=k == args.steps - 1, **kw)
     eng.sync()
     e.record(stream)
     torch.cuda.synchronize()
@@ -219,9 +220,9 @@ def bench_rank(args):
     e2e_steps = args.steps
     dist.barrier()
     t0 = time.perf_counter()
-    for _ in range(e2e_steps):
+    for k in range(e2e_steps):
         tok_d.copy_(tok_h, non_blocking=True)
-        eng.iteration(**kw)
+        eng.iteration(last=k == e2e_steps - 1, **kw)
         cks = eng.step_result()
     torch.cuda.synchronize()
     e2e_ms = torch.tensor([(time.perf_counter() - t0) * 1e3 / e2e_steps], device="cuda")

@@ -53,7 +53,7 @@ def check_engine(tr, m, cfg, iters=2, nvme_dir="", hoist=True, prestage=True, st
         if it == 1:
             with pytest.raises(RuntimeError):
                 e.step_result()  # no iteration yet
-        e.iteration(hoist=hoist, prestage=prestage, **HP)
+        e.iteration(hoist=hoist, prestage=prestage, last=it == iters, **HP)
         early = e.step_result()  # waits for the compute stream only
         got = e.access_checksums()
         want = np.array([ref.checksum(params[i]) for i in accesses], dtype=np.uint64)
@@ -167,14 +167,17 @@ def test_comparison_policies_on_the_executor(tmpd, pol, k):
 def test_chunk_trace_c2_mini(tmpd):
     plan = T.plan_chunks("opt-1.3b", world=64, rank=5, chunks_per_layer=2)
     tp = os.path.join(tmpd, "c2mini.jsonl")
-    info = T.write_chunk_trace(tp, plan, iterations=2, tokens=64)
+    info = T.write_chunk_trace(tp, plan, iterations=3, tokens=64)
     S, n = plan.chunk_bytes, plan.n_chunks
     g = int(0.4 * n)
     mp = T.write_machine(os.path.join(tmpd, "m.json"), g * S, (n - g) * S + n * 6 * S)
-    st = check_engine(tp, mp, {"policy": "tencache"}, iters=2)
+    st = check_engine(tp, mp, {"policy": "tencache"}, iters=3)
     rep = P.run(tp, mp, {"policy": "tencache"})
     assert st["param_hits"] == rep["param_hits"]
     assert st["h2d_bytes"] > 0 and st["d2h_bytes"] > 0
+    # every state crosses PCIe exactly once each way per iteration (the next
+    # iteration's prologue staging included, none re-staged or dropped)
+    assert st["opt_h2d_bytes"] == 3 * n * 6 * S and st["opt_d2h_bytes"] == 3 * n * 6 * S
 
 
 def test_zero3_exchange_world1(tmpd):
