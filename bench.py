@@ -128,6 +128,7 @@ def hbm_context(chunk_bytes, reps=8):
             if load:
                 pcie()
             e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            K.spin(300.0, 1, stream=s_main)  # the host enqueues the launch before the GPU reaches e0
             e0.record(s_main)
             fn(i)
             e1.record(s_main)
@@ -149,8 +150,9 @@ def hbm_context(chunk_bytes, reps=8):
             "adamw_under_pcie_GBps": round(byt / adam_load / 1e9, 1),
             "hbm_copy_alone_GBps": round(byt / copy_alone / 1e9, 1),
             "hbm_copy_under_pcie_GBps": round(byt / copy_load / 1e9, 1),
-            "how": "median of %d event-timed launches of the same byte count; 'under_pcie' = while 2 x 256 MiB "
-                   "pinned H2D and D2H copies run on two other streams" % reps}
+            "how": "median of %d event-timed launches of the same byte count, each behind a 300 us spin so host "
+                   "submission latency is excluded; 'under_pcie' = while 2 x 256 MiB pinned H2D and D2H copies run "
+                   "on two other streams" % reps}
 
 
 def build_c2(workdir, tokens, tflops, iters=1):
@@ -338,7 +340,7 @@ def run_ours(args):
     }
     del eng
     if not args.no_cpu_baseline and args.config == "c2":
-        line["cpu_baseline"] = cpu_baseline(info, cfg, dec_bytes)
+        line["cpu_baseline"] = cpu_baseline_full(args)
     line["clocks"] = clk.summary()
     return line
 
@@ -464,42 +466,18 @@ def run_reference_arm(args):
             "e2e": {"value": round(v, 4), "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
 
 
-def cpu_baseline(info, cfg, dec_bytes):
-    """Bounded sample of the reference CPU path on this host: one iteration of
-    reference decisions (oracle/_ref IPolicy) + AdamW on 4 state chunks (port,
-    all threads) + memcpy of the decision bytes, scaled to a full step."""
-    import numpy as np
-    from oracle import ref
-    S, n = info["chunk_bytes"], info["params"]
-    ns_iter, _ = ref.time_decisions(info["trace"], info["machine"], cfg, iterations=2)
-    k = S // 2
-    st = np.zeros(3 * k, np.float32)  # touched below: no first-touch page faults inside the timing
-    st[:k] = 0.02
-    g = np.full(k, 0x3A83, np.uint16)  # bf16 ~1e-3 (a normal value: no denormal slow paths on the host)
-    ref.adamw(st[:k], st[k:2 * k], st[2 * k:], g, 1e-4, 0.9, 0.999, 1e-8, 0.01, 1)
-    reps = 4
-    t0 = time.perf_counter()
-    for t in range(1, reps + 1):
-        ref.adamw(st[:k], st[k:2 * k], st[2 * k:], g, 1e-4, 0.9, 0.999, 1e-8, 0.01, t)
-    adam_s = (time.perf_counter() - t0) / reps
-    a = np.ones(S, np.uint8)
-    b = np.ones(S, np.uint8)
-    ref.memcpy(b, a, S)
-    t0 = time.perf_counter()
-    for _ in range(4):
-        ref.memcpy(b, a, S)
-    cp_s = (time.perf_counter() - t0) / 4
-    compute_s = 0.0
-    for line in open(info["trace"]):
-        r = json.loads(line)
-        if "s" in r and r["s"]["phase"] != "o":
-            compute_s += r["s"]["us"] * 1e-6
-    step_s = ns_iter * 1e-9 + adam_s * n + cp_s * dec_bytes / S + compute_s
-    return {"value": round(dec_bytes / step_s / 1e9, 4), "unit": "GB/s", "cores": ref.threads(),
-            "kind": "reference", "ms_per_step": round(step_s * 1e3, 2),
-            "sample": f"reference IPolicy decisions for 2 C2 iterations ({ns_iter / 1e6:.2f} ms/iter) + "
-                      f"AdamW on {reps} state chunks ({adam_s * 1e3:.1f} ms each) + 4 x {S} B memcpy, "
-                      f"scaled to {n} chunks, plus the trace compute time"}
+def cpu_baseline_full(args):
+    """The reference arm's own CPU path (run_reference_arm: reference IPolicy
+    decisions from oracle/_ref, host memcpy migrations, CPU checksums, the
+    trace compute time, OpenMP AdamW on every host thread) for 2 timed C2
+    iterations after 1 warm-up, on this box's host cores."""
+    ns = argparse.Namespace(**vars(args))
+    ns.steps, ns.warmup = 2, 1
+    r = run_reference_arm(ns)
+    cb = dict(r["cpu_baseline"])
+    cb["ms_per_step"] = r["ms_per_step"]
+    cb["sample"] = "2 full C2 iterations after 1 warm-up: " + cb["sample"].split(": ", 1)[1]
+    return cb
 
 
 def main():

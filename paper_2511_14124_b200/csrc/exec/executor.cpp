@@ -779,7 +779,6 @@ std::size_t Executor::stage_state(TensorRec& s) {
   cudaEvent_t e1 = copy(h2d_opt_, stage_[b], h.ptr, s.bytes, true);
   h.sync.readers.push_back(e1);
   stage_sync_[b] = SlotSync{e1, {}};
-  stats_.opt_h2d_bytes += s.bytes;
   staged_[index_of(s.id)] = b;
   return b;
 }
@@ -807,6 +806,7 @@ void Executor::optimizer_work(TensorRec& s, TensorRec& p) {
     auto it = staged_.find(index_of(s.id));
     b = it != staged_.end() ? it->second : stage_state(s);
     staged_.erase(index_of(s.id));
+    stats_.opt_h2d_bytes += s.bytes;  // counted at the update it feeds (staging may be a prologue)
     stg = stage_[b];
     // (null once a drain between the prologue's staging and this update completed it)
     if (stage_sync_[b].writer) TCB_CK(cudaStreamWaitEvent(opt_, stage_sync_[b].writer, 0));

@@ -31,6 +31,7 @@ def timeit(name, fn, nbytes, clean=True):
             flush.max()
         torch.cuda.synchronize()
         s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        K.spin(300.0)  # host submission latency stays outside the events
         s.record()
         fn(i)
         e.record()
@@ -60,4 +61,5 @@ big = torch.empty(6 * S, dtype=torch.uint8, device="cuda")
 timeit("checksum_6S", lambda i: K.checksum(big, cks), 6 * S, clean=False)
 print(json.dumps(res))
 os.makedirs("gpurun_out", exist_ok=True)
-json.dump(res, open("gpurun_out/kernels_alone.json", "w"), indent=1)
+if os.environ.get("KALONE_OUT", "1") == "1":
+    json.dump(res, open("gpurun_out/kernels_alone.json", "w"), indent=1)
