@@ -33,6 +33,8 @@ cudaError_t launch_pack(const PackSeg* segs, std::uint32_t n, std::uint64_t tota
 cudaError_t launch_checksum(const void* data, std::uint64_t bytes, unsigned long long* out, cudaStream_t st,
                             int max_ctas = 0);
 cudaError_t launch_spin(std::uint64_t ns, int ctas, cudaStream_t st);
+// Diagnostic: one thread writes %globaltimer (ns) to *out when the stream reaches it.
+cudaError_t launch_stamp(unsigned long long* out, cudaStream_t st);
 // Deterministic N(0, sigma) bf16 fill (counter-based RNG keyed by seed, stream).
 cudaError_t launch_fill_normal_bf16(std::uint16_t* out, std::uint64_t n, float sigma, std::uint64_t seed,
                                     std::uint64_t stream_id, cudaStream_t st);

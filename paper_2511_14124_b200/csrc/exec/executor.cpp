@@ -214,6 +214,7 @@ Executor::Executor(const std::string& trace_path, const std::string& machine_pat
   if (const char* c = std::getenv("TC_PRESTAGE_GATE")) prestage_gate_ = std::atoi(c) != 0;
   if (const char* c = std::getenv("TC_EDGE_FILL")) edge_fill_ = std::atoi(c) != 0;
   if (const char* c = std::getenv("TC_LOOKAHEAD")) lookahead_ = std::atoi(c) != 0;
+  if (const char* c = std::getenv("TC_ADAM_STAMPS")) adam_stamps_ = std::atoi(c) != 0;
   if (!std::getenv("TC_SYNC_NVME")) {
     try {
       io_ = std::make_unique<NvmeQueue>(device_, nvme_fd_);
@@ -263,7 +264,7 @@ Executor::Executor(const std::string& trace_path, const std::string& machine_pat
   for (const auto& s : trace_.steps)
     if (s.phase != Phase::OptimizerUpdate) n_accesses_ += s.tensor_ids.size();
   TCB_CK(cudaMalloc(&d_checksums_, 2 * std::max<std::size_t>(n_accesses_, 1) * sizeof(std::uint64_t)));
-  TCB_CK(cudaMalloc(&d_span_, 2 * 2 * std::max<std::size_t>(recs_.size(), 1) * sizeof(unsigned long long)));
+  TCB_CK(cudaMalloc(&d_span_, 2 * 4 * std::max<std::size_t>(recs_.size(), 1) * sizeof(unsigned long long)));
   h_checksums_.assign(n_accesses_, 0);
   TCB_CK(cudaHostAlloc(&h_result_, 2 * std::max<std::size_t>(n_accesses_, 1) * sizeof(std::uint64_t),
                        cudaHostAllocDefault));
@@ -293,6 +294,10 @@ Executor::Executor(const std::string& trace_path, const std::string& machine_pat
 }
 
 Executor::~Executor() {
+  if (adam_stamps_ && stamps_)
+    std::fprintf(stderr, "[tencache] AdamW launches: %.0f: stream reaches it -> first CTA %.2f us, "
+                 "last CTA end -> next op %.2f us (avg)\n",
+                 static_cast<double>(stamps_), stamp_pre_ns_ / stamps_ * 1e-3, stamp_post_ns_ / stamps_ * 1e-3);
   cudaSetDevice(device_);
   try {
     drain();
@@ -837,8 +842,10 @@ void Executor::optimizer_work(TensorRec& s, TensorRec& p) {
     smax = span_base_ + cap + span_cursor_;
     ++span_cursor_;
   }
+  if (adam_stamps_ && smin) TCB_CK(launch_stamp(smin + 2 * cap, opt_));
   TCB_CK(launch_adamw(st, st + n, st + 2 * n, reinterpret_cast<const std::uint16_t*>(p.grad),
                       reinterpret_cast<std::uint16_t*>(pout), n, sc, so_.grad_scale, opt_, smin, smax));
+  if (adam_stamps_ && smin) TCB_CK(launch_stamp(smin + 3 * cap, opt_));
   TCB_CK(cudaEventRecord(a1, opt_));
   adam_.emplace_back(a0, a1);
   ++stats_.kernel_launches;
@@ -1006,7 +1013,7 @@ void Executor::iteration(const StepOptions& so, cudaStream_t compute) {
   cks_base_ = d_checksums_ + (events_.generation() % 2) * std::max<std::size_t>(n_accesses_, 1);
   {  // per-launch AdamW spans: mins start at UINT64_MAX (0xff bytes), maxes at 0
     const std::size_t cap = std::max<std::size_t>(recs_.size(), 1);
-    span_base_ = d_span_ + (events_.generation() % 2) * 2 * cap;
+    span_base_ = d_span_ + (events_.generation() % 2) * 4 * cap;  // [min | max | pre stamp | post stamp]
     span_cursor_ = 0;
     TCB_CK(cudaMemsetAsync(span_base_, 0xff, cap * sizeof(unsigned long long), opt_));
     TCB_CK(cudaMemsetAsync(span_base_ + cap, 0, cap * sizeof(unsigned long long), opt_));
@@ -1253,13 +1260,18 @@ void Executor::harvest_front() {
                     n_accesses_ * sizeof(std::uint64_t), cudaMemcpyDeviceToHost));
   if (rec.spans) {
     const std::size_t cap = std::max<std::size_t>(recs_.size(), 1);
-    std::vector<unsigned long long> sp(2 * cap);
-    TCB_CK(cudaMemcpy(sp.data(), d_span_ + rec.cks_buf * 2 * cap, sp.size() * sizeof(unsigned long long),
+    std::vector<unsigned long long> sp(4 * cap);
+    TCB_CK(cudaMemcpy(sp.data(), d_span_ + rec.cks_buf * 4 * cap, sp.size() * sizeof(unsigned long long),
                       cudaMemcpyDeviceToHost));
     for (std::size_t k = 0; k < rec.spans; ++k)
       if (sp[cap + k] > sp[k]) {
         stats_.adam_span_ms += static_cast<double>(sp[cap + k] - sp[k]) * 1e-6;
         ++stats_.adam_spans;
+        if (adam_stamps_ && sp[2 * cap + k] && sp[3 * cap + k] >= sp[cap + k]) {
+          stamp_pre_ns_ += static_cast<double>(sp[k]) - static_cast<double>(sp[2 * cap + k]);
+          stamp_post_ns_ += static_cast<double>(sp[3 * cap + k] - sp[cap + k]);
+          ++stamps_;
+        }
       }
   }
   scrub(rec.gen);

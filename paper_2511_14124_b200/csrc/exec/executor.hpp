@@ -301,6 +301,8 @@ class Executor {
   std::size_t prestage_lookahead_ = 2;
   int prestage_fwd_override_ = -1;  // TC_PRESTAGE_FWD: states staged for the forward (-1: bandwidth model)
   bool prestage_gate_ = false;      // TC_PRESTAGE_GATE: forward refill waits for the last cache prefetch
+  bool adam_stamps_ = false;        // TC_ADAM_STAMPS: %globaltimer stamps around each AdamW (diagnostic)
+  double stamp_pre_ns_ = 0, stamp_post_ns_ = 0, stamps_ = 0;
   bool lookahead_ = true;           // TC_LOOKAHEAD: decide + pre-stage iteration t+1 at the end of t
   std::optional<std::vector<Hook>> ahead_;
   bool edge_fill_ = false;          // TC_EDGE_FILL: fill the stage ring at the forward->backward edge (neutral on C2)
