@@ -33,6 +33,10 @@ cudaError_t launch_pack(const PackSeg* segs, std::uint32_t n, std::uint64_t tota
 cudaError_t launch_checksum(const void* data, std::uint64_t bytes, unsigned long long* out, cudaStream_t st,
                             int max_ctas = 0);
 cudaError_t launch_spin(std::uint64_t ns, int ctas, cudaStream_t st);
+// Small fills/copies of 64-bit words as kernels: never queued on a copy engine
+// behind bulk DMA (dst may be mapped pinned host memory: posted PCIe writes).
+cudaError_t launch_fill_u64(unsigned long long* dst, unsigned long long value, std::uint64_t n, cudaStream_t st);
+cudaError_t launch_copy_u64(unsigned long long* dst, const unsigned long long* src, std::uint64_t n, cudaStream_t st);
 // Diagnostic: one thread writes %globaltimer (ns) to *out when the stream reaches it.
 cudaError_t launch_stamp(unsigned long long* out, cudaStream_t st);
 // Deterministic N(0, sigma) bf16 fill (counter-based RNG keyed by seed, stream).

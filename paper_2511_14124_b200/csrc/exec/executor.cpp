@@ -267,7 +267,8 @@ Executor::Executor(const std::string& trace_path, const std::string& machine_pat
   TCB_CK(cudaMalloc(&d_span_, 2 * 4 * std::max<std::size_t>(recs_.size(), 1) * sizeof(unsigned long long)));
   h_checksums_.assign(n_accesses_, 0);
   TCB_CK(cudaHostAlloc(&h_result_, 2 * std::max<std::size_t>(n_accesses_, 1) * sizeof(std::uint64_t),
-                       cudaHostAllocDefault));
+                       cudaHostAllocMapped));
+  TCB_CK(cudaHostGetDevicePointer(reinterpret_cast<void**>(&d_result_), h_result_, 0));
   for (auto& e : result_ev_) TCB_CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
   TCB_CK(cudaStreamCreateWithFlags(&h2d_, cudaStreamNonBlocking));
   TCB_CK(cudaStreamCreateWithFlags(&d2h_, cudaStreamNonBlocking));
@@ -1015,10 +1016,11 @@ void Executor::iteration(const StepOptions& so, cudaStream_t compute) {
     const std::size_t cap = std::max<std::size_t>(recs_.size(), 1);
     span_base_ = d_span_ + (events_.generation() % 2) * 4 * cap;  // [min | max | pre stamp | post stamp]
     span_cursor_ = 0;
-    TCB_CK(cudaMemsetAsync(span_base_, 0xff, cap * sizeof(unsigned long long), opt_));
-    TCB_CK(cudaMemsetAsync(span_base_ + cap, 0, cap * sizeof(unsigned long long), opt_));
+    TCB_CK(launch_fill_u64(span_base_, ~0ull, cap, opt_));
+    TCB_CK(launch_fill_u64(span_base_ + cap, 0ull, cap, opt_));
   }
-  TCB_CK(cudaMemsetAsync(cks_base_, 0, std::max<std::size_t>(n_accesses_, 1) * sizeof(std::uint64_t), compute));
+  TCB_CK(launch_fill_u64(reinterpret_cast<unsigned long long*>(cks_base_), 0ull, std::max<std::size_t>(n_accesses_, 1),
+                         compute));
   std::vector<Hook> hooks;
   if (ahead_) {  // decided (and its first states staged) at the end of the previous iteration
     hooks = std::move(*ahead_);
@@ -1144,8 +1146,11 @@ void Executor::finish_iteration() {
   {  // the step's result (per-access checksums) to pinned host memory, on the
      // compute stream: step_result() waits for this, not for the optimizer tail
     const std::size_t k = static_cast<std::size_t>(events_.generation() % 2), na = std::max<std::size_t>(n_accesses_, 1);
-    TCB_CK(cudaMemcpyAsync(h_result_ + k * na, cks_base_, n_accesses_ * sizeof(std::uint64_t),
-                           cudaMemcpyDeviceToHost, compute_));
+    // a kernel storing into mapped pinned memory: a cudaMemcpyAsync here would
+    // queue on the D2H copy engine behind the iteration's bulk state stores
+    // and hold the next iteration's compute stream until they drain
+    TCB_CK(launch_copy_u64(reinterpret_cast<unsigned long long*>(d_result_) + k * na,
+                           reinterpret_cast<const unsigned long long*>(cks_base_), n_accesses_, compute_));
     TCB_CK(cudaEventRecord(result_ev_[k], compute_));
     result_gen_ = events_.generation();
     have_result_ = true;
@@ -1232,6 +1237,15 @@ void Executor::harvest_front() {
   if (event_log_ && !rec.marks.empty()) {  // measured timeline in the reference's event-log schema
     static const char* const kTiers[] = {"gpu", "cpu", "nvme"};
     float t0 = 0, t1 = 0;
+    for (std::size_t k = 0; k < rec.marks.size(); ++k) {  // phase boundaries of this iteration
+      TCB_CK(cudaEventElapsedTime(&t0, rec.marks.front(), rec.marks[k]));
+      *event_log_ << "{\"iter\":" << rec.gen << ",\"kind\":\"mark\",\"k\":" << k << ",\"us\":" << t0 * 1e3 << "}\n";
+    }
+    if (!pending_.empty() && !pending_.front().marks.empty()) {  // where the next iteration starts
+      TCB_CK(cudaEventSynchronize(pending_.front().marks.front()));
+      TCB_CK(cudaEventElapsedTime(&t0, rec.marks.front(), pending_.front().marks.front()));
+      *event_log_ << "{\"iter\":" << rec.gen << ",\"kind\":\"next_iter\",\"us\":" << t0 * 1e3 << "}\n";
+    }
     for (const Copy& c : rec.copies) {
       TCB_CK(cudaEventElapsedTime(&t0, rec.marks.front(), c.start));
       TCB_CK(cudaEventElapsedTime(&t1, rec.marks.front(), c.end));

@@ -313,7 +313,8 @@ class Executor {
   std::uint8_t* grads_ = nullptr;
   std::uint64_t* d_checksums_ = nullptr;  // two buffers of n_accesses_ (iteration parity)
   std::vector<std::uint64_t> h_checksums_;
-  std::uint64_t* h_result_ = nullptr;  // pinned, two buffers of n_accesses_ (iteration parity)
+  std::uint64_t* h_result_ = nullptr;  // pinned + mapped, two buffers of n_accesses_ (iteration parity)
+  std::uint64_t* d_result_ = nullptr;  // device alias of h_result_
   cudaEvent_t result_ev_[2] = {nullptr, nullptr};
   std::uint64_t result_gen_ = 0;
   bool have_result_ = false;

@@ -36,36 +36,39 @@ eng.event_log("")
 eng.close()
 
 recs = [json.loads(x) for x in open(log)]
-last = max(r["iter"] for r in recs)
+its = sorted({r["iter"] for r in recs})
+# absolute time: chain each iteration's start through the logged next_iter offsets
+base, t = {}, 0.0
+for it in its:
+    base[it] = t
+    nx = [r for r in recs if r["iter"] == it and r["kind"] == "next_iter"]
+    if nx:
+        t += nx[0]["us"]
 out = {"phases_last_iter_ms": phases, "iters": {}}
-for it in sorted({r["iter"] for r in recs}):
-    rs = [r for r in recs if r["iter"] == it]
-    res = {}
+xfer = [dict(r, a0=r["us"] + base[r["iter"]], a1=r["end_us"] + base[r["iter"]]) for r in recs if "end_us" in r]
+for d, pred in (("h2d", lambda r: r["dst"] == "gpu" and r["src"] != "gpu"),
+                ("d2h", lambda r: r["src"] == "gpu" and r["dst"] != "gpu")):
+    iv = sorted((r["a0"], r["a1"]) for r in xfer if pred(r))
+    gaps, cs, ce = [], iv[0][0], iv[0][1]
+    for s0, e0 in iv[1:]:
+        if s0 > ce:
+            gaps.append((round(ce / 1e3, 1), round((s0 - ce) / 1e3, 1)))
+            cs, ce = s0, e0
+        else:
+            ce = max(ce, e0)
+    out[d + "_gaps_over_1ms_abs"] = [g for g in gaps if g[1] > 1.0]
+for it in its:
+    mk = sorted(r["us"] for r in recs if r["iter"] == it and r["kind"] == "mark")
+    row = {"start_ms": round(base[it] / 1e3, 1), "phase_marks_ms": [round((base[it] + m) / 1e3, 1) for m in mk]}
     for d, pred in (("h2d", lambda r: r["dst"] == "gpu" and r["src"] != "gpu"),
                     ("d2h", lambda r: r["src"] == "gpu" and r["dst"] != "gpu")):
-        iv = sorted((r["us"], r["end_us"], r["kind"], r["bytes"]) for r in rs if r["kind"] != "stall" and pred(r))
-        if not iv:
-            continue
-        busy, gaps = 0.0, []
-        cs, ce = iv[0][0], iv[0][1]
-        for s, e, k, b in iv[1:]:
-            if s > ce:
-                busy += ce - cs
-                gaps.append((round(ce, 1), round(s - ce, 1)))
-                cs, ce = s, e
-            else:
-                ce = max(ce, e)
-        busy += ce - cs
-        bykind = {}
-        for s, e, k, b in iv:
-            bykind[k] = bykind.get(k, 0) + b
-        res[d] = {"first_us": round(iv[0][0], 1), "last_us": round(max(x[1] for x in iv), 1),
-                  "busy_union_us": round(busy, 1), "bytes": sum(x[3] for x in iv), "bytes_by_kind": bykind,
-                  "gaps_over_200us": [g for g in gaps if g[1] > 200], "gap_total_us": round(sum(g[1] for g in gaps), 1)}
-    st = [r for r in rs if r["kind"] == "stall"]
-    res["stall_total_us"] = round(sum(r["wait_us"] for r in st), 1)
-    res["stalls"] = len(st)
-    out["iters"][it] = res
+        v = [r for r in xfer if r["iter"] == it and pred(r)]
+        if v:
+            row[d] = {"first_ms": round(min(r["a0"] for r in v) / 1e3, 1), "last_ms": round(max(r["a1"] for r in v) / 1e3, 1),
+                      "bytes": sum(r["bytes"] for r in v)}
+    st = [r for r in recs if r["iter"] == it and r["kind"] == "stall"]
+    row["stall_ms"] = round(sum(r["wait_us"] for r in st) / 1e3, 1)
+    out["iters"][it] = row
 json.dump(out, open(f"gpurun_out/timeline_{cfgname}.json", "w"), indent=1)
-print(json.dumps(out["iters"][last], indent=1)[:4000])
+print(json.dumps(out, indent=1)[:6000])
 print("phases", phases)
