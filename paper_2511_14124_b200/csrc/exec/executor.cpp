@@ -269,6 +269,9 @@ Executor::Executor(const std::string& trace_path, const std::string& machine_pat
   TCB_CK(cudaHostAlloc(&h_result_, 2 * std::max<std::size_t>(n_accesses_, 1) * sizeof(std::uint64_t),
                        cudaHostAllocMapped));
   TCB_CK(cudaHostGetDevicePointer(reinterpret_cast<void**>(&d_result_), h_result_, 0));
+  TCB_CK(cudaHostAlloc(reinterpret_cast<void**>(&h_span_), 2 * 4 * std::max<std::size_t>(recs_.size(), 1) *
+                       sizeof(unsigned long long), cudaHostAllocMapped));
+  TCB_CK(cudaHostGetDevicePointer(reinterpret_cast<void**>(&d_span_host_), h_span_, 0));
   for (auto& e : result_ev_) TCB_CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
   TCB_CK(cudaStreamCreateWithFlags(&h2d_, cudaStreamNonBlocking));
   TCB_CK(cudaStreamCreateWithFlags(&d2h_, cudaStreamNonBlocking));
@@ -318,6 +321,7 @@ Executor::~Executor() {
   if (grads_) cudaFree(grads_);
   if (d_checksums_) cudaFree(d_checksums_);
   if (h_result_) cudaFreeHost(h_result_);
+  if (h_span_) cudaFreeHost(h_span_);
   for (auto& e : result_ev_)
     if (e) cudaEventDestroy(e);
   if (d_span_) cudaFree(d_span_);
@@ -1155,6 +1159,11 @@ void Executor::finish_iteration() {
     result_gen_ = events_.generation();
     have_result_ = true;
   }
+  {  // this iteration's AdamW spans/stamps to mapped host memory, behind its last update
+    const std::size_t cap = std::max<std::size_t>(recs_.size(), 1);
+    TCB_CK(launch_copy_u64(reinterpret_cast<unsigned long long*>(d_span_host_) + (events_.generation() % 2) * 4 * cap,
+                           span_base_, 4 * cap, opt_));
+  }
   IterRecord rec;
   rec.gen = events_.generation();
   rec.copies = std::move(copies_);
@@ -1270,13 +1279,15 @@ void Executor::harvest_front() {
     TCB_CK(cudaEventElapsedTime(&ms, a0, a1));
     stats_.adam_ms += ms;
   }
-  TCB_CK(cudaMemcpy(h_checksums_.data(), d_checksums_ + rec.cks_buf * std::max<std::size_t>(n_accesses_, 1),
-                    n_accesses_ * sizeof(std::uint64_t), cudaMemcpyDeviceToHost));
+  // from the mapped copies written by kernels at the iteration's end: a
+  // synchronous cudaMemcpy here would enter the legacy stream (often the
+  // caller's compute stream) and queue on the D2H copy engine behind the
+  // next iteration's bulk state stores, stalling that stream until they drain
+  std::memcpy(h_checksums_.data(), h_result_ + rec.cks_buf * std::max<std::size_t>(n_accesses_, 1),
+              n_accesses_ * sizeof(std::uint64_t));
   if (rec.spans) {
     const std::size_t cap = std::max<std::size_t>(recs_.size(), 1);
-    std::vector<unsigned long long> sp(4 * cap);
-    TCB_CK(cudaMemcpy(sp.data(), d_span_ + rec.cks_buf * 4 * cap, sp.size() * sizeof(unsigned long long),
-                      cudaMemcpyDeviceToHost));
+    const unsigned long long* sp = h_span_ + rec.cks_buf * 4 * cap;
     for (std::size_t k = 0; k < rec.spans; ++k)
       if (sp[cap + k] > sp[k]) {
         stats_.adam_span_ms += static_cast<double>(sp[cap + k] - sp[k]) * 1e-6;

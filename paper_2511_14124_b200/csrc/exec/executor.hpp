@@ -315,6 +315,8 @@ class Executor {
   std::vector<std::uint64_t> h_checksums_;
   std::uint64_t* h_result_ = nullptr;  // pinned + mapped, two buffers of n_accesses_ (iteration parity)
   std::uint64_t* d_result_ = nullptr;  // device alias of h_result_
+  unsigned long long* h_span_ = nullptr;       // pinned + mapped copy of the AdamW span buffers (parity)
+  unsigned long long* d_span_host_ = nullptr;  // device alias of h_span_
   cudaEvent_t result_ev_[2] = {nullptr, nullptr};
   std::uint64_t result_gen_ = 0;
   bool have_result_ = false;
