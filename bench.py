@@ -534,6 +534,8 @@ def main():
         return
     if world > 1 or args.zero3:
         from paper_2511_14124_b200 import zero3
+        args.clock_sampler = ClockSampler
+        args.hbm_peak = peaks().get("hbm_gbs")
         line = zero3.bench_rank(args)
         if rank == 0 and line:
             emit(line)
