@@ -345,3 +345,45 @@ def test_many_iterations_pipelined(tmpd):
     for pol in ("tencache", "tencache+opt"):
         st = check_engine(tr, m, {"policy": pol}, iters=8, nvme_dir=tmpd, stages=3)
         assert st["param_hits"] == P.run(tr, m, {"policy": pol})["param_hits"]
+
+
+def test_back_to_back_iterations_with_prologue(tmpd):
+    """The production loop: iterations enqueued back to back (each one's
+    prologue decides and stages the next), the step result read after every
+    iteration without draining, no reads in between. Every step result and
+    the final parameters/states equal the oracle's; every state crossed PCIe
+    exactly once per direction per iteration."""
+    plan = T.plan_chunks("opt-1.3b", world=64, rank=3, chunks_per_layer=2)
+    iters = 5
+    tp = os.path.join(tmpd, "b2b.jsonl")
+    T.write_chunk_trace(tp, plan, iterations=iters, tokens=64)
+    S, n = plan.chunk_bytes, plan.n_chunks
+    g = int(0.4 * n)
+    mp = T.write_machine(os.path.join(tmpd, "m.json"), g * S, (n - g) * S + n * 6 * S)
+    tensors, steps = load(tp)
+    e = Engine(tp, mp, {"policy": "tencache"}, gpu_spare_slots=16)
+    e.seed(3)
+    params = {i: e.read_tensor(i, S).view(np.uint16).copy() for i in range(1, n + 1)}
+    states = {n + i: e.read_tensor(n + i, 6 * S).view(np.float32).copy() for i in range(1, n + 1)}
+    grads = {i: e.read_grad(i, S).copy() for i in range(1, n + 1)}
+    e.reset_stats()
+    accesses = [i for s in steps if s["phase"] != "o" for i in s["ids"]]
+    opt_steps = [s["ids"] for s in steps if s["phase"] == "o"]
+    results = []
+    for it in range(1, iters + 1):
+        e.iteration(last=it == iters, **HP)
+        results.append(e.step_result())
+    for it in range(1, iters + 1):
+        want = np.array([ref.checksum(params[i]) for i in accesses], dtype=np.uint64)
+        assert np.array_equal(results[it - 1], want), f"step result of iteration {it}"
+        for sid, pid in opt_steps:
+            k = S // 2
+            st = states[sid]
+            params[pid] = ref.adamw(st[:k], st[k:2 * k], st[2 * k:], grads[pid], HP["lr"], HP["beta1"], HP["beta2"],
+                                    HP["eps"], HP["weight_decay"], it)
+    for i in range(1, n + 1):
+        assert np.array_equal(e.read_tensor(i, S).view(np.uint16), params[i]), f"param {i}"
+        assert np.array_equal(e.read_tensor(n + i, 6 * S).view(np.uint32), states[n + i].view(np.uint32)), f"state {n + i}"
+    st = e.stats()
+    assert st["opt_h2d_bytes"] == iters * n * 6 * S and st["opt_d2h_bytes"] == iters * n * 6 * S
+    e.close()
