@@ -242,6 +242,7 @@ def run_ours(args):
         tokens_d.copy_(tokens_h, non_blocking=True)
         eng.iteration(last=k == e2e_steps - 1, **step_kw)
         cks = eng.step_result()
+    eng.sync()  # the last step's write-back tail (incl. NVMe writes) is part of the step
     torch.cuda.synchronize()
     e2e_ms = (time.perf_counter() - t0) * 1e3 / e2e_steps
     eng.reset_stats()

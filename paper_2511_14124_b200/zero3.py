@@ -248,6 +248,7 @@ def bench_rank(args):
         tok_d.copy_(tok_h, non_blocking=True)
         eng.iteration(last=k == e2e_steps - 1, **kw)
         cks = eng.step_result()
+    eng.sync()  # the last step's write-back tail (incl. NVMe writes) is part of the step
     torch.cuda.synchronize()
     e2e_ms = reduce((time.perf_counter() - t0) * 1e3 / e2e_steps, dist.ReduceOp.MAX)
     line = None
