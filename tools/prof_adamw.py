@@ -59,6 +59,12 @@ cks = torch.zeros(1, dtype=torch.int64, device="cuda")
 timeit("checksum", lambda i: K.checksum(src, cks), S)
 big = torch.empty(6 * S, dtype=torch.uint8, device="cuda")
 timeit("checksum_6S", lambda i: K.checksum(big, cks), 6 * S, clean=False)
+# the same byte streams through torch's own kernels, for scale at these sizes
+timeit("torch_cast_bf16_to_f32", lambda i: f32.copy_(grad), 6 * n)
+timeit("torch_cast_f32_to_bf16", lambda i: pout.copy_(f32), 6 * n)
+half = torch.empty(plan.total_bytes, dtype=torch.uint8, device="cuda")
+timeit("torch_copy_pack_bytes", lambda i: half.copy_(src[: plan.total_bytes]), 2 * plan.total_bytes)
+timeit("torch_sum_checksum_bytes", lambda i: src.view(torch.int32).sum(), S)
 print(json.dumps(res))
 os.makedirs("gpurun_out", exist_ok=True)
 if os.environ.get("KALONE_OUT", "1") == "1":
