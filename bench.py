@@ -294,7 +294,7 @@ def run_ours(args):
                                if args.config == "c4" else
                                ("C5 rank 0 of 8: Llama-3 70B ZeRO-3 shard, parameters and optimizer states homed in "
                                 "pinned host memory, GPU cache sized from 180 GB HBM (BASELINE.json configs[4])"),
-                   "model": {"c2": "opt-1.3b", "c3": "llama2-7b", "c4": "gpt3-13b", "c5": "llama3-70b"}[args.config],
+                   "trace_of": {"c2": "opt-1.3b", "c3": "llama2-7b", "c4": "gpt3-13b", "c5": "llama3-70b"}[args.config],
                    "chunks": info["params"], "chunk_bytes": info["chunk_bytes"],
                    "gpu_param_chunks": info["gpu_chunks"], "policy": cfg["policy"],
                    "tokens_per_step": args.tokens, "compute": args.compute,
@@ -458,7 +458,7 @@ def run_reference_arm(args):
             "warmup": args.warmup, "ms_per_step": round(ms, 3), "higher_is_better": True, "scaling": "weak",
             "vs_baseline": None, "dtype": "fp32", "impl": "reference",
             "data": "synthetic", "config": {"workload": "C2: OPT-1.3B offloaded training step (CPU reference path)",
-                                           "model": "opt-1.3b", "chunks": n, "chunk_bytes": S, "policy": "tencache"},
+                                           "trace_of": "opt-1.3b", "chunks": n, "chunk_bytes": S, "policy": "tencache"},
             "hit_rate": {"exact": rep["hit_rate"]},
             "cpu_baseline": {"value": round(v, 4), "unit": "GB/s", "cores": threads, "kind": "reference",
                              "sample": f"{args.steps} full C2 iterations: reference IPolicy decisions "

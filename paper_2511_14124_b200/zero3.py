@@ -265,7 +265,7 @@ def bench_rank(args):
                                         + ", optimizer states in pinned host memory"
                                         + (f" [{world} ranks sharing {ndev} GPU(s): functional run, timings not "
                                            "meaningful]" if shared else "")),
-                           "model": model, "chunks_per_rank": n, "gpu_chunks_per_rank": g, "chunk_bytes": S,
+                           "trace_of": model, "chunks_per_rank": n, "gpu_chunks_per_rank": g, "chunk_bytes": S,
                            "parallelism": f"zero3 x{world}", "exchange": exchange,
                            "l2": "inputs larger than L2 (GBs streamed per step)"},
                 "value_definition": ("sum over ranks of cache-decision bytes per step / max-over-ranks step time"
