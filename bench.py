@@ -38,6 +38,8 @@ ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
 METRIC = "step time & migrated GB/s per GPU vs PCIe roofline; GPU cache hit rate"
+C2_WORKLOAD = ("C2: OPT-1.3B offloaded training step, GPU->pinned-CPU tier, size-class buffer reuse "
+               "(BASELINE.json configs[1])")
 ADAM_BYTES_PER_ELEM = 28  # read p32,m,v (12) + g bf16 (2); write p32,m,v (12) + p bf16 (2)
 
 
@@ -284,8 +286,7 @@ def run_ours(args):
         "value_definition": value_def,
         "ms_per_step": round(ms, 3), "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
         "dtype": "bf16/fp32", "data": "synthetic (seeded N(0,0.02) params, N(0,1e-3) grads; chunk trace)",
-        "config": {"workload": ("C2: OPT-1.3B offloaded training step, 1xB200, GPU->pinned-CPU tier, "
-                                "size-class buffer reuse (BASELINE.json configs[1])") if args.config == "c2" else
+        "config": {"workload": C2_WORKLOAD if args.config == "c2" else
                                ("C3 at N=1: Llama-2 7B ZeRO-3 (NCCL exchange, world 1), optimizer states in pinned "
                                 "host memory (BASELINE.json configs[2])") if args.config == "c3" else
                                ("C4 rank 0 of 8: GPT-3 13B ZeRO-3 shard with GPU/CPU/NVMe tiers, NVMe via pinned "
@@ -456,9 +457,14 @@ def run_reference_arm(args):
     v = dec_bytes / (ms * 1e-3) / 1e9
     return {"metric": METRIC, "value": round(v, 4), "unit": "GB/s", "n_gpus": 1, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": round(ms, 3), "higher_is_better": True, "scaling": "weak",
-            "vs_baseline": None, "dtype": "fp32", "impl": "reference",
-            "data": "synthetic", "config": {"workload": "C2: OPT-1.3B offloaded training step (CPU reference path)",
-                                           "trace_of": "opt-1.3b", "chunks": n, "chunk_bytes": S, "policy": "tencache"},
+            "vs_baseline": None, "dtype": "bf16/fp32", "impl": "reference",
+            "data": "synthetic",
+            "config": {"workload": C2_WORKLOAD, "trace_of": "opt-1.3b", "chunks": n, "chunk_bytes": S,
+                       "gpu_param_chunks": info["gpu_chunks"], "policy": "tencache", "tokens_per_step": args.tokens,
+                       "compute": "sleep for the trace compute time", "compute_model_tflops": args.tflops,
+                       "parallelism": "host cores (%d threads)" % threads,
+                       "path": "reference IPolicy decisions (oracle/_ref), host memcpy migrations, CPU checksums, "
+                               "OpenMP AdamW (oracle/numerics.c)"},
             "hit_rate": {"exact": rep["hit_rate"]},
             "cpu_baseline": {"value": round(v, 4), "unit": "GB/s", "cores": threads, "kind": "reference",
                              "sample": f"{args.steps} full C2 iterations: reference IPolicy decisions "
