@@ -277,7 +277,8 @@ Executor::Executor(const std::string& trace_path, const std::string& machine_pat
   TCB_CK(cudaStreamCreateWithFlags(&d2h_, cudaStreamNonBlocking));
   int lo_prio = 0, hi_prio = 0;  // the fused AdamW gets the highest stream priority
   TCB_CK(cudaDeviceGetStreamPriorityRange(&lo_prio, &hi_prio));
-  TCB_CK(cudaStreamCreateWithPriority(&opt_, cudaStreamNonBlocking, hi_prio));
+  const char* op = std::getenv("TC_OPT_PRIORITY");  // diagnostic: 0 = default priority for the AdamW stream
+  TCB_CK(cudaStreamCreateWithPriority(&opt_, cudaStreamNonBlocking, (op && std::atoi(op) == 0) ? lo_prio : hi_prio));
   TCB_CK(cudaStreamCreateWithFlags(&h2d_opt_, cudaStreamNonBlocking));
   TCB_CK(cudaStreamCreateWithFlags(&d2h_opt_, cudaStreamNonBlocking));
 
