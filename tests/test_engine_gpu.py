@@ -387,3 +387,44 @@ def test_back_to_back_iterations_with_prologue(tmpd):
     st = e.stats()
     assert st["opt_h2d_bytes"] == iters * n * 6 * S and st["opt_d2h_bytes"] == iters * n * 6 * S
     e.close()
+
+
+def test_full_size_c2_bit_exact(tmpd):
+    """BASELINE configs[1] at full size (OPT-1.3B: 79 chunks of 33.6 MB, 31 in
+    the GPU tier, 15.9 GB of optimizer states in pinned host memory), two
+    back-to-back iterations exactly as bench.py runs them (compute stand-in,
+    prologue, non-draining results): every per-access checksum of both
+    iterations, every final parameter and every optimizer state bit-exact
+    against the oracle, hit count == model clock, each state over PCIe once
+    per direction per iteration."""
+    info = T.config_c2(tmpd, iterations=2, tokens=16384)
+    S, n = info["chunk_bytes"], info["params"]
+    e = Engine(info["trace"], info["machine"], {"policy": "tencache"}, gpu_spare_slots=16)
+    e.seed(0)
+    params = {i: e.read_tensor(i, S).view(np.uint16).copy() for i in range(1, n + 1)}
+    states = {n + i: e.read_tensor(n + i, 6 * S).view(np.float32).copy() for i in range(1, n + 1)}
+    grads = {i: e.read_grad(i, S).copy() for i in range(1, n + 1)}
+    e.reset_stats()
+    tensors, steps = load(info["trace"])
+    accesses = [i for s in steps if s["phase"] != "o" for i in s["ids"]]
+    opt_steps = [s["ids"] for s in steps if s["phase"] == "o"]
+    results = []
+    for it in (1, 2):
+        e.iteration(lr=1e-4, compute_mode=1, spin_ctas=1, last=it == 2)
+        results.append(e.step_result())
+    k = S // 2
+    for it in (1, 2):
+        cks = {}
+        want = np.array([cks.setdefault(i, ref.checksum(params[i])) for i in accesses], dtype=np.uint64)
+        assert np.array_equal(results[it - 1], want), f"iteration {it}: access checksums"
+        for sid, pid in opt_steps:
+            st = states[sid]
+            params[pid] = ref.adamw(st[:k], st[k:2 * k], st[2 * k:], grads[pid], 1e-4, 0.9, 0.999, 1e-8, 0.01, it)
+    for i in range(1, n + 1):
+        assert np.array_equal(e.read_tensor(i, S).view(np.uint16), params[i]), f"param {i}"
+        assert np.array_equal(e.read_tensor(n + i, 6 * S).view(np.uint32), states[n + i].view(np.uint32)), \
+            f"state {n + i}"
+    st = e.stats()
+    assert st["param_hits"] == P.run(info["trace"], info["machine"], {"policy": "tencache"})["param_hits"]
+    assert st["opt_h2d_bytes"] == 2 * n * 6 * S and st["opt_d2h_bytes"] == 2 * n * 6 * S
+    e.close()
