@@ -29,9 +29,7 @@ cudaError_t launch_cast_f32_to_bf16(const float* in, std::uint16_t* out, std::ui
 // inverse = false: dst[dst_off..] <- src[src_off..]; true: dst[src_off..] <- src[dst_off..]
 cudaError_t launch_pack(const PackSeg* segs, std::uint32_t n, std::uint64_t total, const void* src, void* dst,
                         bool inverse, bool aligned16, cudaStream_t st);
-// max_ctas > 0 caps the grid (the forward/backward stand-in leaves SMs to concurrent kernels).
-cudaError_t launch_checksum(const void* data, std::uint64_t bytes, unsigned long long* out, cudaStream_t st,
-                            int max_ctas = 0);
+cudaError_t launch_checksum(const void* data, std::uint64_t bytes, unsigned long long* out, cudaStream_t st);
 cudaError_t launch_spin(std::uint64_t ns, int ctas, cudaStream_t st);
 // Small fills/copies of 64-bit words as kernels: never queued on a copy engine
 // behind bulk DMA (dst may be mapped pinned host memory: posted PCIe writes).

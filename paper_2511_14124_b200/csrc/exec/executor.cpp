@@ -208,7 +208,6 @@ Executor::Executor(const std::string& trace_path, const std::string& machine_pat
     fcntl(nvme_fd_, F_SETFL, fl | O_DIRECT);
   }
   if (ftruncate(nvme_fd_, static_cast<off_t>(off)) != 0) throw DeviceError(TC_EIO, "ftruncate NVMe tier file");
-  if (const char* c = std::getenv("TC_CHECKSUM_CTAS")) checksum_ctas_ = std::atoi(c);
   if (const char* c = std::getenv("TC_OPT_YIELD")) opt_yield_ = std::atoi(c) != 0;
   if (const char* c = std::getenv("TC_PRESTAGE_FWD")) prestage_fwd_override_ = std::atoi(c);
   if (const char* c = std::getenv("TC_PRESTAGE_GATE")) prestage_gate_ = std::atoi(c) != 0;
@@ -757,7 +756,7 @@ void Executor::param_step(const TraceStep& step, std::size_t, cudaStream_t cs) {
       zero3_access(x, step.phase == Phase::Backward, cs);
     } else if (access_cursor_ < n_accesses_) {
       TCB_CK(launch_checksum(where(x), x.bytes & ~3ull,
-                             reinterpret_cast<unsigned long long*>(cks_base_ + access_cursor_), cs, checksum_ctas_));
+                             reinterpret_cast<unsigned long long*>(cks_base_ + access_cursor_), cs));
       ++stats_.kernel_launches;
       ++access_cursor_;
     }

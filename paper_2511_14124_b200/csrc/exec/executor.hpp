@@ -324,9 +324,8 @@ class Executor {
   unsigned long long* d_span_ = nullptr;  // 2 parities x n_params x (min, max) AdamW kernel spans
   unsigned long long* span_base_ = nullptr;
   std::size_t span_cursor_ = 0;
-  int checksum_ctas_ = 0;
   bool opt_yield_ = false;                 // optimizer copies queue behind earlier decision copies (env TC_OPT_YIELD)
-  cudaEvent_t last_h2d_ = nullptr, last_d2h_ = nullptr;  // most recent decision copy per direction  // grid cap of the stand-in's checksum (env TC_CHECKSUM_CTAS; 0 = full)
+  cudaEvent_t last_h2d_ = nullptr, last_d2h_ = nullptr;  // most recent decision copy per direction
   std::size_t n_accesses_ = 0, access_cursor_ = 0;
   int nvme_fd_ = -1;
   std::unique_ptr<NvmeQueue> io_;  // async NVMe tier I/O (null: synchronous fallback)

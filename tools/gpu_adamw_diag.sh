@@ -3,7 +3,6 @@ timeout 300 python tools/adamw_contention.py > gpurun_out/contention.log 2>&1
 for v in 2 0 4; do
   TC_ADAMW_VARIANT=$v timeout 300 python bench.py --steps 4 --warmup 3 --no-cpu-baseline > gpurun_out/bench_v$v.json 2>>gpurun_out/b.err
 done
-TC_CHECKSUM_CTAS=16 timeout 300 python bench.py --steps 4 --warmup 3 --no-cpu-baseline > gpurun_out/bench_cks16.json 2>>gpurun_out/b.err
 timeout 300 python bench.py --steps 4 --warmup 3 --no-cpu-baseline --compute none > gpurun_out/bench_nocompute.json 2>>gpurun_out/b.err
 cat gpurun_out/contention.log
 for f in gpurun_out/bench_v*.json gpurun_out/bench_cks16.json gpurun_out/bench_nocompute.json; do python -c "
