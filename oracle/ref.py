@@ -34,6 +34,8 @@ def lib():
         L.tcref_run.argtypes = [C.c_char_p, C.c_char_p, C.c_char_p, C.c_char_p, C.c_char_p, C.c_int]
         L.tcref_time_run.argtypes = [C.c_char_p, C.c_char_p, C.c_char_p, C.c_int, C.POINTER(C.c_double)]
         L.tcref_decisions.argtypes = [C.c_char_p, C.c_char_p, C.c_char_p, C.c_char_p, C.c_int]
+        L.tcref_sweep.argtypes = [C.c_char_p, C.c_char_p, C.c_char_p, C.c_char_p, C.POINTER(C.c_double), C.c_uint,
+                                  C.c_uint, C.c_char_p, C.POINTER(C.c_double)]
         L.tcref_time_decisions.argtypes = [C.c_char_p, C.c_char_p, C.c_char_p, C.c_int,
                                            C.POINTER(C.c_double), C.POINTER(C.c_double)]
         L.tcref_synthesize.argtypes = [C.c_uint, C.c_uint, C.POINTER(C.c_ulonglong), C.c_int, C.c_double,
@@ -87,6 +89,17 @@ def time_run(trace_path, machine_path="", cfg=None, repeats=1):
     out = C.c_double()
     _chk(lib().tcref_time_run(_b(trace_path), _b(machine_path), _b(json.dumps(cfg or {})), repeats, C.byref(out)))
     return out.value
+
+
+def sweep(trace_path, machine_path="", cfg=None, axis="gpu_capacity", values=(), threads=1):
+    """The reference's sweep() (engine.cpp:334-384): (reports, wall ns)."""
+    vals = (C.c_double * max(len(values), 1))(*values)
+    ns = C.c_double()
+    with tempfile.TemporaryDirectory() as d:
+        op = os.path.join(d, "s.json")
+        _chk(lib().tcref_sweep(_b(trace_path), _b(machine_path), _b(json.dumps(cfg or {})), _b(axis), vals,
+                               len(values), threads, _b(op), C.byref(ns)))
+        return json.load(open(op)), ns.value
 
 
 def time_decisions(trace_path, machine_path="", cfg=None, iterations=1):

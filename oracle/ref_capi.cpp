@@ -233,6 +233,29 @@ int tcref_time_run(const char* trace_path, const char* machine_path, const char*
   })
 }
 
+// The reference's sweep() (engine.cpp:334-384) over one axis on `threads`
+// threads: reports as a JSON array (same schema as tcref_run) and the
+// wall-clock cost in ns.
+int tcref_sweep(const char* trace_path, const char* machine_path, const char* cfg_json, const char* axis,
+                const double* values, unsigned n, unsigned threads, const char* out_path, double* out_ns) {
+  GUARD({
+    ExecutionTrace trace = load_trace(trace_path);
+    MachineConfig m = get_machine(machine_path);
+    RunConfig c = parse_cfg(cfg_json);
+    const std::vector<double> v(values, values + n);
+    auto t0 = std::chrono::steady_clock::now();
+    std::vector<SimReport> reps = sweep(trace, m, c, sweep_axis_from_string(axis), v, threads);
+    auto t1 = std::chrono::steady_clock::now();
+    if (out_ns) *out_ns = std::chrono::duration<double, std::nano>(t1 - t0).count();
+    if (out_path && *out_path) {
+      nlohmann::json arr = nlohmann::json::array();
+      for (const SimReport& r : reps) arr.push_back(report_json(r));
+      std::ofstream(out_path) << arr.dump() << "\n";
+    }
+    return 0;
+  })
+}
+
 int tcref_decisions(const char* trace_path, const char* machine_path, const char* cfg_json,
                     const char* out_path, int with_pools) {
   GUARD({

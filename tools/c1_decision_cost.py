@@ -42,7 +42,9 @@ vals = [40e6 + 5e6 * k for k in range(16)]
 t0 = time.perf_counter()
 P.sweep(tr, m, {}, axis="gpu_capacity", values=vals, threads=os.cpu_count())
 t_ours = time.perf_counter() - t0
-out["sweep_c1b_16_values_all_cores_s"] = {"ours": round(t_ours, 3)}
+_, ref_ns = ref.sweep(tr, m, {}, "gpu_capacity", vals, threads=os.cpu_count())
+out["sweep_c1b_16_values_all_cores_s"] = {"ours": round(t_ours, 3), "reference": round(ref_ns * 1e-9, 3),
+                                          "speedup": round(ref_ns * 1e-9 / t_ours, 1)}
 print(json.dumps(out, indent=1))
 os.makedirs("gpurun_out", exist_ok=True)
 json.dump(out, open("gpurun_out/c1_decision_cost.json", "w"), indent=1)
