@@ -74,10 +74,19 @@ __global__ void __launch_bounds__(kThr) gather_unpack_kernel(GatherArgs a) {
   std::uint8_t* dst = a.view + a.view_off[q] + tile * kTile;
   const std::uint64_t len = min(kTile, a.bytes[q] - tile * kTile);
   const bool vec = ((reinterpret_cast<std::uintptr_t>(src) | reinterpret_cast<std::uintptr_t>(dst) | len) & 15) == 0;
-  if (vec) {
+  if (vec) {  // four 16-byte peer loads in flight per thread (NVLink latency)
     const uint4* s4 = reinterpret_cast<const uint4*>(src);
     uint4* d4 = reinterpret_cast<uint4*>(dst);
-    for (std::uint64_t i = threadIdx.x; i < len / 16; i += kThr) d4[i] = s4[i];
+    const std::uint64_t nv = len / 16;
+    std::uint64_t i = threadIdx.x;
+    for (; i + 3 * kThr < nv; i += 4 * kThr) {
+      const uint4 r0 = s4[i], r1 = s4[i + kThr], r2 = s4[i + 2 * kThr], r3 = s4[i + 3 * kThr];
+      d4[i] = r0;
+      d4[i + kThr] = r1;
+      d4[i + 2 * kThr] = r2;
+      d4[i + 3 * kThr] = r3;
+    }
+    for (; i < nv; i += kThr) d4[i] = s4[i];
   } else {
     for (std::uint64_t i = threadIdx.x; i < len; i += kThr) dst[i] = src[i];
   }
@@ -98,7 +107,14 @@ struct PullArgs {
   std::uint64_t view_off, bytes, chunk_bytes;
   std::uint16_t* grad;
   unsigned* done;
+  int vec;  // every view + view_off and grad 16-byte aligned: 16-byte loads/stores
 };
+
+__device__ __forceinline__ std::uint32_t rne_bf16(float f) {
+  std::uint32_t u = __float_as_uint(f);
+  if ((u & 0x7fffffffu) > 0x7f800000u) return ((u >> 16) | 0x40u) & 0xffffu;
+  return (u + 0x7fffu + ((u >> 16) & 1u)) >> 16;
+}
 
 // Each thread reduces 8 bf16 values across all ranks' views (fp32, rank
 // order, one rounding); padding of the chunk is written as zero.
@@ -113,6 +129,36 @@ __global__ void __launch_bounds__(kThr) pull_reduce_kernel(PullArgs a) {
   const std::uint64_t n = a.chunk_bytes / 2, valid = a.bytes / 2;
   for (std::uint64_t i = (static_cast<std::uint64_t>(blockIdx.x) * kThr + threadIdx.x) * 8; i < n;
        i += static_cast<std::uint64_t>(gridDim.x) * kThr * 8) {
+    if (a.vec && i + 8 <= valid) {  // 16 bytes per rank per thread, same fp32 order as below
+      uint4 w[kMaxPeers];
+#pragma unroll
+      for (int q = 0; q < kMaxPeers; ++q)
+        if (q < a.t.world) w[q] = *reinterpret_cast<const uint4*>(a.t.gview[q] + a.view_off + i * 2);
+      float acc[8];
+      const std::uint32_t* w0 = reinterpret_cast<const std::uint32_t*>(&w[0]);
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        acc[2 * k] = __uint_as_float(w0[k] << 16);
+        acc[2 * k + 1] = __uint_as_float(w0[k] & 0xffff0000u);
+      }
+#pragma unroll
+      for (int q = 1; q < kMaxPeers; ++q) {
+        if (q >= a.t.world) break;
+        const std::uint32_t* wq = reinterpret_cast<const std::uint32_t*>(&w[q]);
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+          acc[2 * k] += __uint_as_float(wq[k] << 16);
+          acc[2 * k + 1] += __uint_as_float(wq[k] & 0xffff0000u);
+        }
+      }
+      uint4 o;
+      o.x = rne_bf16(acc[0]) | (rne_bf16(acc[1]) << 16);
+      o.y = rne_bf16(acc[2]) | (rne_bf16(acc[3]) << 16);
+      o.z = rne_bf16(acc[4]) | (rne_bf16(acc[5]) << 16);
+      o.w = rne_bf16(acc[6]) | (rne_bf16(acc[7]) << 16);
+      *reinterpret_cast<uint4*>(a.grad + i) = o;
+      continue;
+    }
     float acc[8];
     {  // the sum starts from rank 0's value (not +0): a single rank reduces to an exact copy, -0 included
       const std::uint16_t* v = reinterpret_cast<const std::uint16_t*>(a.t.gview[0] + a.view_off);
@@ -128,12 +174,7 @@ __global__ void __launch_bounds__(kThr) pull_reduce_kernel(PullArgs a) {
 #pragma unroll
     for (int k = 0; k < 8; ++k) {
       if (i + k >= n) break;
-      std::uint32_t u = __float_as_uint(acc[k]);
-      if ((u & 0x7fffffffu) > 0x7f800000u)
-        u = (u >> 16) | 0x40u;
-      else
-        u = (u + 0x7fffu + ((u >> 16) & 1u)) >> 16;
-      a.grad[i + k] = static_cast<std::uint16_t>(i + k < valid ? u : 0u);
+      a.grad[i + k] = static_cast<std::uint16_t>(i + k < valid ? rne_bf16(acc[k]) : 0u);
     }
   }
   __syncthreads();
@@ -202,6 +243,9 @@ cudaError_t launch_p2p_pull_reduce(const PeerTable& t, std::uint32_t gepoch, std
   a.chunk_bytes = chunk_bytes;
   a.grad = grad;
   a.done = scratch_counters() + kMaxPeers;
+  std::uintptr_t al = reinterpret_cast<std::uintptr_t>(grad) | view_off;
+  for (int q = 0; q < t.world; ++q) al |= reinterpret_cast<std::uintptr_t>(t.gview[q]);
+  a.vec = (al & 15) == 0 ? 1 : 0;
   const std::uint64_t units = (chunk_bytes / 2 + 8 * kThr - 1) / (8 * kThr);
   const unsigned grid = static_cast<unsigned>(std::max<std::uint64_t>(1, std::min<std::uint64_t>(units, 4 * 148)));
   pull_reduce_kernel<<<grid, kThr, 0, st>>>(a);
