@@ -259,8 +259,10 @@ def run_ours(args):
     traffic = None
     tf = os.path.join(ROOT, "profiles", "adamw_dram_bytes.json")
     if os.path.exists(tf):
-        try:
-            traffic = json.load(open(tf)).get("dram_bytes_per_launch")
+        try:  # ncu --set full capture of one C2 launch, scaled to this config's launch size
+            tj = json.load(open(tf))
+            traffic = int(tj["dram_bytes_per_launch"] * ADAM_BYTES_PER_ELEM * elems_per_launch
+                          / tj["algorithmic_bytes_per_launch"])
         except Exception:
             traffic = None
     pcie_peak = {"h2d": args.pcie_h2d, "d2h": args.pcie_d2h}
