@@ -163,6 +163,33 @@ def run_prespin(name, background=None):
     res[name] = {"median_us": round(med, 2), "GBps_median": round(28 * n / (med * 1e-6) / 1e9, 1)}
 
 
+def run_cross_stream(name, background=None, same_stream=False):
+    """The in-step dependency shape: a kernel on another stream (the compute
+    stream's backward step) records an event; the AdamW stream waits for it,
+    records its start event and launches."""
+    times = []
+    for r in range(reps):
+        if background:
+            background()
+        dep = torch.cuda.Event()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        src = hi if same_stream else side
+        K.spin(300.0, 1, stream=src)
+        dep.record(src)
+        hi.wait_event(dep)
+        e0.record(hi)
+        K.adamw(states[r % nst], grad, pout, 1e-4, 0.9, 0.999, 1e-8, 0.01, r + 1, stream=hi)
+        e1.record(hi)
+        torch.cuda.synchronize()
+        times.append(e0.elapsed_time(e1) * 1e3)
+    times.sort()
+    med = times[len(times) // 2]
+    res[name] = {"median_us": round(med, 2), "GBps_median": round(28 * n / (med * 1e-6) / 1e9, 1)}
+
+
+run_cross_stream("cross_stream_dep")
+run_cross_stream("cross_stream_dep_with_pcie_copies", copies)
+run_cross_stream("same_stream_dep_with_pcie_copies", copies, same_stream=True)
 run_prespin("prespin_alone")
 run_prespin("prespin_with_pcie_copies", copies)
 run_graph("graph_alone")
