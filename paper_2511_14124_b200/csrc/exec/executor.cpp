@@ -196,18 +196,10 @@ Executor::Executor(const std::string& trace_path, const std::string& machine_pat
   }
   std::string dir = opts.nvme_dir && *opts.nvme_dir ? opts.nvme_dir : "";
   if (dir.empty()) dir = std::getenv("TMPDIR") ? std::getenv("TMPDIR") : "/tmp";
-  nvme_path_ = dir + "/tencache_nvme_XXXXXX";
-  std::vector<char> tmpl(nvme_path_.begin(), nvme_path_.end());
-  tmpl.push_back(0);
-  nvme_fd_ = mkstemp(tmpl.data());
-  if (nvme_fd_ < 0) throw DeviceError(TC_EIO, "cannot create NVMe tier file in " + dir);
-  nvme_path_ = tmpl.data();
-  unlink(nvme_path_.c_str());
-  if (opts.direct_io && all_aligned) {
-    int fl = fcntl(nvme_fd_, F_GETFL);
-    fcntl(nvme_fd_, F_SETFL, fl | O_DIRECT);
+  {
+    const char* nf = std::getenv("TC_NVME_FILES");
+    nvme_ = std::make_unique<StripedFile>(dir, off, nf ? std::atoi(nf) : 16, opts.direct_io && all_aligned);
   }
-  if (ftruncate(nvme_fd_, static_cast<off_t>(off)) != 0) throw DeviceError(TC_EIO, "ftruncate NVMe tier file");
   if (const char* c = std::getenv("TC_OPT_YIELD")) opt_yield_ = std::atoi(c) != 0;
   if (const char* c = std::getenv("TC_PRESTAGE_FWD")) prestage_fwd_override_ = std::atoi(c);
   if (const char* c = std::getenv("TC_PRESTAGE_GATE")) prestage_gate_ = std::atoi(c) != 0;
@@ -216,7 +208,7 @@ Executor::Executor(const std::string& trace_path, const std::string& machine_pat
   if (const char* c = std::getenv("TC_ADAM_STAMPS")) adam_stamps_ = std::atoi(c) != 0;
   if (!std::getenv("TC_SYNC_NVME")) {
     try {
-      io_ = std::make_unique<NvmeQueue>(device_, nvme_fd_);
+      io_ = std::make_unique<NvmeQueue>(device_, nvme_.get());
       TCB_CK(cudaStreamCreateWithFlags(&io_join_, cudaStreamNonBlocking));
     } catch (const std::exception&) {
       io_.reset();  // no stream memory operations: synchronous NVMe I/O
@@ -332,7 +324,6 @@ Executor::~Executor() {
   if (d2h_opt_) cudaStreamDestroy(d2h_opt_);
   if (io_join_) cudaStreamDestroy(io_join_);
   if (compute_owned_) cudaStreamDestroy(compute_owned_);
-  if (nvme_fd_ >= 0) close(nvme_fd_);
   if (z3_) {
     for (auto& [k, cp] : z3_->plans)
       if (cp.segs) cudaFree(cp.segs);
@@ -515,24 +506,14 @@ cudaEvent_t Executor::copy(cudaStream_t s, void* dst, const void* src, std::uint
 }
 
 void Executor::nvme_read(const TensorRec& r, void* dst) {
-  std::uint64_t done = 0;
-  auto* p = static_cast<std::uint8_t*>(dst);
-  while (done < r.bytes) {
-    const ssize_t k = pread(nvme_fd_, p + done, r.bytes - done, static_cast<off_t>(r.nvme_off + done));
-    if (k <= 0) throw DeviceError(TC_EIO, "NVMe tier read failed for tensor " + std::to_string(r.id));
-    done += static_cast<std::uint64_t>(k);
-  }
+  if (!nvme_->io(false, static_cast<std::uint8_t*>(dst), r.bytes, r.nvme_off))
+    throw DeviceError(TC_EIO, "NVMe tier read failed for tensor " + std::to_string(r.id));
   stats_.nvme_read_bytes += r.bytes;
 }
 
 void Executor::nvme_write(TensorRec& r, const void* src) {
-  std::uint64_t done = 0;
-  const auto* p = static_cast<const std::uint8_t*>(src);
-  while (done < r.bytes) {
-    const ssize_t k = pwrite(nvme_fd_, p + done, r.bytes - done, static_cast<off_t>(r.nvme_off + done));
-    if (k <= 0) throw DeviceError(TC_EIO, "NVMe tier write failed for tensor " + std::to_string(r.id));
-    done += static_cast<std::uint64_t>(k);
-  }
+  if (!nvme_->io(true, const_cast<std::uint8_t*>(static_cast<const std::uint8_t*>(src)), r.bytes, r.nvme_off))
+    throw DeviceError(TC_EIO, "NVMe tier write failed for tensor " + std::to_string(r.id));
   r.nvme_valid = true;
   stats_.nvme_write_bytes += r.bytes;
 }
@@ -1604,21 +1585,13 @@ void Executor::read_tensor(TensorId id, void* dst, std::uint64_t bytes) {
   if (r.tier == PTier::Gpu) {
     TCB_CK(cudaMemcpy(dst, where(r), bytes, cudaMemcpyDeviceToHost));
   } else if (r.tier == PTier::Nvme) {
-    std::uint64_t done = 0;
-    auto* p = static_cast<std::uint8_t*>(dst);
     if (!r.nvme_valid) throw DeviceError(TC_EINTERNAL, "NVMe replica of tensor is stale");
-    std::uint8_t* tmp = nullptr;
+    std::uint8_t* tmp = nullptr;  // pinned and page-aligned (O_DIRECT tiers)
     TCB_CK(cudaMallocHost(reinterpret_cast<void**>(&tmp), bytes));
-    while (done < bytes) {
-      const ssize_t k = pread(nvme_fd_, tmp + done, bytes - done, static_cast<off_t>(r.nvme_off + done));
-      if (k <= 0) {
-        cudaFreeHost(tmp);
-        throw DeviceError(TC_EIO, "read_tensor: NVMe read failed");
-      }
-      done += static_cast<std::uint64_t>(k);
-    }
-    std::memcpy(p, tmp, bytes);
+    const bool ok = nvme_->io(false, tmp, bytes, r.nvme_off);
+    if (ok) std::memcpy(dst, tmp, bytes);
     cudaFreeHost(tmp);
+    if (!ok) throw DeviceError(TC_EIO, "read_tensor: NVMe read failed");
   } else {
     std::memcpy(dst, where(r), bytes);
   }

@@ -327,13 +327,12 @@ class Executor {
   bool opt_yield_ = false;                 // optimizer copies queue behind earlier decision copies (env TC_OPT_YIELD)
   cudaEvent_t last_h2d_ = nullptr, last_d2h_ = nullptr;  // most recent decision copy per direction
   std::size_t n_accesses_ = 0, access_cursor_ = 0;
-  int nvme_fd_ = -1;
+  std::unique_ptr<StripedFile> nvme_;  // NVMe tier backing files
   std::unique_ptr<NvmeQueue> io_;  // async NVMe tier I/O (null: synchronous fallback)
   cudaStream_t io_join_ = nullptr;  // joins a job's dependencies into one event of the submitting generation
   std::vector<cudaEvent_t> io_deps(std::vector<cudaEvent_t> deps);
   std::uint64_t nvme_read_async(TensorRec& r, void* dst, SlotSync& target);
   std::uint64_t nvme_write_async(TensorRec& r, const void* src, SlotSync& source);
-  std::string nvme_path_;
 
   // h2d_/d2h_: cache decisions (prefetch, evict, restore); h2d_opt_/d2h_opt_:
   // optimizer-state staging and write-back, so evictions never queue behind

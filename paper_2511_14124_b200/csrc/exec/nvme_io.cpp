@@ -1,6 +1,7 @@
 #include "nvme_io.hpp"
 
 #include <cuda.h>
+#include <fcntl.h>
 #include <unistd.h>
 
 #include <algorithm>
@@ -31,7 +32,48 @@ void stream_wait_value32(cudaStream_t s, const unsigned* dev_addr, unsigned valu
     throw DeviceError(TC_ECUDA, "cuStreamWaitValue32 failed");
 }
 
-NvmeQueue::NvmeQueue(int device, int fd) : device_(device), fd_(fd) {
+StripedFile::StripedFile(const std::string& dir, std::uint64_t bytes, int files, bool direct) {
+  files = std::max(1, files);
+  const std::uint64_t stripes = (bytes + kStripe - 1) / kStripe;
+  const std::uint64_t per_file = ((stripes + files - 1) / files) * kStripe;
+  for (int k = 0; k < files; ++k) {
+    std::string path = dir + "/tencache_nvme_XXXXXX";
+    std::vector<char> tmpl(path.begin(), path.end());
+    tmpl.push_back(0);
+    const int fd = mkstemp(tmpl.data());
+    if (fd < 0) throw DeviceError(TC_EIO, "cannot create NVMe tier file in " + dir);
+    unlink(tmpl.data());
+    fds_.push_back(fd);
+    if (direct) fcntl(fd, F_SETFL, fcntl(fd, F_GETFL) | O_DIRECT);
+    if (ftruncate(fd, static_cast<off_t>(per_file)) != 0) throw DeviceError(TC_EIO, "ftruncate NVMe tier file");
+  }
+}
+
+StripedFile::~StripedFile() {
+  for (int fd : fds_) close(fd);
+}
+
+bool StripedFile::io(bool write, std::uint8_t* buf, std::uint64_t bytes, std::uint64_t off) const {
+  const std::uint64_t k = fds_.size();
+  while (bytes) {
+    const std::uint64_t stripe = off / kStripe, in = off % kStripe;
+    const std::uint64_t len = std::min(bytes, kStripe - in);
+    const int fd = fds_[stripe % k];
+    const std::uint64_t foff = (stripe / k) * kStripe + in;
+    for (std::uint64_t done = 0; done < len;) {
+      const ssize_t r = write ? pwrite(fd, buf + done, len - done, static_cast<off_t>(foff + done))
+                              : pread(fd, buf + done, len - done, static_cast<off_t>(foff + done));
+      if (r <= 0) return false;
+      done += static_cast<std::uint64_t>(r);
+    }
+    buf += len;
+    off += len;
+    bytes -= len;
+  }
+  return true;
+}
+
+NvmeQueue::NvmeQueue(int device, const StripedFile* file) : device_(device), file_(file) {
   void* fn = nullptr;
   cudaDriverEntryPointQueryResult q;
   if (cudaGetDriverEntryPoint("cuStreamWaitValue32", &fn, cudaEnableDefault, &q) != cudaSuccess ||
@@ -186,14 +228,7 @@ void NvmeQueue::work() {
       p = pieces_.front();
       pieces_.pop_front();
     }
-    bool ok = true;
-    for (std::uint64_t done = 0; ok && done < p.bytes;) {
-      const ssize_t k = p.write ? pwrite(fd_, p.buf + done, p.bytes - done, static_cast<off_t>(p.off + done))
-                                : pread(fd_, p.buf + done, p.bytes - done, static_cast<off_t>(p.off + done));
-      if (k <= 0) ok = false;
-      else done += static_cast<std::uint64_t>(k);
-    }
-    piece_done(p.seq, ok);
+    piece_done(p.seq, file_->io(p.write, p.buf, p.bytes, p.off));
   }
 }
 

@@ -26,10 +26,29 @@ namespace tcb {
 // >= value (cuStreamWaitValue32 through the runtime's driver entry point).
 void stream_wait_value32(cudaStream_t s, const unsigned* dev_addr, unsigned value);
 
+// The NVMe tier's backing store: one logical byte range striped over K files
+// in 16 MiB stripes (file = stripe % K). Buffered writes to one file
+// serialise on the inode lock in the kernel; K files let the I/O pool's
+// workers write in parallel.
+class StripedFile {
+ public:
+  static constexpr std::uint64_t kStripe = 16ull << 20;
+  StripedFile(const std::string& dir, std::uint64_t bytes, int files, bool direct);
+  ~StripedFile();
+  StripedFile(const StripedFile&) = delete;
+  StripedFile& operator=(const StripedFile&) = delete;
+  // Full transfer at logical offset `off`; false on an I/O error.
+  bool io(bool write, std::uint8_t* buf, std::uint64_t bytes, std::uint64_t off) const;
+  int files() const { return static_cast<int>(fds_.size()); }
+
+ private:
+  std::vector<int> fds_;
+};
+
 class NvmeQueue {
  public:
   // Throws DeviceError when stream memory operations are unavailable.
-  NvmeQueue(int device, int fd);
+  NvmeQueue(int device, const StripedFile* file);
   ~NvmeQueue();
 
   // `after`: an earlier job on the same host buffer that must be complete
@@ -65,7 +84,8 @@ class NvmeQueue {
   void work();
   void piece_done(std::uint64_t seq, bool ok);
 
-  int device_, fd_;
+  int device_;
+  const StripedFile* file_;
   std::deque<Piece> pieces_;
   std::map<std::uint64_t, std::uint32_t> remaining_;  // seq -> pieces left
   std::condition_variable piece_cv_;
