@@ -1641,7 +1641,7 @@ int tc_engine_create(const char* trace_path, const char* machine_path, const cha
   TC_GUARD({
     if (out == nullptr || trace_path == nullptr) return set_error(TC_EARG, "tc_engine_create: null argument");
     tc_engine_options o{};
-    o.gpu_spare_slots = 4;
+    o.gpu_spare_slots = 16;
     o.host_spare_slots = 1;
     o.opt_stage_slots = 12;
     o.grad_bytes_per_param_byte = 1;
