@@ -173,7 +173,7 @@ typedef struct tc_engine tc_engine;
 typedef struct {
   int device;              /* CUDA device ordinal */
   const char* nvme_dir;    /* directory for the NVMe tier file ("" = none) */
-  int gpu_spare_slots;     /* extra HBM slots per class for restore cycles */
+  int gpu_spare_slots;     /* extra HBM slots per class beyond the policy tier (in-flight moves; default 16) */
   int host_spare_slots;    /* extra pinned slots per class */
   int opt_stage_slots;     /* HBM staging buffers for the optimizer pipeline */
   int direct_io;           /* O_DIRECT for the NVMe tier */
