@@ -119,12 +119,9 @@ __device__ __forceinline__ std::uint32_t rne_bf16(float f) {
 // Each thread reduces 8 bf16 values across all ranks' views (fp32, rank
 // order, one rounding); padding of the chunk is written as zero.
 __global__ void __launch_bounds__(kThr) pull_reduce_kernel(PullArgs a) {
-  __shared__ int s_ok;
-  if (threadIdx.x == 0) {
+  if (threadIdx.x == 0)  // every rank's gradient view of this epoch is published
     for (int q = 0; q < a.t.world; ++q)
       while (ld_acquire_sys(&a.t.ctl[q]->gpub) < a.gepoch) __nanosleep(200);
-    s_ok = 1;
-  }
   __syncthreads();
   const std::uint64_t n = a.chunk_bytes / 2, valid = a.bytes / 2;
   for (std::uint64_t i = (static_cast<std::uint64_t>(blockIdx.x) * kThr + threadIdx.x) * 8; i < n;
