@@ -40,8 +40,10 @@ mp = T.write_machine(os.path.join(d, "m.json"), int(0.4 * n) * S, (n - int(0.4 *
 for pol in ("tencache", "tencache+opt"):
     e = Engine(tp, mp, {"policy": pol}, nvme_dir=d)
     e.seed(0)
-    e.iteration(lr=1e-3)
-    e.iteration(lr=1e-3)
+    e.iteration(lr=1e-3)          # enqueues iteration 2's prologue
+    e.step_result()               # mapped-memory result, no drain
+    e.iteration(lr=1e-3, last=True)
+    e.step_result()
     e.sync()
     e.close()
 from paper_2511_14124_b200 import zero3 as Z  # noqa: E402
@@ -50,10 +52,12 @@ tz = os.path.join(d, "z.jsonl")
 Z.write_rank_trace(tz, lay, 0, iterations=1, tokens=32)
 nz, Sz = lay.chunks_per_rank, lay.chunk_bytes
 mz = T.write_machine(os.path.join(d, "mz.json"), nz * Sz, nz * 7 * Sz)
-e = Engine(tz, mz, {"policy": "tencache"})
-e.seed(0)
-Z.enable(e, lay, 0, 1)
-e.iteration(lr=1e-3)
-e.sync()
-e.close()
+for ex in ("nccl", "p2p"):  # both ZeRO-3 exchanges (fused peer-memory kernels at world 1)
+    e = Engine(tz, mz, {"policy": "tencache"})
+    e.seed(0)
+    Z.enable(e, lay, 0, 1, exchange=ex)
+    e.iteration(lr=1e-3)
+    e.iteration(lr=1e-3, last=True)
+    e.sync()
+    e.close()
 print("sanitize workload done")
