@@ -205,7 +205,9 @@ def run_ours(args):
     t0 = time.perf_counter()
     eng = Engine(info["trace"], info["machine"], cfg, nvme_dir=nvme_dir, direct_io=args.direct_io,
                  opt_stage_slots=args.stages, gpu_spare_slots=args.gpu_spares)
+    t_create = time.perf_counter() - t0
     eng.seed(0)
+    t_seed = time.perf_counter() - t0 - t_create
     if args.config == "c3":  # ZeRO-3 exchange inside the step (NCCL, world size 1 here)
         from paper_2511_14124_b200 import zero3 as Z
         Z.enable(eng, info["layout"], 0, 1)
@@ -343,6 +345,7 @@ def run_ours(args):
                 "path": "Engine.iteration (ctypes C-ABI tc_engine_iteration), host wall clock"},
         "gpu_launches": int(st["kernel_launches"]),
         "setup_s": round(setup_s, 2),
+        "setup_breakdown_s": {"engine_create_pin_and_carve": round(t_create, 2), "seed": round(t_seed, 2)},
     }
     del eng
     if not args.no_cpu_baseline and args.config == "c2":

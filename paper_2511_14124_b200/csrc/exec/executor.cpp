@@ -4,6 +4,7 @@
 #include <nvtx3/nvToolsExt.h>
 
 #include <fcntl.h>
+#include <sys/mman.h>
 #include <unistd.h>
 
 #include <algorithm>
@@ -59,6 +60,32 @@ void EventArena::recycle_upto(std::uint64_t gen) {
 void EventArena::recycle_all() { recycle_upto(~0ull); }
 
 // -------------------------------------------------------------- SlotPool
+// Pinned host memory for the pools: anonymous mmap backed by transparent huge
+// pages, first-touched by all host threads, then cudaHostRegister. Measured
+// on the B200 boxes (tools/pin_probe.cpp, 16 GiB): cudaHostAlloc 7.0 s, this
+// 0.72 s (4 KiB pages: 2.4 s) — pinning cost is per page. Returns null (the
+// caller falls back to cudaHostAlloc) if the registration is refused.
+static std::uint8_t* pin_region(std::uint64_t bytes, std::uint64_t* mapped_len) {
+  void* p = mmap(nullptr, bytes, PROT_READ | PROT_WRITE, MAP_PRIVATE | MAP_ANONYMOUS, -1, 0);
+  if (p == MAP_FAILED) return nullptr;
+  madvise(p, bytes, MADV_HUGEPAGE);
+  const unsigned nt = std::max(1u, std::min(16u, std::thread::hardware_concurrency()));
+  std::vector<std::thread> th;
+  for (unsigned k = 0; k < nt; ++k)
+    th.emplace_back([=] {
+      const std::uint64_t per = (bytes / nt) & ~((2ull << 20) - 1), b = k * per, e = k + 1 == nt ? bytes : b + per;
+      std::memset(static_cast<char*>(p) + b, 0, e - b);
+    });
+  for (auto& t : th) t.join();
+  if (cudaHostRegister(p, bytes, cudaHostRegisterPortable) != cudaSuccess) {
+    cudaGetLastError();
+    munmap(p, bytes);
+    return nullptr;
+  }
+  *mapped_len = bytes;
+  return static_cast<std::uint8_t*>(p);
+}
+
 // One region per tier carved in ascending class order (bufpool.cpp:47-66).
 // Host regions are pinned in pieces of at most 16 GiB (whole slots each): a
 // single ~80 GB cudaHostAlloc is fragile on VMs, slots never straddle pieces.
@@ -71,39 +98,55 @@ void SlotPool::allocate(bool device, int dev) {
   std::vector<std::pair<std::uint64_t, std::uint32_t>> slots;  // (size, class) in carving order
   for (const auto& [size, n] : want_)
     for (std::uint32_t i = 0; i < n; ++i) slots.emplace_back(size, i);
-  std::size_t k = 0;
-  while (k < slots.size()) {
+  // region plan: whole slots per piece
+  std::vector<std::pair<std::size_t, std::size_t>> ranges;  // [begin, end) of slots
+  std::vector<std::uint64_t> pieces;
+  for (std::size_t k = 0; k < slots.size();) {
     std::uint64_t piece = 0;
     std::size_t end = k;
     while (end < slots.size() && (piece == 0 || piece + slots[end].first <= kRegion || device)) piece += slots[end++].first;
-    std::uint8_t* base = nullptr;
-    if (device)
-      TCB_CK(cudaMalloc(&base, piece));
-    else
-      TCB_CK(cudaHostAlloc(reinterpret_cast<void**>(&base), piece, cudaHostAllocPortable));
-    regions_.push_back(base);
-    std::uint64_t off = 0;
-    for (; k < end; ++k) {
-      SlotClass& c = classes_[slots[k].first];
-      c.size = slots[k].first;
-      Slot s;
-      s.ptr = base + off;
-      off += slots[k].first;
-      c.free_fifo.push_back(static_cast<std::uint32_t>(c.slots.size()));
-      c.slots.push_back(s);
+    ranges.emplace_back(k, end);
+    pieces.push_back(piece);
+    k = end;
+  }
+  regions_.assign(pieces.size(), nullptr);
+  if (device) {
+    for (std::size_t r = 0; r < pieces.size(); ++r) TCB_CK(cudaMalloc(&regions_[r], pieces[r]));
+  } else {
+    mapped_.assign(pieces.size(), 0);
+    for (std::size_t r = 0; r < pieces.size(); ++r) {
+      regions_[r] = pin_region(pieces[r], &mapped_[r]);
+      if (!regions_[r]) TCB_CK(cudaHostAlloc(reinterpret_cast<void**>(&regions_[r]), pieces[r], cudaHostAllocPortable));
     }
   }
-  (void)dev;
+  for (std::size_t r = 0; r < pieces.size(); ++r) {
+    std::uint64_t off = 0;
+    for (std::size_t k = ranges[r].first; k < ranges[r].second; ++k) {
+      SlotClass& c = classes_[slots[k].first];
+      c.size = slots[k].first;
+      Slot sl;
+      sl.ptr = regions_[r] + off;
+      off += slots[k].first;
+      c.free_fifo.push_back(static_cast<std::uint32_t>(c.slots.size()));
+      c.slots.push_back(sl);
+    }
+  }
 }
 
 void SlotPool::release_memory() {
-  for (std::uint8_t* r : regions_) {
-    if (device_)
+  for (std::size_t i = 0; i < regions_.size(); ++i) {
+    std::uint8_t* r = regions_[i];
+    if (device_) {
       cudaFree(r);
-    else
+    } else if (i < mapped_.size() && mapped_[i]) {
+      cudaHostUnregister(r);
+      munmap(r, mapped_[i]);
+    } else {
       cudaFreeHost(r);
+    }
   }
   regions_.clear();
+  mapped_.clear();
 }
 
 SlotClass& SlotPool::cls(std::uint64_t size) {
@@ -129,13 +172,23 @@ std::uint64_t round_up(std::uint64_t x, std::uint64_t a) { return (x + a - 1) / 
 Executor::Executor(const std::string& trace_path, const std::string& machine_path, const std::string& cfg_json,
                    const tc_engine_options& opts)
     : opts_(opts) {
+  const bool timing = std::getenv("TC_SETUP_TIMING") != nullptr;  // diagnostic: setup phases to stderr
+  auto t_last = std::chrono::steady_clock::now();
+  auto lap = [&](const char* what) {
+    if (!timing) return;
+    const auto now = std::chrono::steady_clock::now();
+    std::fprintf(stderr, "[tencache setup] %-28s %8.3f s\n", what, std::chrono::duration<double>(now - t_last).count());
+    t_last = now;
+  };
   device_ = opts.device;
   TCB_CK(cudaSetDevice(device_));
+  lap("cuda context");
   trace_ = load_trace(trace_path);
   machine_ = machine_from(machine_path.c_str());
   cfg_ = parse_run_config(cfg_json.c_str());
   policy_ = make_policy(trace_, machine_, cfg_);
   policy_->init();
+  lap("trace + policy init");
 
   // tensor table
   recs_.reserve(trace_.tensors.size());
@@ -165,6 +218,7 @@ Executor::Executor(const std::string& trace_path, const std::string& machine_pat
   // logical pool sizes, plus spare slots per class.
   const int gspare = std::max(opts.gpu_spare_slots, 1), hspare = std::max(opts.host_spare_slots, 1);
   std::map<std::pair<int, std::uint64_t>, std::uint32_t> need = simulate_occupancy();
+  lap("occupancy dry run");
   if (const SchedulerState* st = policy_->scheduler_state()) {
     std::map<std::pair<int, std::uint64_t>, std::uint32_t> logical;
     for (const Chunk& c : st->gpu_pool.chunks()) ++logical[{0, c.size}];
@@ -183,8 +237,10 @@ Executor::Executor(const std::string& trace_path, const std::string& machine_pat
     host_opt_.plan(size, need[{2, size}] + hspare + 1);          // +1 transient
   }
   gpu_.allocate(true, device_);
+  lap("HBM pool");
   host_param_.allocate(false, device_);
   host_opt_.allocate(false, device_);
+  lap("pinned host pools");
 
   // NVMe tier: one sparse file, a 4 KiB-aligned extent per tensor
   std::uint64_t off = 0;
@@ -215,6 +271,7 @@ Executor::Executor(const std::string& trace_path, const std::string& machine_pat
     }
   }
 
+  lap("NVMe tier files + I/O pool");
   for (const auto& [size, _] : pclass) {
     void* p = nullptr;
     TCB_CK(cudaHostAlloc(&p, size, cudaHostAllocPortable));
@@ -242,6 +299,7 @@ Executor::Executor(const std::string& trace_path, const std::string& machine_pat
     }
     pout_next_[size] = 0;
   }
+  lap("bounce + HBM stages");
   std::uint64_t gbytes = 0;
   for (const auto& r : recs_)
     if (!r.is_state) gbytes += r.bytes;

@@ -109,6 +109,7 @@ class SlotPool {
   std::map<std::uint64_t, std::uint32_t> want_;
   std::map<std::uint64_t, SlotClass> classes_;
   std::vector<std::uint8_t*> regions_;  // contiguous carving, split into <= kRegion pieces for pinning
+  std::vector<std::uint64_t> mapped_;   // host regions: mmap length (0: cudaHostAlloc fallback)
   bool device_ = false;
   std::uint64_t bytes_ = 0;
 };
