@@ -1,4 +1,4 @@
-"""The fused ZeRO-3 exchange at world size 2 — two processes sharing ONE B200
+"""The fused ZeRO-3 exchange at world sizes 2-4 — processes sharing ONE B200
 through CUDA IPC (NCCL cannot run two ranks on one GPU; the peer-memory
 protocol can). Checks: every access checksum equals the sum over ranks of the
 checksum of that rank's piece (so each rank read the right bytes of the
@@ -97,12 +97,15 @@ def _rank(rank, world, port, d, q):
         dist.destroy_process_group()
 
 
-def test_p2p_exchange_two_ranks_one_gpu():
+@pytest.mark.parametrize("world", [2, 3, 4, 8])
+def test_p2p_exchange_ranks_sharing_one_gpu(world):
+    """world 3 gives uneven shards; 4 and 8 more peers per read counter (8 = the
+    north_star box: every peer table slot in use)."""
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     d = tempfile.mkdtemp()
     port = _port()
-    ps = [ctx.Process(target=_rank, args=(r, 2, port, d, q)) for r in range(2)]
+    ps = [ctx.Process(target=_rank, args=(r, world, port, d, q)) for r in range(world)]
     for p in ps:
         p.start()
     res = {}
@@ -113,4 +116,4 @@ def test_p2p_exchange_two_ranks_one_gpu():
         p.join(timeout=60)
         if p.is_alive():
             p.kill()
-    assert res == {0: "ok", 1: "ok"}, res
+    assert res == {r: "ok" for r in range(world)}, res
