@@ -147,6 +147,26 @@ def exchanged_bytes(engine):
     return int(N.lib().tc_engine_exchanged_bytes(engine._h))
 
 
+def bind_to_gpu_numa(dev: int) -> bool:
+    """Pin this rank's threads to the CPUs local to its GPU (NVML's affinity
+    mask), so the first touch of its pinned pools and NVMe bounce memory lands
+    on the GPU's NUMA node and each rank drives its own host link. No-op where
+    NVML or the mask is unavailable."""
+    try:
+        import pynvml
+        pynvml.nvmlInit()
+        h = pynvml.nvmlDeviceGetHandleByIndex(dev)
+        words = pynvml.nvmlDeviceGetCpuAffinity(h, (os.cpu_count() + 63) // 64)
+        cpus = {64 * w + b for w, m in enumerate(words) for b in range(64) if (m >> b) & 1}
+        cpus &= set(range(os.cpu_count()))
+        if cpus:
+            os.sched_setaffinity(0, cpus)
+            return True
+    except Exception:
+        pass
+    return False
+
+
 def bench_rank(args):
     """bench.py under torchrun (N>1, or --zero3): each rank runs its own
     engine on its ZeRO-3 shard with the exchange inside the step; step time is
@@ -179,6 +199,8 @@ def bench_rank(args):
     dev = local % ndev
     shared = world > ndev
     torch.cuda.set_device(dev)
+    if not shared:
+        bind_to_gpu_numa(dev)
     if shared:
         dist.init_process_group("gloo")
         exchange = "p2p"
