@@ -194,7 +194,8 @@ def run_ours(args):
         nvme_dir = wd
     elif args.config == "c4":
         from paper_2511_14124_b200 import traces as T
-        info = T.config_c4_rank(wd, tokens=args.tokens, effective_tflops=args.tflops)
+        info = T.config_c4_rank(wd, tokens=args.tokens, effective_tflops=args.tflops,
+                                cpu_state_fraction=args.cpu_state_fraction)
         cfg = {"policy": "tencache+opt"}
         nvme_dir = tempfile.mkdtemp(dir=args.nvme_dir)
     else:
@@ -525,6 +526,9 @@ def main():
                     help="C2 cache policy on the same executor (the paper's baselines for comparison)")
     ap.add_argument("--nvme-dir", default="/tmp", help="directory of the NVMe tier file (c4)")
     ap.add_argument("--direct-io", action="store_true", help="O_DIRECT NVMe tier I/O")
+    ap.add_argument("--cpu-state-fraction", type=float, default=0.6,
+                    help="c4: share of the rank's optimizer states the CPU tier holds (the rest in NVMe); "
+                         "1.0 = the 13B ZeRO-3 rank with every state in pinned host memory")
     args = ap.parse_args()
     if args.stages is None:
         args.stages = 128 if args.config in ("c3", "c5") else 12
