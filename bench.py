@@ -205,7 +205,7 @@ def run_ours(args):
     dec_bytes, dec_h2d, dec_d2h, rep = decision_bytes_per_iter(info["trace"], info["machine"], cfg)
     t0 = time.perf_counter()
     eng = Engine(info["trace"], info["machine"], cfg, nvme_dir=nvme_dir, direct_io=args.direct_io,
-                 opt_stage_slots=args.stages, gpu_spare_slots=args.gpu_spares)
+                 opt_stage_slots=args.stages, gpu_spare_slots=args.gpu_spares, host_spare_slots=args.host_spares)
     t_create = time.perf_counter() - t0
     eng.seed(0)
     t_seed = time.perf_counter() - t0 - t_create
@@ -521,6 +521,9 @@ def main():
                     help="spare HBM slots per parameter class beyond the policy's logical GPU tier: a prefetch "
                          "lands in a free slot while the slot's previous occupant is still waiting for its "
                          "update and eviction (profiles/r01_ring_sweep.json)")
+    ap.add_argument("--host-spares", type=int, default=1,
+                    help="spare pinned-host slots per class beyond the policy's CPU pools (lets NVMe reads run ahead "
+                         "of the slot they replace)")
     ap.add_argument("--policy", default="tencache",
                     choices=["tencache", "tencache+opt", "zero-infinity", "l2l", "no-offload"],
                     help="C2 cache policy on the same executor (the paper's baselines for comparison)")

@@ -262,6 +262,20 @@ Executor::Executor(const std::string& trace_path, const std::string& machine_pat
   if (const char* c = std::getenv("TC_EDGE_FILL")) edge_fill_ = std::atoi(c) != 0;
   if (const char* c = std::getenv("TC_LOOKAHEAD")) lookahead_ = std::atoi(c) != 0;
   if (const char* c = std::getenv("TC_ADAM_STAMPS")) adam_stamps_ = std::atoi(c) != 0;
+  {  // migration-bound? trace compute time vs the optimizer states' H2D time alone (machine.cpp:101-111)
+    double compute_us = 0, state_bytes = 0;
+    for (const TraceStep& st : trace_.steps)
+      if (st.phase != Phase::OptimizerUpdate) compute_us += st.compute_us * cfg_.batch_scale;
+    for (const auto& r : recs_)
+      if (r.is_state) state_bytes += static_cast<double>(r.bytes);
+    try {
+      const double bw = to_double(machine_.effective_bandwidth(Tier::Cpu, Tier::Gpu)) * 1e3;  // bytes per us
+      adam_on_compute_ = bw > 0 && compute_us < state_bytes / bw;
+    } catch (...) {
+      adam_on_compute_ = false;
+    }
+  }
+  if (const char* c = std::getenv("TC_ADAM_ON_COMPUTE")) adam_on_compute_ = std::atoi(c) != 0;
   if (!std::getenv("TC_SYNC_NVME")) {
     try {
       io_ = std::make_unique<NvmeQueue>(device_, nvme_.get());
@@ -841,6 +855,7 @@ void Executor::refill_stages(std::size_t want_staged) {
 }
 
 void Executor::optimizer_work(TensorRec& s, TensorRec& p) {
+  cudaStream_t ost = adam_stream();
   const bool state_on_gpu = s.tier == PTier::Gpu;  // no-offload posture: update in place in HBM
   if (!state_on_gpu && s.tier != PTier::HostOpt)
     throw DeviceError(TC_EINTERNAL, "optimizer state not in host memory at its update");
@@ -850,7 +865,7 @@ void Executor::optimizer_work(TensorRec& s, TensorRec& p) {
   if (state_on_gpu) {
     Slot& gs = slot_of(s);
     stg = gs.ptr;
-    wait_for_write(opt_, gs.sync);
+    wait_for_write(ost, gs.sync);
   } else {
     auto it = staged_.find(index_of(s.id));
     b = it != staged_.end() ? it->second : stage_state(s);
@@ -858,9 +873,9 @@ void Executor::optimizer_work(TensorRec& s, TensorRec& p) {
     stats_.opt_h2d_bytes += s.bytes;  // counted at the update it feeds (staging may be a prologue)
     stg = stage_[b];
     // (null once a drain between the prologue's staging and this update completed it)
-    if (stage_sync_[b].writer) TCB_CK(cudaStreamWaitEvent(opt_, stage_sync_[b].writer, 0));
+    if (stage_sync_[b].writer) TCB_CK(cudaStreamWaitEvent(ost, stage_sync_[b].writer, 0));
   }
-  if (p.grad_ready) TCB_CK(cudaStreamWaitEvent(opt_, p.grad_ready, 0));
+  if (p.grad_ready) TCB_CK(cudaStreamWaitEvent(ost, p.grad_ready, 0));
   std::uint8_t* pout;
   SlotSync* psync;
   const bool on_gpu = p.tier == PTier::Gpu;
@@ -874,9 +889,9 @@ void Executor::optimizer_work(TensorRec& s, TensorRec& p) {
     psync = &pout_sync_[p.bytes][k];
     k = (k + 1) % pout_scratch_[p.bytes].size();
   }
-  wait_for_write(opt_, *psync);
+  wait_for_write(ost, *psync);
   cudaEvent_t a0 = events_.get(true), a1 = events_.get(true);
-  TCB_CK(cudaEventRecord(a0, opt_));
+  TCB_CK(cudaEventRecord(a0, ost));
   auto* st = reinterpret_cast<float*>(stg);
   const AdamScalars sc = adam_scalars(so_.lr, so_.beta1, so_.beta2, so_.eps, so_.weight_decay, adam_step_);
   unsigned long long *smin = nullptr, *smax = nullptr;
@@ -886,11 +901,11 @@ void Executor::optimizer_work(TensorRec& s, TensorRec& p) {
     smax = span_base_ + cap + span_cursor_;
     ++span_cursor_;
   }
-  if (adam_stamps_ && smin) TCB_CK(launch_stamp(smin + 2 * cap, opt_));
+  if (adam_stamps_ && smin) TCB_CK(launch_stamp(smin + 2 * cap, ost));
   TCB_CK(launch_adamw(st, st + n, st + 2 * n, reinterpret_cast<const std::uint16_t*>(p.grad),
-                      reinterpret_cast<std::uint16_t*>(pout), n, sc, so_.grad_scale, opt_, smin, smax));
-  if (adam_stamps_ && smin) TCB_CK(launch_stamp(smin + 3 * cap, opt_));
-  TCB_CK(cudaEventRecord(a1, opt_));
+                      reinterpret_cast<std::uint16_t*>(pout), n, sc, so_.grad_scale, ost, smin, smax));
+  if (adam_stamps_ && smin) TCB_CK(launch_stamp(smin + 3 * cap, ost));
+  TCB_CK(cudaEventRecord(a1, ost));
   adam_.emplace_back(a0, a1);
   ++stats_.kernel_launches;
   stats_.adam_elems += n;
@@ -1059,8 +1074,8 @@ void Executor::iteration(const StepOptions& so, cudaStream_t compute) {
     const std::size_t cap = std::max<std::size_t>(recs_.size(), 1);
     span_base_ = d_span_ + (events_.generation() % 2) * 4 * cap;  // [min | max | pre stamp | post stamp]
     span_cursor_ = 0;
-    TCB_CK(launch_fill_u64(span_base_, ~0ull, cap, opt_));
-    TCB_CK(launch_fill_u64(span_base_ + cap, 0ull, cap, opt_));
+    TCB_CK(launch_fill_u64(span_base_, ~0ull, cap, adam_stream()));  // same stream as the updates
+    TCB_CK(launch_fill_u64(span_base_ + cap, 0ull, cap, adam_stream()));
   }
   TCB_CK(launch_fill_u64(reinterpret_cast<unsigned long long*>(cks_base_), 0ull, std::max<std::size_t>(n_accesses_, 1),
                          compute));
@@ -1122,7 +1137,7 @@ void Executor::iteration(const StepOptions& so, cudaStream_t compute) {
         if (hoist[h.step] == n) {  // in place: waits for the state's decisions
           TensorRec& s = rec(step.tensor_ids.front());
           if (s.partner < 0) throw DeviceError(TC_EINTERNAL, "optimizer step without a paired state");
-          wait_barriers(opt_);
+          wait_barriers(adam_stream());
           optimizer_work(s, recs_[static_cast<std::size_t>(s.partner)]);
         }
       } else {
@@ -1201,7 +1216,7 @@ void Executor::finish_iteration() {
   {  // this iteration's AdamW spans/stamps to mapped host memory, behind its last update
     const std::size_t cap = std::max<std::size_t>(recs_.size(), 1);
     TCB_CK(launch_copy_u64(reinterpret_cast<unsigned long long*>(d_span_host_) + (events_.generation() % 2) * 4 * cap,
-                           span_base_, 4 * cap, opt_));
+                           span_base_, 4 * cap, adam_stream()));
   }
   IterRecord rec;
   rec.gen = events_.generation();

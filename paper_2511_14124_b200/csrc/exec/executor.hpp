@@ -303,6 +303,14 @@ class Executor {
   int prestage_fwd_override_ = -1;  // TC_PRESTAGE_FWD: states staged for the forward (-1: bandwidth model)
   bool prestage_gate_ = false;      // TC_PRESTAGE_GATE: forward refill waits for the last cache prefetch
   bool adam_stamps_ = false;        // TC_ADAM_STAMPS: %globaltimer stamps around each AdamW (diagnostic)
+  // Updates on the compute stream when the trace is migration-bound (the
+  // compute stream idles on copies anyway, and a same-stream launch skips the
+  // cross-stream scheduling latency); on the opt stream when compute-bound, to
+  // overlap. TC_ADAM_ON_COMPUTE=0/1 overrides.
+  bool adam_on_compute_ = false;
+  // never with a ZeRO-3 exchange: an in-place update may wait for peers'
+  // reads of its slot, which must not stall this rank's compute stream
+  cudaStream_t adam_stream() const { return adam_on_compute_ && compute_ && !z3_ ? compute_ : opt_; }
   double stamp_pre_ns_ = 0, stamp_post_ns_ = 0, stamps_ = 0;
   bool lookahead_ = true;           // TC_LOOKAHEAD: decide + pre-stage iteration t+1 at the end of t
   std::optional<std::vector<Hook>> ahead_;

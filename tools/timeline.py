@@ -20,9 +20,12 @@ stages = int(os.environ.get("STAGES", "12"))
 wd = tempfile.mkdtemp(dir="/dev/shm")
 if cfgname == "c5":
     info = T.config_c5_rank(wd)
+elif cfgname == "c4":
+    info = T.config_c4_rank(wd)
 else:
     info = T.config_c2(wd, iterations=1)
-eng = Engine(info["trace"], info["machine"], {"policy": "tencache"}, opt_stage_slots=stages)
+pol = "tencache+opt" if cfgname == "c4" else "tencache"
+eng = Engine(info["trace"], info["machine"], {"policy": pol}, opt_stage_slots=stages, nvme_dir=wd)
 eng.seed(0)
 os.makedirs("gpurun_out", exist_ok=True)
 log = f"gpurun_out/timeline_{cfgname}.jsonl"
