@@ -508,14 +508,20 @@ void Executor::wait_for_read(cudaStream_t s, const SlotSync& y) {
 void Executor::wait_for_write(cudaStream_t s, const SlotSync& y) {
   if (y.writer) TCB_CK(cudaStreamWaitEvent(s, y.writer, 0));
   for (cudaEvent_t e : y.readers) TCB_CK(cudaStreamWaitEvent(s, e, 0));
-  if (io_) io_->stream_wait(s, std::max(y.io_read, y.io_write));
+  if (io_) {
+    io_->stream_wait(s, y.io_read);
+    io_->stream_wait(s, y.io_write);
+  }
   if (y.peer_cnt && y.peer_target) stream_wait_value32(s, y.peer_cnt, y.peer_target);
 }
 
 void Executor::host_wait_all(const SlotSync& y) {
   if (y.writer) TCB_CK(cudaEventSynchronize(y.writer));
   for (cudaEvent_t e : y.readers) TCB_CK(cudaEventSynchronize(e));
-  if (io_) io_->wait(std::max(y.io_read, y.io_write));
+  if (io_) {
+    io_->wait(y.io_read);
+    io_->wait(y.io_write);
+  }
 }
 
 // The I/O worker waits on events later, on its own thread; an event it names
@@ -540,7 +546,7 @@ std::uint64_t Executor::nvme_read_async(TensorRec& r, void* dst, SlotSync& targe
   // after: the buffer's previous job and the extent's previous job (a pending
   // write of the same tensor must land before it is read back)
   const std::uint64_t k = io_->submit_read(dst, r.bytes, r.nvme_off, io_deps(std::move(waits)),
-                                           std::max({target.io_read, target.io_write, r.nvme_job}));
+                                           {target.io_read, target.io_write, r.nvme_job});
   r.nvme_job = k;
   target = SlotSync{};
   target.io_write = k;
@@ -554,7 +560,10 @@ std::uint64_t Executor::nvme_write_async(TensorRec& r, const void* src, SlotSync
   std::vector<cudaEvent_t> waits;
   if (source.writer) waits.push_back(source.writer);
   const std::uint64_t k =
-      io_->submit_write(src, r.bytes, r.nvme_off, io_deps(std::move(waits)), std::max(source.io_write, r.nvme_job));
+      io_->submit_write(src, r.bytes, r.nvme_off, io_deps(std::move(waits)),
+                        // the buffer's previous reader too: source.io_read must keep naming a job
+                        // whose completion implies every earlier read of the buffer finished
+                        {source.io_write, source.io_read, r.nvme_job});
   r.nvme_job = k;
   source.io_read = k;
   r.nvme_valid = true;
@@ -782,7 +791,7 @@ void Executor::apply(const Req& r) {
 void Executor::wait_barriers(cudaStream_t cs) {
   for (cudaEvent_t e : barriers_) TCB_CK(cudaStreamWaitEvent(cs, e, 0));
   barriers_.clear();
-  if (barrier_io_ && io_) io_->stream_wait(cs, barrier_io_);
+  if (barrier_io_ && io_) io_->stream_wait_upto(cs, barrier_io_);
   barrier_io_ = 0;
 }
 
@@ -1274,7 +1283,7 @@ void Executor::harvest_front() {
       std::this_thread::sleep_for(std::chrono::microseconds(50));
     }
   }
-  if (io_) io_->wait(rec.io_seq);  // no queued job may still name an event we recycle
+  if (io_) io_->wait_upto(rec.io_seq);  // no queued job may still name an event we recycle
   float ms = 0;
   phase_ms_.clear();
   for (std::size_t i = 0; i + 1 < rec.marks.size(); ++i) {

@@ -73,6 +73,10 @@ bool StripedFile::io(bool write, std::uint8_t* buf, std::uint64_t bytes, std::ui
   return true;
 }
 
+static double now_s() {
+  return std::chrono::duration<double>(std::chrono::steady_clock::now().time_since_epoch()).count();
+}
+
 NvmeQueue::NvmeQueue(int device, const StripedFile* file) : device_(device), file_(file) {
   void* fn = nullptr;
   cudaDriverEntryPointQueryResult q;
@@ -87,6 +91,13 @@ NvmeQueue::NvmeQueue(int device, const StripedFile* file) : device_(device), fil
   *flag_ = 0;
   if (cudaHostGetDevicePointer(&flag_dev_, h, 0) != cudaSuccess)
     throw DeviceError(TC_ECUDA, "cannot map the NVMe completion word");
+  void* rh = nullptr;
+  if (cudaHostAlloc(&rh, sizeof(std::uint32_t) * kRing, cudaHostAllocMapped | cudaHostAllocPortable) != cudaSuccess)
+    throw DeviceError(TC_ECUDA, "cannot allocate the NVMe completion ring");
+  ring_ = static_cast<volatile std::uint32_t*>(rh);
+  for (std::uint32_t i = 0; i < kRing; ++i) ring_[i] = 0;
+  if (cudaHostGetDevicePointer(&ring_dev_, rh, 0) != cudaSuccess)
+    throw DeviceError(TC_ECUDA, "cannot map the NVMe completion ring");
   // probe once: a satisfied wait must be accepted by this driver/device
   cudaStream_t s;
   cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking);
@@ -97,6 +108,7 @@ NvmeQueue::NvmeQueue(int device, const StripedFile* file) : device_(device), fil
   cudaStreamDestroy(s);
   if (r != CUDA_SUCCESS) {
     cudaFreeHost(h);
+    cudaFreeHost(rh);
     throw DeviceError(TC_ECUDA, "stream memory operations unsupported");
   }
   dispatcher_ = std::thread([this] { dispatch(); });
@@ -106,6 +118,9 @@ NvmeQueue::NvmeQueue(int device, const StripedFile* file) : device_(device), fil
 }
 
 NvmeQueue::~NvmeQueue() {
+  if (std::getenv("TC_NVME_STATS"))
+    std::fprintf(stderr, "[nvme] %llu reads waited %.3f s, %llu writes waited %.3f s between submit and dispatch\n",
+                 static_cast<unsigned long long>(jobs_r_), wait_r_, static_cast<unsigned long long>(jobs_w_), wait_w_);
   {
     std::lock_guard<std::mutex> g(mu_);
     stop_ = true;
@@ -116,6 +131,7 @@ NvmeQueue::~NvmeQueue() {
   for (auto& w : workers_)
     if (w.joinable()) w.join();
   if (flag_) cudaFreeHost(const_cast<std::uint32_t*>(flag_));
+  if (ring_) cudaFreeHost(const_cast<std::uint32_t*>(ring_));
 }
 
 static const bool kDebug = std::getenv("TC_NVME_DEBUG") != nullptr;
@@ -124,10 +140,12 @@ std::uint64_t NvmeQueue::submit(Job j) {
   std::lock_guard<std::mutex> g(mu_);
   if (!error_.empty()) throw DeviceError(TC_EIO, error_);
   j.seq = ++submitted_;
+  j.t_submit = now_s();
+  std::erase(j.after, 0ull);
   if (kDebug)
-    std::fprintf(stderr, "[nvme] submit %llu %s %llu B @%llu waits=%zu\n", static_cast<unsigned long long>(j.seq),
-                 j.write ? "W" : "R", static_cast<unsigned long long>(j.bytes), static_cast<unsigned long long>(j.off),
-                 j.waits.size());
+    std::fprintf(stderr, "[nvme] submit %llu %s %llu B @%llu waits=%zu after=%zu\n",
+                 static_cast<unsigned long long>(j.seq), j.write ? "W" : "R", static_cast<unsigned long long>(j.bytes),
+                 static_cast<unsigned long long>(j.off), j.waits.size(), j.after.size());
   (j.write ? bytes_written_ : bytes_read_) += j.bytes;
   q_.push_back(std::move(j));
   cv_.notify_one();
@@ -135,16 +153,42 @@ std::uint64_t NvmeQueue::submit(Job j) {
 }
 
 std::uint64_t NvmeQueue::submit_read(void* dst, std::uint64_t bytes, std::uint64_t off, std::vector<cudaEvent_t> w,
-                                     std::uint64_t after) {
-  return submit(Job{false, dst, bytes, off, 0, std::move(w), after});
+                                     std::vector<std::uint64_t> after) {
+  return submit(Job{false, dst, bytes, off, 0, std::move(w), std::move(after)});
 }
 
 std::uint64_t NvmeQueue::submit_write(const void* src, std::uint64_t bytes, std::uint64_t off,
-                                      std::vector<cudaEvent_t> w, std::uint64_t after) {
-  return submit(Job{true, const_cast<void*>(src), bytes, off, 0, std::move(w), after});
+                                      std::vector<cudaEvent_t> w, std::vector<std::uint64_t> after) {
+  return submit(Job{true, const_cast<void*>(src), bytes, off, 0, std::move(w), std::move(after)});
 }
 
+std::uint64_t NvmeQueue::done() const {
+  std::lock_guard<std::mutex> g(mu_);
+  return done_;
+}
+
+std::uint64_t NvmeQueue::submitted() const {
+  std::lock_guard<std::mutex> g(mu_);
+  return submitted_;
+}
+
+// A job's own completion word: a GPU stream waits for exactly the job it
+// consumes, never for unrelated earlier jobs (which may be waiting on GPU work
+// queued behind it).
 void NvmeQueue::stream_wait(cudaStream_t s, std::uint64_t seq) {
+  if (seq == 0) return;
+  {
+    std::lock_guard<std::mutex> g(mu_);
+    if (is_done(seq)) return;
+  }
+  auto* word = static_cast<std::uint32_t*>(ring_dev_) + (seq % kRing);
+  const CUresult r = reinterpret_cast<WaitValue32>(wait_fn_)(
+      reinterpret_cast<CUstream>(s), reinterpret_cast<CUdeviceptr>(word), static_cast<cuuint32_t>(seq),
+      CU_STREAM_WAIT_VALUE_GEQ);
+  if (r != CUDA_SUCCESS) throw DeviceError(TC_ECUDA, "cuStreamWaitValue32 failed");
+}
+
+void NvmeQueue::stream_wait_upto(cudaStream_t s, std::uint64_t seq) {
   if (seq == 0 || seq <= done()) return;
   const CUresult r = reinterpret_cast<WaitValue32>(wait_fn_)(
       reinterpret_cast<CUstream>(s), reinterpret_cast<CUdeviceptr>(flag_dev_), static_cast<cuuint32_t>(seq),
@@ -154,22 +198,28 @@ void NvmeQueue::stream_wait(cudaStream_t s, std::uint64_t seq) {
 
 std::string NvmeQueue::describe() {
   std::lock_guard<std::mutex> g(mu_);
-  std::string s = "nvme queue: submitted " + std::to_string(submitted_) + " done " + std::to_string(done_) +
+  std::string s = "nvme queue: submitted " + std::to_string(submitted_) + " watermark " + std::to_string(done_) +
                   " flag " + std::to_string(*flag_) + " queued " + std::to_string(q_.size()) + " pieces " +
-                  std::to_string(pieces_.size()) + " dispatching " + std::to_string(dispatching_) + " phase " +
-                  std::to_string(dispatch_phase_) + " open:";
+                  std::to_string(pieces_.size()) + " complete-above-watermark " + std::to_string(completed_.size()) +
+                  " in flight:";
   int k = 0;
   for (const auto& [seq, left] : remaining_) {
     if (k++ > 8) break;
     s += " " + std::to_string(seq) + "(" + std::to_string(static_cast<int>(left)) + ")";
   }
+  if (!q_.empty()) {
+    const Job& j = q_.front();
+    s += "; oldest queued " + std::to_string(j.seq) + (j.write ? " W" : " R") + " after:";
+    for (std::uint64_t a : j.after) s += " " + std::to_string(a) + (is_done(a) ? "(done)" : "(open)");
+  }
   return s;
 }
 
 void NvmeQueue::wait(std::uint64_t seq) {
+  if (seq == 0) return;
   if (kDebug) std::fprintf(stderr, "[nvme] host wait %llu\n", static_cast<unsigned long long>(seq));
   std::unique_lock<std::mutex> g(mu_);
-  while (!done_cv_.wait_for(g, std::chrono::seconds(30), [&] { return done_ >= seq || !error_.empty(); })) {
+  while (!done_cv_.wait_for(g, std::chrono::seconds(30), [&] { return is_done(seq) || !error_.empty(); })) {
     g.unlock();
     std::fprintf(stderr, "[nvme] still waiting for job %llu: %s\n", static_cast<unsigned long long>(seq),
                  describe().c_str());
@@ -178,35 +228,54 @@ void NvmeQueue::wait(std::uint64_t seq) {
   if (!error_.empty()) throw DeviceError(TC_EIO, error_);
 }
 
-std::uint64_t NvmeQueue::done() const {
-  std::lock_guard<std::mutex> g(const_cast<std::mutex&>(mu_));
-  return done_;
+void NvmeQueue::wait_upto(std::uint64_t seq) {
+  if (seq == 0) return;
+  std::unique_lock<std::mutex> g(mu_);
+  while (!done_cv_.wait_for(g, std::chrono::seconds(30), [&] { return done_ >= seq || !error_.empty(); })) {
+    g.unlock();
+    std::fprintf(stderr, "[nvme] still waiting for jobs up to %llu: %s\n", static_cast<unsigned long long>(seq),
+                 describe().c_str());
+    g.lock();
+  }
+  if (!error_.empty()) throw DeviceError(TC_EIO, error_);
 }
 
-// Jobs in FIFO order: await their events, then fan out pieces of <= 16 MiB.
+int NvmeQueue::ready(const Job& j) {
+  for (std::uint64_t a : j.after)
+    if (!is_done(a)) return 0;
+  for (cudaEvent_t e : j.waits) {
+    if (!e) continue;
+    const cudaError_t q = cudaEventQuery(e);
+    if (q == cudaErrorNotReady) return 0;
+    if (q != cudaSuccess) return -1;
+  }
+  return 1;
+}
+
+// Out-of-order dispatch: the first queued job whose events have completed and
+// whose `after` jobs are done is split into pieces of <= 16 MiB for the pool;
+// when none is ready the dispatcher re-polls (events complete without notice).
 void NvmeQueue::dispatch() {
   cudaSetDevice(device_);
   constexpr std::uint64_t kPiece = 16ull << 20;
+  std::unique_lock<std::mutex> g(mu_);
   for (;;) {
-    Job j;
-    {
-      std::unique_lock<std::mutex> g(mu_);
-      cv_.wait(g, [&] { return stop_ || !q_.empty(); });
-      if (q_.empty()) return;
-      j = std::move(q_.front());
-      q_.pop_front();
-      remaining_[j.seq] = ~0u;  // open (not yet split) until its pieces are queued
-      dispatching_ = j.seq;
-      dispatch_phase_ = 1;
+    if (stop_ && q_.empty()) return;
+    auto it = q_.begin();
+    int st = 0;
+    for (; it != q_.end(); ++it) {
+      if (it->seq >= done_ + kRing / 2) break;  // completion-ring window
+      if ((st = ready(*it)) != 0) break;
     }
-    bool ok = true;
-    for (cudaEvent_t e : j.waits)
-      if (e && cudaEventSynchronize(e) != cudaSuccess) ok = false;
-    std::unique_lock<std::mutex> g(mu_);
-    dispatch_phase_ = 2;
-    if (j.after) done_cv_.wait(g, [&] { return done_ >= j.after || !error_.empty(); });  // same-buffer order
-    dispatch_phase_ = 3;
-    if (!ok) error_ = "event wait failed before NVMe I/O";
+    if (it == q_.end() || st == 0) {
+      cv_.wait_for(g, std::chrono::microseconds(50));
+      continue;
+    }
+    Job j = std::move(*it);
+    q_.erase(it);
+    if (st < 0) error_ = "event wait failed before NVMe I/O";
+    (j.write ? wait_w_ : wait_r_) += now_s() - j.t_submit;
+    ++(j.write ? jobs_w_ : jobs_r_);
     const std::uint64_t n = std::max<std::uint64_t>(1, (j.bytes + kPiece - 1) / kPiece);
     remaining_[j.seq] = static_cast<std::uint32_t>(n);
     for (std::uint64_t k = 0; k < n; ++k) {
@@ -232,25 +301,28 @@ void NvmeQueue::work() {
   }
 }
 
-// A job is complete when its last piece lands; the published watermark is
-// the highest seq below which every job is complete.
+// A job is complete when its last piece lands: its ring word is published,
+// and the watermark advances over every contiguous complete job. Both are
+// stored under the lock (a watermark must never regress: a GPU stream waiting
+// for a value above a regressed word hangs).
 void NvmeQueue::piece_done(std::uint64_t seq, bool ok) {
   std::lock_guard<std::mutex> g(mu_);
   if (!ok) error_ = "NVMe tier I/O failed";
-  if (--remaining_[seq] == 0) remaining_.erase(seq);
-  // open = being dispatched or with pieces in flight (remaining_), or still queued (q_)
-  const std::uint64_t oldest_open = remaining_.empty() ? submitted_ + 1 : remaining_.begin()->first;
-  const std::uint64_t first_queued = q_.empty() ? submitted_ + 1 : q_.front().seq;
-  const std::uint64_t mark = std::min(oldest_open, first_queued) - 1;
+  if (--remaining_[seq] != 0) return;
+  remaining_.erase(seq);
+  completed_.insert(seq);
+  __atomic_store_n(const_cast<std::uint32_t*>(ring_ + (seq % kRing)), static_cast<std::uint32_t>(seq),
+                   __ATOMIC_RELEASE);
+  while (!completed_.empty() && *completed_.begin() == done_ + 1) {
+    completed_.erase(completed_.begin());
+    ++done_;
+  }
+  __atomic_store_n(const_cast<std::uint32_t*>(flag_), static_cast<std::uint32_t>(done_), __ATOMIC_RELEASE);
   if (kDebug)
-    std::fprintf(stderr, "[nvme] piece of %llu done; mark %llu (done %llu)\n", static_cast<unsigned long long>(seq),
-                 static_cast<unsigned long long>(mark), static_cast<unsigned long long>(done_));
-  if (mark <= done_) return;
-  done_ = mark;
-  // published under the lock: two workers must never store the watermark out
-  // of order (a GPU stream waiting for a value above a regressed word hangs)
-  __atomic_store_n(const_cast<std::uint32_t*>(flag_), static_cast<std::uint32_t>(mark), __ATOMIC_RELEASE);
+    std::fprintf(stderr, "[nvme] job %llu done; watermark %llu\n", static_cast<unsigned long long>(seq),
+                 static_cast<unsigned long long>(done_));
   done_cv_.notify_all();
+  cv_.notify_one();  // a queued job may have been waiting for this one
 }
 
 }  // namespace tcb

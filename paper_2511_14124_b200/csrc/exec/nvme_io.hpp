@@ -15,6 +15,7 @@
 #include <map>
 #include <string>
 #include <mutex>
+#include <set>
 #include <thread>
 #include <vector>
 
@@ -51,28 +52,33 @@ class NvmeQueue {
   NvmeQueue(int device, const StripedFile* file);
   ~NvmeQueue();
 
-  // `after`: an earlier job on the same host buffer that must be complete
-  // before this one starts (jobs otherwise run concurrently in the pool).
+  // `after`: earlier jobs that must be complete before this one starts (the
+  // buffer's previous jobs, the file extent's previous job). Jobs otherwise
+  // start out of order, as soon as their events and `after` jobs are done.
   std::uint64_t submit_read(void* dst, std::uint64_t bytes, std::uint64_t file_off, std::vector<cudaEvent_t> waits,
-                            std::uint64_t after = 0);
+                            std::vector<std::uint64_t> after = {});
   std::uint64_t submit_write(const void* src, std::uint64_t bytes, std::uint64_t file_off,
-                             std::vector<cudaEvent_t> waits, std::uint64_t after = 0);
-  void stream_wait(cudaStream_t s, std::uint64_t seq);  // GPU-side wait for job `seq`
-  void wait(std::uint64_t seq);                         // host-side wait
-  void wait_all() { wait(submitted_); }
-  std::uint64_t done() const;
-  std::uint64_t submitted() const { return submitted_; }
+                             std::vector<cudaEvent_t> waits, std::vector<std::uint64_t> after = {});
+  void stream_wait(cudaStream_t s, std::uint64_t seq);       // GPU-side wait for job `seq` alone
+  void stream_wait_upto(cudaStream_t s, std::uint64_t seq);  // GPU-side wait for every job <= seq
+  void wait(std::uint64_t seq);                              // host-side wait for job `seq`
+  void wait_upto(std::uint64_t seq);                         // host-side wait for every job <= seq
+  void wait_all() { wait_upto(submitted()); }
+  std::uint64_t done() const;  // watermark: every job <= done() is complete
+  std::uint64_t submitted() const;
   std::uint64_t bytes_read() const { return bytes_read_; }
   std::string describe();  // state dump for hang diagnostics
   std::uint64_t bytes_written() const { return bytes_written_; }
 
  private:
+  static constexpr std::uint32_t kRing = 1u << 16;  // per-job completion words (seq % kRing)
   struct Job {
     bool write;
     void* buf;
     std::uint64_t bytes, off, seq;
     std::vector<cudaEvent_t> waits;
-    std::uint64_t after = 0;
+    std::vector<std::uint64_t> after;
+    double t_submit = 0;  // steady-clock seconds (TC_NVME_STATS)
   };
   struct Piece {
     bool write;
@@ -83,25 +89,30 @@ class NvmeQueue {
   void dispatch();
   void work();
   void piece_done(std::uint64_t seq, bool ok);
+  bool is_done(std::uint64_t seq) const { return seq <= done_ || completed_.count(seq) != 0; }  // mu_ held
+  int ready(const Job& j);  // mu_ held: 1 ready, 0 not yet, -1 event failed
 
   int device_;
   const StripedFile* file_;
   std::deque<Piece> pieces_;
-  std::map<std::uint64_t, std::uint32_t> remaining_;  // seq -> pieces left
+  std::map<std::uint64_t, std::uint32_t> remaining_;  // seq -> pieces left (dispatched jobs)
+  std::set<std::uint64_t> completed_;                 // complete jobs above the watermark
   std::condition_variable piece_cv_;
   std::vector<std::thread> workers_;
-  volatile std::uint32_t* flag_ = nullptr;  // mapped pinned word: last completed seq
+  volatile std::uint32_t* flag_ = nullptr;  // mapped pinned word: the watermark
   void* flag_dev_ = nullptr;
+  volatile std::uint32_t* ring_ = nullptr;  // mapped pinned words: ring_[seq % kRing] = seq once complete
+  void* ring_dev_ = nullptr;
   void* wait_fn_ = nullptr;                 // cuStreamWaitValue32
-  std::mutex mu_;
+  mutable std::mutex mu_;
   std::condition_variable cv_, done_cv_;
-  std::deque<Job> q_;
+  std::deque<Job> q_;  // submitted, not yet dispatched (submission order)
   std::uint64_t submitted_ = 0, done_ = 0, bytes_read_ = 0, bytes_written_ = 0;
-  std::uint64_t dispatching_ = 0;  // job the dispatcher is on
-  int dispatch_phase_ = 0;         // 0 idle, 1 events, 2 after, 3 split
   bool stop_ = false;
   std::string error_;
   std::thread dispatcher_;
+  double wait_r_ = 0, wait_w_ = 0;  // TC_NVME_STATS: submit -> dispatch time
+  std::uint64_t jobs_r_ = 0, jobs_w_ = 0;
 };
 
 }  // namespace tcb
