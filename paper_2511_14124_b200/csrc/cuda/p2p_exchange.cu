@@ -116,6 +116,49 @@ __device__ __forceinline__ std::uint32_t rne_bf16(float f) {
   return (u + 0x7fffu + ((u >> 16) & 1u)) >> 16;
 }
 
+// U units of 8 elements per iteration while all U are inside the valid
+// range and world <= W: U x world 16-byte loads issued before the sums.
+// Advances i0 past the units it handled; same fp32 rank order as the kernel.
+template <int U, int W>
+__device__ __forceinline__ void pull_units(const PullArgs& a, std::uint64_t& i0, std::uint64_t stride,
+                                           std::uint64_t valid) {
+  if (a.t.world > W) return;
+  for (; i0 + (U - 1) * stride + 8 <= valid; i0 += U * stride) {
+    uint4 w[U][W];
+#pragma unroll
+    for (int u = 0; u < U; ++u)
+#pragma unroll
+      for (int q = 0; q < W; ++q)
+        if (q < a.t.world) w[u][q] = *reinterpret_cast<const uint4*>(a.t.gview[q] + a.view_off + (i0 + u * stride) * 2);
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      float acc[8];
+      const std::uint32_t* w0 = reinterpret_cast<const std::uint32_t*>(&w[u][0]);
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        acc[2 * k] = __uint_as_float(w0[k] << 16);
+        acc[2 * k + 1] = __uint_as_float(w0[k] & 0xffff0000u);
+      }
+#pragma unroll
+      for (int q = 1; q < W; ++q) {
+        if (q >= a.t.world) break;
+        const std::uint32_t* wq = reinterpret_cast<const std::uint32_t*>(&w[u][q]);
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+          acc[2 * k] += __uint_as_float(wq[k] << 16);
+          acc[2 * k + 1] += __uint_as_float(wq[k] & 0xffff0000u);
+        }
+      }
+      uint4 o;
+      o.x = rne_bf16(acc[0]) | (rne_bf16(acc[1]) << 16);
+      o.y = rne_bf16(acc[2]) | (rne_bf16(acc[3]) << 16);
+      o.z = rne_bf16(acc[4]) | (rne_bf16(acc[5]) << 16);
+      o.w = rne_bf16(acc[6]) | (rne_bf16(acc[7]) << 16);
+      *reinterpret_cast<uint4*>(a.grad + i0 + u * stride) = o;
+    }
+  }
+}
+
 // Each thread reduces 8 bf16 values across all ranks' views (fp32, rank
 // order, one rounding); padding of the chunk is written as zero.
 __global__ void __launch_bounds__(kThr) pull_reduce_kernel(PullArgs a) {
@@ -124,8 +167,13 @@ __global__ void __launch_bounds__(kThr) pull_reduce_kernel(PullArgs a) {
       while (ld_acquire_sys(&a.t.ctl[q]->gpub) < a.gepoch) __nanosleep(200);
   __syncthreads();
   const std::uint64_t n = a.chunk_bytes / 2, valid = a.bytes / 2;
-  for (std::uint64_t i = (static_cast<std::uint64_t>(blockIdx.x) * kThr + threadIdx.x) * 8; i < n;
-       i += static_cast<std::uint64_t>(gridDim.x) * kThr * 8) {
+  const std::uint64_t stride = static_cast<std::uint64_t>(gridDim.x) * kThr * 8;
+  std::uint64_t i0 = (static_cast<std::uint64_t>(blockIdx.x) * kThr + threadIdx.x) * 8;
+  if (a.vec && a.t.world <= 4) {  // U units per iteration: U x world 16-byte loads in flight per thread
+    pull_units<4, 2>(a, i0, stride, valid);  // world <= 2
+    pull_units<2, 4>(a, i0, stride, valid);  // world <= 4 (and the rest of world <= 2)
+  }
+  for (std::uint64_t i = i0; i < n; i += stride) {
     if (a.vec && i + 8 <= valid) {  // 16 bytes per rank per thread, same fp32 order as below
       uint4 w[kMaxPeers];
 #pragma unroll
@@ -244,7 +292,10 @@ cudaError_t launch_p2p_pull_reduce(const PeerTable& t, std::uint32_t gepoch, std
   for (int q = 0; q < t.world; ++q) al |= reinterpret_cast<std::uintptr_t>(t.gview[q]);
   a.vec = (al & 15) == 0 ? 1 : 0;
   const std::uint64_t units = (chunk_bytes / 2 + 8 * kThr - 1) / (8 * kThr);
-  const unsigned grid = static_cast<unsigned>(std::max<std::uint64_t>(1, std::min<std::uint64_t>(units, 4 * 148)));
+  // grid-stride over <= 8 x 148 CTAs: every CTA pays a system-scope poll of
+  // the peers' publish words and a completion atomic, so one unit per thread
+  // (8192 CTAs per chunk) measured 2x slower than this
+  const unsigned grid = static_cast<unsigned>(std::max<std::uint64_t>(1, std::min<std::uint64_t>(units, 8 * 148)));
   pull_reduce_kernel<<<grid, kThr, 0, st>>>(a);
   return cudaGetLastError();
 }
