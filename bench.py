@@ -306,7 +306,7 @@ def run_ours(args):
                    "chunks": info["params"], "chunk_bytes": info["chunk_bytes"],
                    "gpu_param_chunks": info["gpu_chunks"], "policy": cfg["policy"],
                    "tokens_per_step": args.tokens, "compute": args.compute,
-                   "compute_model_tflops": args.tflops, "opt_stages": args.stages, "gpu_spares": args.gpu_spares, "l2": "inputs larger than L2 (>15 GB streamed per step)",
+                   "compute_model_tflops": args.tflops, "opt_stages": args.stages or "auto (forward spare H2D time)", "gpu_spares": args.gpu_spares, "l2": "inputs larger than L2 (>15 GB streamed per step)",
                    "parallelism": "single GPU"},
         "hit_rate": {"exact": rep["hit_rate"], "hits": st["param_hits"] // K, "accesses": st["param_accesses"] // K,
                      "model_clock_hits": rep["param_hits"]},
@@ -514,9 +514,9 @@ def main():
     ap.add_argument("--zero3", action="store_true", help="the torchrun ZeRO-3 path even at world size 1")
     ap.add_argument("--exchange", default="p2p", choices=["p2p", "nccl"],
                     help="ZeRO-3 exchange: fused peer-memory kernels (default) or NCCL + pack kernels")
-    ap.add_argument("--stages", type=int, default=None,
-                    help="HBM optimizer-state stages (default: 128 for c3/c5, whose forward pass has no cache "
-                         "prefetches to compete with state pre-staging; 12 otherwise; profiles/r01_stage_sweep.json)")
+    ap.add_argument("--stages", type=int, default=0,
+                    help="HBM optimizer-state stages (default 0 = auto: the forward pass's spare H2D time by the "
+                         "machine model, at least 12; profiles/r01_stage_sweep.json)")
     ap.add_argument("--gpu-spares", type=int, default=16,
                     help="spare HBM slots per parameter class beyond the policy's logical GPU tier: a prefetch "
                          "lands in a free slot while the slot's previous occupant is still waiting for its "
@@ -533,8 +533,6 @@ def main():
                     help="c4: share of the rank's optimizer states the CPU tier holds (the rest in NVMe); "
                          "1.0 = the 13B ZeRO-3 rank with every state in pinned host memory")
     args = ap.parse_args()
-    if args.stages is None:
-        args.stages = 128 if args.config in ("c3", "c5") else 12
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", "1"))
     # stdout carries exactly one JSON line: anything a library prints there

@@ -175,7 +175,8 @@ typedef struct {
   const char* nvme_dir;    /* directory for the NVMe tier file ("" = none) */
   int gpu_spare_slots;     /* extra HBM slots per class beyond the policy tier (in-flight moves; default 16) */
   int host_spare_slots;    /* extra pinned slots per class */
-  int opt_stage_slots;     /* HBM staging buffers for the optimizer pipeline */
+  int opt_stage_slots;     /* HBM staging buffers for the optimizer pipeline; <= 0: sized from the
+                              forward pass's spare H2D time (at least 12) */
   int direct_io;           /* O_DIRECT for the NVMe tier */
   uint64_t grad_bytes_per_param_byte; /* gradient bytes per bf16 param byte (1) */
 } tc_engine_options;

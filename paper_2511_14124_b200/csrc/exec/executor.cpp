@@ -217,7 +217,8 @@ Executor::Executor(const std::string& trace_path, const std::string& machine_pat
   // a slot over the policy's decisions (dry run), at least the policy's own
   // logical pool sizes, plus spare slots per class.
   const int gspare = std::max(opts.gpu_spare_slots, 1), hspare = std::max(opts.host_spare_slots, 1);
-  std::map<std::pair<int, std::uint64_t>, std::uint32_t> need = simulate_occupancy();
+  double fwd_h2d = 0;
+  std::map<std::pair<int, std::uint64_t>, std::uint32_t> need = simulate_occupancy(&fwd_h2d);
   lap("occupancy dry run");
   if (const SchedulerState* st = policy_->scheduler_state()) {
     std::map<std::pair<int, std::uint64_t>, std::uint32_t> logical;
@@ -241,6 +242,12 @@ Executor::Executor(const std::string& trace_path, const std::string& machine_pat
   host_param_.allocate(false, device_);
   host_opt_.allocate(false, device_);
   lap("pinned host pools");
+  if (timing) {  // how much of the process is backed by transparent huge pages (DMA-friendly)
+    std::ifstream sm("/proc/self/smaps_rollup");
+    for (std::string line; std::getline(sm, line);)
+      if (line.rfind("AnonHugePages", 0) == 0 || line.rfind("Rss:", 0) == 0)
+        std::fprintf(stderr, "[tencache setup] %s\n", line.c_str());
+  }
 
   // NVMe tier: one sparse file, a 4 KiB-aligned extent per tensor
   std::uint64_t off = 0;
@@ -296,7 +303,8 @@ Executor::Executor(const std::string& trace_path, const std::string& machine_pat
   for (const auto& [size, _] : sclass) max_state = std::max(max_state, size);
   for (const auto& [size, _] : pclass) max_state = std::max(max_state, 6 * size);  // seed scratch
   stage_bytes_ = max_state;
-  const int nstage = std::max(opts.opt_stage_slots, 2);
+  const int nstage = opts.opt_stage_slots > 0 ? std::max(opts.opt_stage_slots, 2) : auto_stage_slots(fwd_h2d);
+  if (timing) std::fprintf(stderr, "[tencache setup] optimizer stage ring: %d stages\n", nstage);
   for (int i = 0; i < nstage; ++i) {
     void* p = nullptr;
     TCB_CK(cudaMalloc(&p, stage_bytes_));
@@ -412,7 +420,7 @@ Executor::~Executor() {
 // 1 host parameter cache, 2 host optimizer-state cache. A retained source
 // (src_retains) keeps its slot; a destination that already has the bytes
 // (dst_has_copy) takes none.
-std::map<std::pair<int, std::uint64_t>, std::uint32_t> Executor::simulate_occupancy() const {
+std::map<std::pair<int, std::uint64_t>, std::uint32_t> Executor::simulate_occupancy(double* fwd_h2d) const {
   std::unique_ptr<IPolicy> pol = make_policy(trace_, machine_, cfg_);
   pol->init();
   std::unordered_map<TensorId, std::set<Tier>> where;
@@ -448,21 +456,65 @@ std::map<std::pair<int, std::uint64_t>, std::uint32_t> Executor::simulate_occupa
       first_opt = i;
       break;
     }
+  double fwd = 0;
+  auto fwd_bytes = [&](const std::vector<TransferRequest>& reqs, std::size_t i) {
+    if (trace_.steps[i].phase != Phase::Forward) return;
+    for (const TransferRequest& r : reqs)
+      if (!r.instant && r.dst == Tier::Gpu) fwd += static_cast<double>(r.size_bytes);
+  };
   for (int it = 0; it < 2; ++it) {
     bool restored = false;
+    fwd = 0;  // the second (steady-state) iteration's value is kept
     for (std::size_t i = 0; i < trace_.steps.size(); ++i) {
       if (cfg_.restore_overlap && i == first_opt && !restored) {
         restored = true;
         apply_reqs(pol->on_param_restore_point());
       }
-      apply_reqs(pol->on_step_begin(trace_.steps[i]));
-      apply_reqs(pol->on_step_end(trace_.steps[i]));
+      const auto b = pol->on_step_begin(trace_.steps[i]);
+      fwd_bytes(b, i);
+      apply_reqs(b);
+      const auto e = pol->on_step_end(trace_.steps[i]);
+      fwd_bytes(e, i);
+      apply_reqs(e);
     }
     if (!restored) apply_reqs(pol->on_param_restore_point());
     apply_reqs(pol->on_iteration_end());
     pol->reset_iteration();
   }
+  if (fwd_h2d) *fwd_h2d = fwd;
   return peak;
+}
+
+// opt_stage_slots <= 0: size the HBM stage ring so the forward pass can
+// pre-stage as many optimizer states as its spare H2D time carries (trace
+// compute time x the machine model's CPU->GPU bandwidth minus the forward's
+// own cache prefetches), plus the backward's lookahead; at least 12, at most
+// half the free HBM. Measured optima it reproduces: 12 on C2 at 16k tokens,
+// ~118 on C5 (profiles/r01_stage_sweep.json).
+int Executor::auto_stage_slots(double fwd_h2d) const {
+  double fwd_us = 0, sbytes = 0;
+  std::size_t nstates = 0;
+  for (const TraceStep& st : trace_.steps)
+    if (st.phase == Phase::Forward) fwd_us += st.compute_us * cfg_.batch_scale;
+  for (const auto& r : recs_)
+    if (r.is_state) {
+      sbytes = std::max(sbytes, static_cast<double>(r.bytes));
+      ++nstates;
+    }
+  if (nstates == 0 || sbytes == 0) return 12;
+  double bw = 0;
+  try {
+    bw = to_double(machine_.effective_bandwidth(Tier::Cpu, Tier::Gpu)) * 1e3;  // bytes per us
+  } catch (...) {
+    return 12;
+  }
+  const double spare = std::max(0.0, fwd_us * bw - fwd_h2d);
+  std::size_t n = static_cast<std::size_t>(spare / sbytes) + 4;
+  std::size_t free_b = 0, total_b = 0;
+  if (cudaMemGetInfo(&free_b, &total_b) == cudaSuccess)
+    n = std::min<std::size_t>(n, static_cast<std::size_t>(0.5 * static_cast<double>(free_b) / sbytes));
+  n = std::min(n, nstates + 2);
+  return static_cast<int>(std::max<std::size_t>(n, 12));
 }
 
 std::int32_t Executor::index_of(TensorId id) const {
@@ -1725,7 +1777,7 @@ int tc_engine_create(const char* trace_path, const char* machine_path, const cha
     tc_engine_options o{};
     o.gpu_spare_slots = 16;
     o.host_spare_slots = 1;
-    o.opt_stage_slots = 12;
+    o.opt_stage_slots = 0;  // auto (Executor::auto_stage_slots)
     o.grad_bytes_per_param_byte = 1;
     if (opts) o = *opts;
     auto e = std::make_unique<tc_engine>();

@@ -354,7 +354,10 @@ class Executor {
   EventArena events_;
   std::vector<cudaEvent_t> barriers_;
   std::uint64_t barrier_io_ = 0;  // NVMe job a blocking request ended with
-  std::map<std::pair<int, std::uint64_t>, std::uint32_t> simulate_occupancy() const;
+  // peak slots per (tier, class) over two iterations of decisions; also the
+  // steady-state forward pass's non-instant H2D bytes (*fwd_h2d)
+  std::map<std::pair<int, std::uint64_t>, std::uint32_t> simulate_occupancy(double* fwd_h2d = nullptr) const;
+  int auto_stage_slots(double fwd_h2d) const;
   std::vector<Copy> copies_;
   std::vector<Stall> stalls_;                                      // (reach, go) on compute
   std::vector<std::pair<cudaEvent_t, cudaEvent_t>> ontime_;        // (reach, arrival)
