@@ -427,6 +427,7 @@ def run_reference_arm(args):
     def one_iteration(t):
         restored = False
         cks = 0
+        owed = 0.0  # compute time not yet slept: sleeping per step would add the OS timer slack 158x per step
         for i, s in enumerate(steps):
             if i == first_opt and not restored:
                 restored = True
@@ -435,7 +436,13 @@ def run_reference_arm(args):
             if s["phase"] != "o":
                 for tid in s["ids"]:
                     cks ^= ref.checksum(tiers.buf(tid))
-                time.sleep(s["us"] * 1e-6)  # the layer compute the GPU would do
+                owed += s["us"] * 1e-6  # the layer compute the GPU would do
+                if owed >= 2e-3:  # sleep in >= 2 ms slices, to a deadline (no accumulated oversleep)
+                    t_end = time.perf_counter() + owed
+                    time.sleep(max(0.0, owed - 2e-4))
+                    while time.perf_counter() < t_end:
+                        pass
+                    owed = 0.0
             else:
                 sid, pid = s["ids"]
                 st = tiers.buf(sid).view(np.float32)
@@ -444,6 +451,10 @@ def run_reference_arm(args):
                           want_bf16=False)
                 ref.num().tcnum_cast_f32_to_bf16(ref._p(st[:k]), ref._p(tiers.buf(pid)), k)
             apply(rp.call("E", i))
+        if owed > 0:
+            t_end = time.perf_counter() + owed
+            while time.perf_counter() < t_end:
+                pass
         if not restored:
             apply(rp.call("R"))
         apply(rp.call("I"))
