@@ -560,7 +560,12 @@ def main():
     if args.impl == "reference":
         if rank != 0:
             return
-        emit(run_reference_arm(args))
+        # rank 0 alone runs the reference's CPU path on every host core:
+        # torchrun pins OMP_NUM_THREADS=1 per rank, which would leave it one
+        os.environ["OMP_NUM_THREADS"] = str(len(os.sched_getaffinity(0)))
+        line = run_reference_arm(args)
+        line["n_gpus"] = world
+        emit(line)
         return
     if world > 1 or args.zero3:
         from paper_2511_14124_b200 import zero3
