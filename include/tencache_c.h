@@ -30,7 +30,8 @@ enum {
   TC_EARG = 6,        /* std::invalid_argument / domain_error / bad handle */
   TC_ECUDA = 7,       /* CUDA runtime failure (no reference counterpart) */
   TC_EIO = 8,         /* NVMe tier file I/O failure (no reference counterpart) */
-  TC_ENCCL = 9        /* NCCL failure (no reference counterpart) */
+  TC_ENCCL = 9,       /* NCCL failure (no reference counterpart) */
+  TC_ERANGE = 10      /* output buffer too small: nothing lost, see tc_policy_call */
 };
 
 const char* tc_last_error(void);
@@ -59,7 +60,10 @@ void tc_policy_destroy(tc_policy* p);
 
 /* IPolicy hooks (engine.hpp:63-70): hook 0 on_step_begin(step), 1
  * on_step_end(step), 2 on_param_restore_point, 3 on_iteration_end,
- * 4 reset_iteration. Writes min(n, cap) requests; *n = total. */
+ * 4 reset_iteration. *n = number of requests. If they do not fit (n > cap) the
+ * call returns TC_ERANGE, writes none and keeps them in the handle: the policy
+ * state has advanced, so fetch them with hook 5 (drain, no state change) and a
+ * buffer of at least *n before any other hook. */
 int tc_policy_call(tc_policy* p, int hook, uint32_t step, tc_request* out, size_t cap, size_t* n);
 
 /* Pool views for buffer-assignment parity and the executor (bufpool.hpp:41-95):
@@ -203,7 +207,9 @@ void* tc_engine_grad_ptr(tc_engine* e, uint32_t tensor);
 typedef struct {
   double lr, beta1, beta2, eps, weight_decay;
   float grad_scale;
-  int compute_mode;    /* 0: checksum only, 1: checksum + spin for compute_us*batch_scale */
+  int compute_mode;    /* 0: checksum only, 1: checksum + a 1-CTA spin for compute_us*batch_scale,
+                          2: checksum + bf16 tensor-core GEMMs over the migrated chunk that occupy the
+                             GPU for compute_us*batch_scale (cuBLAS; tc_engine_standin_info) */
   int spin_ctas;
   int flags;           /* bit 0: run optimizer updates in place (no hoisting after the last access);
                           bit 1: no pre-staging of optimizer states ahead of their updates;
@@ -234,9 +240,15 @@ typedef struct {
   uint64_t adam_elems;
   double adam_span_ms;                   /* AdamW resident time: first CTA start to last CTA end */
   uint64_t adam_spans;                   /* launches measured in adam_span_ms */
+  uint64_t adam_launches;                /* fused AdamW kernel launches (one may cover several chunks) */
+  uint64_t compute_gemms;                /* stand-in GEMM launches (compute_mode 2) */
+  double compute_flops;                  /* stand-in GEMM FLOPs issued */
 } tc_engine_stats;
 
 int tc_engine_stats_get(tc_engine* e, tc_engine_stats* out);
+/* compute_mode 2's GEMM shape and calibrated alone-throughput, as JSON (after
+ * the first iteration in that mode; "{}" before). */
+int tc_engine_standin_info(tc_engine* e, char* out, size_t cap);
 int tc_engine_stats_reset(tc_engine* e);
 /* Compute-stream phase durations of the last iteration (ms): forward,
  * backward, optimizer (+ drain of all streams). */

@@ -12,7 +12,7 @@ import os
 _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(_HERE, "_lib", "libtencache_b200.so")
 
-TC_OK, TC_EINTERNAL, TC_ECONFIG, TC_EOOM, TC_ETRACE, TC_EPOOL, TC_EARG, TC_ECUDA, TC_EIO, TC_ENCCL = range(10)
+TC_OK, TC_EINTERNAL, TC_ECONFIG, TC_EOOM, TC_ETRACE, TC_EPOOL, TC_EARG, TC_ECUDA, TC_EIO, TC_ENCCL, TC_ERANGE = range(11)
 
 
 class TencacheError(RuntimeError):
@@ -74,7 +74,8 @@ class tc_engine_stats(C.Structure):
                                           "param_accesses", "param_hits", "ontime_accesses", "requests",
                                           "kernel_launches", "copies")] + \
               [(n, C.c_double) for n in ("h2d_busy_ms", "d2h_busy_ms", "stall_ms", "adam_ms")] + \
-              [("adam_elems", C.c_uint64), ("adam_span_ms", C.c_double), ("adam_spans", C.c_uint64)]
+              [("adam_elems", C.c_uint64), ("adam_span_ms", C.c_double), ("adam_spans", C.c_uint64),
+               ("adam_launches", C.c_uint64), ("compute_gemms", C.c_uint64), ("compute_flops", C.c_double)]
 
     def as_dict(self):
         return {n: getattr(self, n) for n, _ in self._fields_}
@@ -135,6 +136,7 @@ _SIGS = {
     "tc_engine_sync": ([C.c_void_p], C.c_int),
     "tc_engine_stats_get": ([C.c_void_p, C.POINTER(tc_engine_stats)], C.c_int),
     "tc_engine_stats_reset": ([C.c_void_p], C.c_int),
+    "tc_engine_standin_info": ([C.c_void_p, C.c_char_p, C.c_size_t], C.c_int),
     "tc_engine_phase_ms": ([C.c_void_p, C.POINTER(C.c_double), C.c_size_t, C.POINTER(C.c_size_t)], C.c_int),
     "tc_nccl_unique_id": ([C.c_void_p], C.c_int),
     "tc_engine_enable_zero3": ([C.c_void_p, C.c_int, C.c_int, C.c_void_p, C.POINTER(C.c_uint64), C.POINTER(C.c_uint64),

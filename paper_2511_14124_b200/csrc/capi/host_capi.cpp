@@ -68,6 +68,7 @@ struct tc_policy {
   MachineConfig machine;
   RunConfig cfg;
   std::unique_ptr<IPolicy> policy;
+  std::vector<TransferRequest> overflow;  // requests of the last call that did not fit the caller's buffer
 };
 
 namespace {
@@ -167,16 +168,24 @@ int tc_policy_call(tc_policy* p, int hook, uint32_t step, tc_request* out, size_
   TC_GUARD({
     if (p == nullptr) return set_error(TC_EARG, "null policy");
     std::vector<TransferRequest> reqs;
+    if (hook != 5 && !p->overflow.empty())
+      return set_error(TC_ERANGE, "tc_policy_call: the previous call's requests were not drained (hook 5)");
     switch (hook) {
       case 0: reqs = p->policy->on_step_begin(p->trace.steps.at(step)); break;
       case 1: reqs = p->policy->on_step_end(p->trace.steps.at(step)); break;
       case 2: reqs = p->policy->on_param_restore_point(); break;
       case 3: reqs = p->policy->on_iteration_end(); break;
       case 4: p->policy->reset_iteration(); break;
+      case 5: reqs = std::move(p->overflow); p->overflow.clear(); break;  // drain, no state change
       default: return set_error(TC_EARG, "unknown hook " + std::to_string(hook));
     }
-    for (std::size_t k = 0; k < reqs.size() && k < cap; ++k) out[k] = to_c(reqs[k]);
     if (n) *n = reqs.size();
+    if (reqs.size() > cap) {  // the policy state has advanced: keep the requests for a hook-5 drain
+      p->overflow = std::move(reqs);
+      return set_error(TC_ERANGE, "tc_policy_call: " + std::to_string(*n) + " requests, buffer holds " +
+                                      std::to_string(cap) + "; drain them with hook 5");
+    }
+    for (std::size_t k = 0; k < reqs.size(); ++k) out[k] = to_c(reqs[k]);
     return TC_OK;
   })
 }

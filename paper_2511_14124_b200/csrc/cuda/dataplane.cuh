@@ -70,6 +70,8 @@ struct PeerTable {
   const std::uint8_t* pool[kMaxPeers];  // peers' HBM parameter pools (self included)
   const std::uint8_t* gview[kMaxPeers]; // peers' full-layer gradient views
   P2PCtl* ctl[kMaxPeers];               // peers' control blocks
+  unsigned* scratch = nullptr;          // this rank's kMaxPeers + 1 zeroed completion counters
+                                        // (per engine: two engines never share them)
 };
 
 // Owner side: publish chunk c at offset `off` of the pool for access `epoch`.

@@ -233,16 +233,6 @@ __global__ void __launch_bounds__(kThr) pull_reduce_kernel(PullArgs a) {
   }
 }
 
-unsigned* scratch_counters() {  // per-process scratch (zero-initialised once)
-  static unsigned* p = [] {
-    unsigned* q = nullptr;
-    cudaMalloc(&q, sizeof(unsigned) * (kMaxPeers + 1));
-    cudaMemset(q, 0, sizeof(unsigned) * (kMaxPeers + 1));
-    return q;
-  }();
-  return p;
-}
-
 }  // namespace
 
 cudaError_t launch_p2p_publish(P2PCtl* ctl, std::uint32_t chunk, std::uint64_t off, std::uint32_t epoch,
@@ -264,7 +254,8 @@ cudaError_t launch_p2p_gather_unpack(const PeerTable& t, std::uint32_t chunk, st
   a.chunk = chunk;
   a.epoch = epoch;
   a.view = view;
-  a.done = scratch_counters();
+  a.done = t.scratch;
+  if (a.done == nullptr) return cudaErrorInvalidValue;
   a.tiles_before[0] = 0;
   for (int q = 0; q < t.world; ++q) {
     a.bytes[q] = piece_bytes[q];
@@ -287,7 +278,8 @@ cudaError_t launch_p2p_pull_reduce(const PeerTable& t, std::uint32_t gepoch, std
   a.bytes = bytes;
   a.chunk_bytes = chunk_bytes;
   a.grad = grad;
-  a.done = scratch_counters() + kMaxPeers;
+  if (t.scratch == nullptr) return cudaErrorInvalidValue;
+  a.done = t.scratch + kMaxPeers;
   std::uintptr_t al = reinterpret_cast<std::uintptr_t>(grad) | view_off;
   for (int q = 0; q < t.world; ++q) al |= reinterpret_cast<std::uintptr_t>(t.gview[q]);
   a.vec = (al & 15) == 0 ? 1 : 0;

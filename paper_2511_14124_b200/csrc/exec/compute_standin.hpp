@@ -1,0 +1,47 @@
+// The layer compute the migration path does not own, as real tensor-core
+// work: bf16 GEMMs Y[M,N] = X[M,K] * W[K,N] whose weight matrix W is the
+// migrated parameter chunk itself, with M chosen so the GEMMs occupy the GPU
+// for the trace step's compute_us (trace.hpp:38). This loads SMs, tensor
+// cores and HBM the way a layer's forward/backward would, so migration
+// overlap and the in-step AdamW are measured under contention (a nanosleep
+// spin occupies nothing). cuBLAS (a plain library GEMM) is loaded at run
+// time by soname, so the process shares torch's copy when one is loaded.
+#pragma once
+
+#include <cstdint>
+#include <string>
+
+#include <cuda_runtime.h>
+
+namespace tcb {
+
+class GemmStandin {
+ public:
+  GemmStandin(int device, std::uint64_t chunk_bytes, double max_us);
+  ~GemmStandin();
+  GemmStandin(const GemmStandin&) = delete;
+  GemmStandin& operator=(const GemmStandin&) = delete;
+
+  // Enqueue GEMMs reading `weights` (>= chunk_bytes) on `s` for ~us microseconds.
+  // Returns the number of GEMM launches.
+  int run(cudaStream_t s, const void* weights, double us);
+  double flops_issued() const { return flops_; }
+  double calibrated_tflops() const { return tflops_; }
+  int K() const { return K_; }
+  int N() const { return N_; }
+  int max_M() const { return max_m_; }
+  std::string describe() const;
+
+ private:
+  void gemm(cudaStream_t s, const void* w, int M);
+  int device_ = 0;
+  void* handle_ = nullptr;  // cublasHandle_t
+  void* x_ = nullptr;       // X [max_M x K] bf16
+  void* y_ = nullptr;       // Y [max_M x N] bf16
+  void* ws_ = nullptr;      // cuBLAS workspace
+  int K_ = 0, N_ = 0, max_m_ = 0;
+  double tflops_ = 0;       // measured alone at construction
+  double flops_ = 0;
+};
+
+}  // namespace tcb

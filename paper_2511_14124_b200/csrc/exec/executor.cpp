@@ -409,6 +409,7 @@ Executor::~Executor() {
       if (cp.segs) cudaFree(cp.segs);
     for (void* p : z3_->opened) cudaIpcCloseMemHandle(p);
     if (z3_->ctl) cudaFree(z3_->ctl);
+    if (z3_->peers.scratch) cudaFree(z3_->peers.scratch);
     for (std::uint8_t* p : {z3_->gather, z3_->view, z3_->gview, z3_->gpad})
       if (p) cudaFree(p);
     if (z3_->comm) nccl().CommDestroy(z3_->comm);
@@ -847,796 +848,6 @@ void Executor::wait_barriers(cudaStream_t cs) {
   barrier_io_ = 0;
 }
 
-void Executor::param_step(const TraceStep& step, std::size_t, cudaStream_t cs) {
-  cudaEvent_t reach = events_.get(true), go = events_.get(true);
-  TCB_CK(cudaEventRecord(reach, cs));
-  for (TensorId id : step.tensor_ids) {
-    TensorRec& x = rec(id);
-    if (x.tier != PTier::Gpu) throw DeviceError(TC_EINTERNAL, "step tensor " + std::to_string(id) + " not GPU-resident");
-    wait_for_read(cs, slot_of(x).sync);
-  }
-  wait_barriers(cs);
-  TCB_CK(cudaEventRecord(go, cs));
-  stalls_.push_back(Stall{reach, go, step.tensor_ids.front()});
-  for (TensorId id : step.tensor_ids) {
-    TensorRec& x = rec(id);
-    ++stats_.param_accesses;
-    if (x.issued_since_access == 0)
-      ++stats_.param_hits;
-    else if (x.arrival)
-      ontime_.emplace_back(reach, x.arrival);
-    x.issued_since_access = 0;
-    if (z3_) {
-      zero3_access(x, step.phase == Phase::Backward, cs);
-    } else if (access_cursor_ < n_accesses_) {
-      TCB_CK(launch_checksum(where(x), x.bytes & ~3ull,
-                             reinterpret_cast<unsigned long long*>(cks_base_ + access_cursor_), cs));
-      ++stats_.kernel_launches;
-      ++access_cursor_;
-    }
-  }
-  if (so_.compute_mode == 1) {
-    const double us = step.compute_us * cfg_.batch_scale;
-    TCB_CK(launch_spin(static_cast<std::uint64_t>(us * 1000.0), so_.spin_ctas, cs));
-    ++stats_.kernel_launches;
-  }
-  cudaEvent_t done = events_.get(false);
-  TCB_CK(cudaEventRecord(done, cs));
-  for (TensorId id : step.tensor_ids) slot_of(rec(id)).sync.readers.push_back(done);
-}
-
-// One optimizer update, data side: state chunk H2D into an HBM stage, fused
-// AdamW on the optimizer stream (bf16 result straight into the parameter's
-// HBM slot when resident, else a scratch buffer), updated state D2H back to
-// its pinned slot, and the parameter write-back when it lives off-GPU.
-// Issue the H2D of a host-resident optimizer state into a free HBM stage.
-std::size_t Executor::stage_state(TensorRec& s) {
-  if (s.tier != PTier::HostOpt) throw DeviceError(TC_EINTERNAL, "optimizer state not in host memory when staged");
-  if (stage_free_.empty()) throw DeviceError(TC_EINTERNAL, "no free optimizer stage");
-  const std::size_t b = stage_free_.front();
-  stage_free_.pop_front();
-  Slot& h = slot_of(s);
-  tag_ = CopyTag{"opt_load", s.id, 1, 0};
-  if (opt_yield_ && last_h2d_) TCB_CK(cudaStreamWaitEvent(h2d_opt_, last_h2d_, 0));
-  wait_for_write(h2d_opt_, stage_sync_[b]);
-  wait_for_read(h2d_opt_, h.sync);
-  cudaEvent_t e1 = copy(h2d_opt_, stage_[b], h.ptr, s.bytes, true);
-  h.sync.readers.push_back(e1);
-  stage_sync_[b] = SlotSync{e1, {}};
-  staged_[index_of(s.id)] = b;
-  return b;
-}
-
-// Keep up to `want_staged` states staged ahead of their updates, in update order.
-void Executor::refill_stages(std::size_t want_staged) {
-  while (prestage_next_ < prestage_order_.size() && staged_.size() < want_staged && stage_free_.size() > 1) {
-    TensorRec& s = recs_[static_cast<std::size_t>(prestage_order_[prestage_next_++])];
-    if (!staged_.count(index_of(s.id)) && s.tier == PTier::HostOpt) stage_state(s);
-  }
-}
-
-void Executor::optimizer_work(TensorRec& s, TensorRec& p) {
-  cudaStream_t ost = adam_stream();
-  const bool state_on_gpu = s.tier == PTier::Gpu;  // no-offload posture: update in place in HBM
-  if (!state_on_gpu && s.tier != PTier::HostOpt)
-    throw DeviceError(TC_EINTERNAL, "optimizer state not in host memory at its update");
-  const std::uint64_t n = p.bytes / 2;
-  std::uint8_t* stg;
-  std::size_t b = 0;
-  if (state_on_gpu) {
-    Slot& gs = slot_of(s);
-    stg = gs.ptr;
-    wait_for_write(ost, gs.sync);
-  } else {
-    auto it = staged_.find(index_of(s.id));
-    b = it != staged_.end() ? it->second : stage_state(s);
-    staged_.erase(index_of(s.id));
-    stats_.opt_h2d_bytes += s.bytes;  // counted at the update it feeds (staging may be a prologue)
-    stg = stage_[b];
-    // (null once a drain between the prologue's staging and this update completed it)
-    if (stage_sync_[b].writer) TCB_CK(cudaStreamWaitEvent(ost, stage_sync_[b].writer, 0));
-  }
-  if (p.grad_ready) TCB_CK(cudaStreamWaitEvent(ost, p.grad_ready, 0));
-  std::uint8_t* pout;
-  SlotSync* psync;
-  const bool on_gpu = p.tier == PTier::Gpu;
-  if (on_gpu) {
-    Slot& g = slot_of(p);
-    pout = g.ptr;
-    psync = &g.sync;
-  } else {
-    std::size_t& k = pout_next_[p.bytes];
-    pout = pout_scratch_[p.bytes][k];
-    psync = &pout_sync_[p.bytes][k];
-    k = (k + 1) % pout_scratch_[p.bytes].size();
-  }
-  wait_for_write(ost, *psync);
-  cudaEvent_t a0 = events_.get(true), a1 = events_.get(true);
-  TCB_CK(cudaEventRecord(a0, ost));
-  auto* st = reinterpret_cast<float*>(stg);
-  const AdamScalars sc = adam_scalars(so_.lr, so_.beta1, so_.beta2, so_.eps, so_.weight_decay, adam_step_);
-  unsigned long long *smin = nullptr, *smax = nullptr;
-  const std::size_t cap = std::max<std::size_t>(recs_.size(), 1);
-  if (span_cursor_ < cap && adamw_variant() >= 2) {  // in-kernel resident span (TMA variants)
-    smin = span_base_ + span_cursor_;
-    smax = span_base_ + cap + span_cursor_;
-    ++span_cursor_;
-  }
-  if (adam_stamps_ && smin) TCB_CK(launch_stamp(smin + 2 * cap, ost));
-  TCB_CK(launch_adamw(st, st + n, st + 2 * n, reinterpret_cast<const std::uint16_t*>(p.grad),
-                      reinterpret_cast<std::uint16_t*>(pout), n, sc, so_.grad_scale, ost, smin, smax));
-  if (adam_stamps_ && smin) TCB_CK(launch_stamp(smin + 3 * cap, ost));
-  TCB_CK(cudaEventRecord(a1, ost));
-  adam_.emplace_back(a0, a1);
-  ++stats_.kernel_launches;
-  stats_.adam_elems += n;
-  *psync = SlotSync{a1, {}};
-  p.nvme_valid = false;  // any NVMe replica of the parameter is now stale
-  if (p.has_home) p.home_valid = false;
-  if (on_gpu) p.arrival = nullptr;
-
-  if (state_on_gpu) {
-    slot_of(s).sync = SlotSync{a1, {}};
-  } else {
-    Slot& h = slot_of(s);
-    stage_sync_[b].readers.push_back(a1);
-    wait_for_read(d2h_opt_, stage_sync_[b]);
-    wait_for_write(d2h_opt_, h.sync);
-    TCB_CK(cudaStreamWaitEvent(d2h_opt_, a1, 0));
-    if (opt_yield_ && last_d2h_) TCB_CK(cudaStreamWaitEvent(d2h_opt_, last_d2h_, 0));
-    tag_ = CopyTag{"opt_store", s.id, 0, 1};
-    cudaEvent_t e3 = copy(d2h_opt_, h.ptr, stg, s.bytes, false);
-    h.sync = SlotSync{e3, {}};
-    stage_sync_[b].readers.push_back(e3);
-    stage_free_.push_back(b);
-    stats_.opt_d2h_bytes += s.bytes;
-  }
-
-  if (!on_gpu) {  // updated-parameter write-back to its home tier (category iii)
-    tag_ = CopyTag{"writeback", p.id, 0, static_cast<std::uint8_t>(p.tier == PTier::Nvme ? 2 : 1)};
-    if (p.tier == PTier::Nvme) {
-      std::uint8_t* bb = bounce_.at(p.bytes);
-      SlotSync& bs = bounce_sync_[p.bytes];
-      if (io_) {
-        wait_for_write(d2h_opt_, bs);
-        TCB_CK(cudaStreamWaitEvent(d2h_opt_, a1, 0));
-        cudaEvent_t e4 = copy(d2h_opt_, bb, pout, p.bytes, false);
-        psync->readers.push_back(e4);
-        bs = SlotSync{e4, {}};
-        nvme_write_async(p, bb, bs);
-      } else {
-        TCB_CK(cudaEventSynchronize(a1));
-        host_wait_all(bs);
-        TCB_CK(cudaMemcpy(bb, pout, p.bytes, cudaMemcpyDeviceToHost));
-        bs = SlotSync{};
-        nvme_write(p, bb);
-      }
-    } else {
-      Slot& ph = slot_of(p);
-      wait_for_write(d2h_opt_, ph.sync);
-      TCB_CK(cudaStreamWaitEvent(d2h_opt_, a1, 0));
-      cudaEvent_t e4 = copy(d2h_opt_, ph.ptr, pout, p.bytes, false);
-      ph.sync = SlotSync{e4, {}};
-      psync->readers.push_back(e4);
-    }
-    stats_.writeback_bytes += p.bytes;
-  }
-}
-
-// The whole iteration's decisions, made up front in the reference's call
-// order (engine.cpp:363-431). Legal because the request stream is a pure
-// function of (trace, capacities, policy) and independent of timing
-// (engine.hpp:49-51); it lets the executor see every future
-// move when it schedules the data work.
-std::vector<Executor::Hook> Executor::decide_iteration() {
-  std::vector<Hook> hooks;
-  std::size_t first_opt = trace_.steps.size();
-  for (std::size_t i = 0; i < trace_.steps.size(); ++i)
-    if (trace_.steps[i].phase == Phase::OptimizerUpdate) {
-      first_opt = i;
-      break;
-    }
-  bool restored = false;
-  for (std::size_t i = 0; i < trace_.steps.size(); ++i) {
-    if (cfg_.restore_overlap && i == first_opt && !restored) {
-      restored = true;
-      hooks.push_back({2, i, policy_->on_param_restore_point()});
-    }
-    hooks.push_back({0, i, policy_->on_step_begin(trace_.steps[i])});
-    hooks.push_back({1, i, policy_->on_step_end(trace_.steps[i])});
-  }
-  if (!restored) hooks.push_back({2, trace_.steps.size(), policy_->on_param_restore_point()});
-  hooks.push_back({3, trace_.steps.size(), policy_->on_iteration_end()});
-  policy_->reset_iteration();
-  return hooks;
-}
-
-// For each step, the optimizer steps whose data work runs right after that
-// step's compute (before its end-hook moves): the parameter's last forward /
-// backward access has happened, its gradient is final, and no decision
-// touches the state until the update's own step. hoist_at[i] lists opt step
-// indexes to run after step i; an opt step not listed runs in place.
-std::vector<std::size_t> Executor::plan_hoisting(const std::vector<Hook>& hooks) {
-  const std::size_t n = trace_.steps.size();
-  std::vector<std::size_t> at(n, n);  // opt step -> host step (n = in place)
-  if (!so_.hoist_optimizer) return at;
-  std::unordered_map<TensorId, std::size_t> last_access;
-  for (std::size_t i = 0; i < n; ++i)
-    if (trace_.steps[i].phase != Phase::OptimizerUpdate)
-      for (TensorId id : trace_.steps[i].tensor_ids) last_access[id] = i;
-  // position of each begin hook, and the hooks touching each tensor
-  std::vector<std::size_t> begin_pos(n, 0), end_pos(n, 0);
-  std::unordered_map<TensorId, std::vector<std::size_t>> touched;
-  for (std::size_t k = 0; k < hooks.size(); ++k) {
-    if (hooks[k].kind == 0) begin_pos[hooks[k].step] = k;
-    if (hooks[k].kind == 1) end_pos[hooks[k].step] = k;
-    for (const Req& r : hooks[k].reqs) touched[r.tensor_id].push_back(k);
-  }
-  // the state's residency at iteration start = the policy's placement
-  for (std::size_t j = 0; j < n; ++j) {
-    const TraceStep& os = trace_.steps[j];
-    if (os.phase != Phase::OptimizerUpdate) continue;
-    const TensorId sid = os.tensor_ids.front();
-    const TensorRec& s = rec(sid);
-    if (!s.is_state || s.partner < 0) continue;
-    const TensorId pid = recs_[static_cast<std::size_t>(s.partner)].id;
-    auto la = last_access.find(pid);
-    if (la == last_access.end()) continue;
-    const std::size_t a = la->second;
-    const Tier home = policy_->initial_tier(sid).value_or(Tier::Nvme);
-    if (home != Tier::Cpu && home != Tier::Gpu) continue;
-    bool moved = false;  // any decision moving the state before its update's end
-    auto t = touched.find(sid);
-    if (t != touched.end())
-      for (std::size_t k : t->second) moved = moved || k <= end_pos[j];
-    if (moved) continue;
-    at[j] = a;
-  }
-  return at;
-}
-
-// How many optimizer states fit through the H2D link during the forward
-// pass on top of the forward's own parameter prefetches, by the machine's
-// bandwidth model (machine.cpp:101-111) and the trace's compute time.
-std::size_t Executor::forward_prestage_budget(const std::vector<Hook>& hooks) const {
-  double fwd_us = 0, fwd_h2d = 0;
-  for (const Hook& h : hooks) {
-    if ((h.kind == 0 || h.kind == 1) && trace_.steps[h.step].phase == Phase::Forward) {
-      if (h.kind == 0) fwd_us += trace_.steps[h.step].compute_us * cfg_.batch_scale;
-      for (const Req& r : h.reqs)
-        if (!r.instant && r.dst == Tier::Gpu) fwd_h2d += static_cast<double>(r.size_bytes);
-    }
-  }
-  double bw;
-  try {
-    bw = to_double(machine_.effective_bandwidth(Tier::Cpu, Tier::Gpu)) * 1e3;  // bytes per us
-  } catch (...) {
-    return 0;
-  }
-  const double spare = fwd_us * bw - fwd_h2d;
-  if (spare <= 0 || prestage_order_.empty()) return std::min<std::size_t>(1, prestage_order_.size());
-  const double sbytes = static_cast<double>(recs_[static_cast<std::size_t>(prestage_order_.front())].bytes);
-  return std::max<std::size_t>(1, static_cast<std::size_t>(spare / sbytes));
-}
-
-void Executor::iteration(const StepOptions& so, cudaStream_t compute) {
-  TCB_CK(cudaSetDevice(device_));
-  if (compute == nullptr) {
-    if (!compute_owned_) TCB_CK(cudaStreamCreateWithFlags(&compute_owned_, cudaStreamNonBlocking));
-    compute = compute_owned_;
-  }
-  compute_ = compute;
-  so_ = so;
-  ++adam_step_;
-  access_cursor_ = 0;
-  if (!ahead_) events_.next_generation();  // else the prologue already opened this generation
-  cks_base_ = d_checksums_ + (events_.generation() % 2) * std::max<std::size_t>(n_accesses_, 1);
-  {  // per-launch AdamW spans: mins start at UINT64_MAX (0xff bytes), maxes at 0
-    const std::size_t cap = std::max<std::size_t>(recs_.size(), 1);
-    span_base_ = d_span_ + (events_.generation() % 2) * 4 * cap;  // [min | max | pre stamp | post stamp]
-    span_cursor_ = 0;
-    TCB_CK(launch_fill_u64(span_base_, ~0ull, cap, adam_stream()));  // same stream as the updates
-    TCB_CK(launch_fill_u64(span_base_ + cap, 0ull, cap, adam_stream()));
-  }
-  TCB_CK(launch_fill_u64(reinterpret_cast<unsigned long long*>(cks_base_), 0ull, std::max<std::size_t>(n_accesses_, 1),
-                         compute));
-  std::vector<Hook> hooks;
-  if (ahead_) {  // decided (and its first states staged) at the end of the previous iteration
-    hooks = std::move(*ahead_);
-    ahead_.reset();
-  } else {
-    nvtxRangePushA("tencache.decide");
-    hooks = decide_iteration();
-    nvtxRangePop();
-    drop_staged();
-  }
-  const std::vector<std::size_t> hoist = plan_hoisting(hooks);
-  const std::size_t n = trace_.steps.size();
-  std::vector<std::vector<std::size_t>> after(n);
-  for (std::size_t j = 0; j < n; ++j)
-    if (hoist[j] < n) after[hoist[j]].push_back(j);
-  // Hoisted updates in execution order; their states can be staged any time
-  // (no decision touches them before their update, plan_hoisting). States
-  // staged by the prologue are skipped by refill_stages.
-  set_prestage_order(hooks, hoist);
-  // states the prologue staged come first in the order: continue after them
-  while (prestage_next_ < prestage_order_.size() && staged_.count(prestage_order_[prestage_next_])) ++prestage_next_;
-  if (so_.prestage) {
-    // The forward refill of iteration t+1 is issued while iteration t's tail
-    // may still be moving; gated, it starts only after t's last cache
-    // prefetch so it never competes with t's critical H2D traffic.
-    if (prestage_gate_ && last_h2d_) TCB_CK(cudaStreamWaitEvent(h2d_opt_, last_h2d_, 0));
-    refill_stages(prestage_fwd_override_ >= 0 ? static_cast<std::size_t>(prestage_fwd_override_)
-                                              : forward_prestage_budget(hooks));
-  }
-  auto mark = [&] {
-    cudaEvent_t e = events_.get(true);
-    TCB_CK(cudaEventRecord(e, compute));
-    phase_marks_.push_back(e);
-  };
-  mark();
-  Phase prev = Phase::Forward;
-  for (const Hook& h : hooks) {
-    if (h.kind == 0) {
-      const TraceStep& step = trace_.steps[h.step];
-      if (step.phase != prev) {
-        mark();
-        if (prev == Phase::Forward && so_.prestage && edge_fill_) {
-          // Forward -> backward edge: the forward's cache prefetches are all
-          // issued and no backward prefetch exists yet, so the H2D link
-          // would idle until the first update frees a stage. Fill the rest
-          // of the ring, starting when the forward's last prefetch lands.
-          if (last_h2d_) TCB_CK(cudaStreamWaitEvent(h2d_opt_, last_h2d_, 0));
-          refill_stages(stage_.size());
-        }
-        prev = step.phase;
-      }
-      nvtxRangePushA(step.phase == Phase::Forward ? "tencache.fwd" : step.phase == Phase::Backward ? "tencache.bwd"
-                                                                                                   : "tencache.opt");
-      execute(h.reqs);
-      if (step.phase == Phase::OptimizerUpdate) {
-        if (hoist[h.step] == n) {  // in place: waits for the state's decisions
-          TensorRec& s = rec(step.tensor_ids.front());
-          if (s.partner < 0) throw DeviceError(TC_EINTERNAL, "optimizer step without a paired state");
-          wait_barriers(adam_stream());
-          optimizer_work(s, recs_[static_cast<std::size_t>(s.partner)]);
-        }
-      } else {
-        param_step(step, h.step, compute);
-        for (std::size_t j : after[h.step]) {
-          TensorRec& s = rec(trace_.steps[j].tensor_ids.front());
-          optimizer_work(s, recs_[static_cast<std::size_t>(s.partner)]);
-          if (so_.prestage) refill_stages(prestage_lookahead_);
-        }
-      }
-      nvtxRangePop();
-    } else {
-      execute(h.reqs);
-    }
-  }
-  mark();
-  finish_iteration();
-  if (lookahead_ && so_.prestage && so_.prologue) prologue_next();
-}
-
-// Hoisted updates of an iteration in execution order = the order their
-// states are staged.
-void Executor::set_prestage_order(const std::vector<Hook>& hooks, const std::vector<std::size_t>& hoist) {
-  const std::size_t n = trace_.steps.size();
-  std::vector<std::vector<std::size_t>> after(n);
-  for (std::size_t j = 0; j < n; ++j)
-    if (hoist[j] < n) after[hoist[j]].push_back(j);
-  prestage_order_.clear();
-  prestage_next_ = 0;
-  for (std::size_t i = 0; i < n; ++i)
-    for (std::size_t j : after[i]) prestage_order_.push_back(index_of(trace_.steps[j].tensor_ids.front()));
-}
-
-// Release stages holding pre-staged states (their bytes may be stale: the
-// caller wrote or re-seeded tensors); the decisions made ahead stay valid.
-void Executor::drop_staged() {
-  for (auto& [idx, b] : staged_) stage_free_.push_back(b);
-  staged_.clear();
-}
-
-// Prologue of iteration t+1, run at the end of iteration t's enqueue: its
-// decisions are made now (the request stream is timing-independent,
-// engine.hpp:49-51) and its first optimizer states are staged right behind
-// t's last state loads, so the H2D link works through t's write-back tail
-// whether or not the caller waits for t's result before calling iteration()
-// again (tc_engine_step_result waits for t's compute stream).
-void Executor::prologue_next() {
-  events_.next_generation();
-  nvtxRangePushA("tencache.decide");
-  std::vector<Hook> hooks = decide_iteration();
-  nvtxRangePop();
-  set_prestage_order(hooks, plan_hoisting(hooks));
-  if (prestage_gate_ && last_h2d_) TCB_CK(cudaStreamWaitEvent(h2d_opt_, last_h2d_, 0));
-  refill_stages(prestage_fwd_override_ >= 0 ? static_cast<std::size_t>(prestage_fwd_override_)
-                                            : forward_prestage_budget(hooks));
-  ahead_ = std::move(hooks);
-}
-
-// The iteration is enqueued; nothing waits for it here. Its timing records
-// and a fence per stream are parked; the previous iteration is harvested
-// (fences awaited, timings summed, its events recycled) so that iteration
-// t+1's forward pass overlaps iteration t's optimizer write-back tail.
-void Executor::finish_iteration() {
-  {  // the step's result (per-access checksums) to pinned host memory, on the
-     // compute stream: step_result() waits for this, not for the optimizer tail
-    const std::size_t k = static_cast<std::size_t>(events_.generation() % 2), na = std::max<std::size_t>(n_accesses_, 1);
-    // a kernel storing into mapped pinned memory: a cudaMemcpyAsync here would
-    // queue on the D2H copy engine behind the iteration's bulk state stores
-    // and hold the next iteration's compute stream until they drain
-    TCB_CK(launch_copy_u64(reinterpret_cast<unsigned long long*>(d_result_) + k * na,
-                           reinterpret_cast<const unsigned long long*>(cks_base_), n_accesses_, compute_));
-    TCB_CK(cudaEventRecord(result_ev_[k], compute_));
-    result_gen_ = events_.generation();
-    have_result_ = true;
-  }
-  {  // this iteration's AdamW spans/stamps to mapped host memory, behind its last update
-    const std::size_t cap = std::max<std::size_t>(recs_.size(), 1);
-    TCB_CK(launch_copy_u64(reinterpret_cast<unsigned long long*>(d_span_host_) + (events_.generation() % 2) * 4 * cap,
-                           span_base_, 4 * cap, adam_stream()));
-  }
-  IterRecord rec;
-  rec.gen = events_.generation();
-  rec.copies = std::move(copies_);
-  rec.stalls = std::move(stalls_);
-  rec.ontime = std::move(ontime_);
-  rec.adam = std::move(adam_);
-  rec.marks = std::move(phase_marks_);
-  for (cudaStream_t x : {h2d_, d2h_, opt_, h2d_opt_, d2h_opt_, compute_}) {
-    cudaEvent_t e = events_.get(true);
-    TCB_CK(cudaEventRecord(e, x));
-    rec.fences.push_back(e);
-  }
-  rec.cks_buf = static_cast<std::size_t>(events_.generation() % 2);
-  rec.io_seq = io_ ? io_->submitted() : 0;
-  rec.spans = span_cursor_;
-  copies_.clear();
-  stalls_.clear();
-  ontime_.clear();
-  adam_.clear();
-  phase_marks_.clear();
-  if (!staged_.empty()) {  // defensive: a staged state whose update did not run
-    for (auto& [idx, b] : staged_) stage_free_.push_back(b);
-    staged_.clear();
-  }
-  pending_.push_back(std::move(rec));
-  while (pending_.size() > 1) harvest_front();
-}
-
-void Executor::harvest_front() {
-  IterRecord rec = std::move(pending_.front());
-  pending_.pop_front();
-  {  // fences, with a diagnostic if an iteration does not drain
-    static const char* const kStreams[] = {"h2d", "d2h", "opt", "h2d_opt", "d2h_opt", "compute"};
-    const auto t0 = std::chrono::steady_clock::now();
-    for (bool reported = false;;) {
-      bool all = true;
-      std::string pending;
-      for (std::size_t i = 0; i < rec.fences.size(); ++i) {
-        const cudaError_t q = cudaEventQuery(rec.fences[i]);
-        if (q == cudaErrorNotReady) {
-          all = false;
-          pending += std::string(" ") + (i < 6 ? kStreams[i] : "?");
-        } else if (q != cudaSuccess) {
-          TCB_CK(q);
-        }
-      }
-      if (all) break;
-      if (!reported && std::chrono::steady_clock::now() - t0 > std::chrono::seconds(30)) {
-        reported = true;
-        std::fprintf(stderr, "[executor] iteration %llu not drained after 30 s; streams pending:%s; %s\n",
-                     static_cast<unsigned long long>(rec.gen), pending.c_str(),
-                     io_ ? io_->describe().c_str() : "no nvme queue");
-      }
-      std::this_thread::sleep_for(std::chrono::microseconds(50));
-    }
-  }
-  if (io_) io_->wait_upto(rec.io_seq);  // no queued job may still name an event we recycle
-  float ms = 0;
-  phase_ms_.clear();
-  for (std::size_t i = 0; i + 1 < rec.marks.size(); ++i) {
-    TCB_CK(cudaEventElapsedTime(&ms, rec.marks[i], rec.marks[i + 1]));
-    phase_ms_.push_back(ms);
-  }
-  if (!rec.marks.empty()) {  // whole iteration: start mark -> last fence
-    float end = 0;
-    for (cudaEvent_t f : rec.fences) {
-      TCB_CK(cudaEventElapsedTime(&ms, rec.marks.front(), f));
-      end = std::max(end, ms);
-    }
-    phase_ms_.push_back(end);
-  }
-  for (const Copy& c : rec.copies) {
-    TCB_CK(cudaEventElapsedTime(&ms, c.start, c.end));
-    (c.h2d ? stats_.h2d_busy_ms : stats_.d2h_busy_ms) += ms;
-  }
-  for (const Stall& st : rec.stalls) {
-    TCB_CK(cudaEventElapsedTime(&ms, st.reach, st.go));
-    stats_.stall_ms += ms;
-  }
-  if (event_log_ && !rec.marks.empty()) {  // measured timeline in the reference's event-log schema
-    static const char* const kTiers[] = {"gpu", "cpu", "nvme"};
-    float t0 = 0, t1 = 0;
-    for (std::size_t k = 0; k < rec.marks.size(); ++k) {  // phase boundaries of this iteration
-      TCB_CK(cudaEventElapsedTime(&t0, rec.marks.front(), rec.marks[k]));
-      *event_log_ << "{\"iter\":" << rec.gen << ",\"kind\":\"mark\",\"k\":" << k << ",\"us\":" << t0 * 1e3 << "}\n";
-    }
-    if (!pending_.empty() && !pending_.front().marks.empty()) {  // where the next iteration starts
-      TCB_CK(cudaEventSynchronize(pending_.front().marks.front()));
-      TCB_CK(cudaEventElapsedTime(&t0, rec.marks.front(), pending_.front().marks.front()));
-      *event_log_ << "{\"iter\":" << rec.gen << ",\"kind\":\"next_iter\",\"us\":" << t0 * 1e3 << "}\n";
-    }
-    for (const Copy& c : rec.copies) {
-      TCB_CK(cudaEventElapsedTime(&t0, rec.marks.front(), c.start));
-      TCB_CK(cudaEventElapsedTime(&t1, rec.marks.front(), c.end));
-      *event_log_ << "{\"bytes\":" << c.bytes << ",\"dst\":\"" << kTiers[c.tag.dst] << "\",\"end_us\":" << t1 * 1e3
-                  << ",\"iter\":" << rec.gen << ",\"kind\":\"" << c.tag.kind << "\",\"src\":\"" << kTiers[c.tag.src]
-                  << "\",\"tensor\":" << c.tag.tensor << ",\"us\":" << t0 * 1e3 << "}\n";
-    }
-    for (const Stall& st : rec.stalls) {
-      TCB_CK(cudaEventElapsedTime(&ms, st.reach, st.go));
-      if (ms <= 0.0005f) continue;
-      TCB_CK(cudaEventElapsedTime(&t0, rec.marks.front(), st.reach));
-      *event_log_ << "{\"dst\":\"gpu\",\"iter\":" << rec.gen << ",\"kind\":\"stall\",\"src\":\"gpu\",\"tensor\":"
-                  << st.tensor << ",\"us\":" << t0 * 1e3 << ",\"wait_us\":" << ms * 1e3 << "}\n";
-    }
-    event_log_->flush();
-  }
-  for (const auto& [reach, arrival] : rec.ontime) {
-    TCB_CK(cudaEventElapsedTime(&ms, reach, arrival));
-    if (ms <= 0.0f) ++stats_.ontime_accesses;
-  }
-  for (const auto& [a0, a1] : rec.adam) {
-    TCB_CK(cudaEventElapsedTime(&ms, a0, a1));
-    stats_.adam_ms += ms;
-  }
-  // from the mapped copies written by kernels at the iteration's end: a
-  // synchronous cudaMemcpy here would enter the legacy stream (often the
-  // caller's compute stream) and queue on the D2H copy engine behind the
-  // next iteration's bulk state stores, stalling that stream until they drain
-  std::memcpy(h_checksums_.data(), h_result_ + rec.cks_buf * std::max<std::size_t>(n_accesses_, 1),
-              n_accesses_ * sizeof(std::uint64_t));
-  if (rec.spans) {
-    const std::size_t cap = std::max<std::size_t>(recs_.size(), 1);
-    const unsigned long long* sp = h_span_ + rec.cks_buf * 4 * cap;
-    for (std::size_t k = 0; k < rec.spans; ++k)
-      if (sp[cap + k] > sp[k]) {
-        stats_.adam_span_ms += static_cast<double>(sp[cap + k] - sp[k]) * 1e-6;
-        ++stats_.adam_spans;
-        if (adam_stamps_ && sp[2 * cap + k] && sp[3 * cap + k] >= sp[cap + k]) {
-          stamp_pre_ns_ += static_cast<double>(sp[k]) - static_cast<double>(sp[2 * cap + k]);
-          stamp_post_ns_ += static_cast<double>(sp[3 * cap + k] - sp[cap + k]);
-          ++stamps_;
-        }
-      }
-  }
-  scrub(rec.gen);
-  events_.recycle_upto(rec.gen);
-}
-
-// Drop every reference to events of generations <= gen (all complete).
-void Executor::scrub(std::uint64_t gen) {
-  const std::uint64_t io_done = io_ ? io_->done() : 0;
-  auto clean = [&](SlotSync& y) {
-    if (y.writer && events_.done_by(y.writer, gen)) y.writer = nullptr;
-    std::erase_if(y.readers, [&](cudaEvent_t e) { return events_.done_by(e, gen); });
-    if (y.io_read <= io_done) y.io_read = 0;
-    if (y.io_write <= io_done) y.io_write = 0;
-  };
-  for (SlotPool* p : {&gpu_, &host_param_, &host_opt_})
-    for (auto& [size, c] : p->classes())
-      for (Slot& s : c.slots) clean(s.sync);
-  for (auto& [k, v] : bounce_sync_) clean(v);
-  for (auto& v : stage_sync_) clean(v);
-  for (auto& [k, v] : pout_sync_)
-    for (auto& y : v) clean(y);
-  for (auto& r : recs_) {
-    if (r.arrival && events_.done_by(r.arrival, gen)) r.arrival = nullptr;
-    if (r.grad_ready && events_.done_by(r.grad_ready, gen)) r.grad_ready = nullptr;
-  }
-  std::erase_if(barriers_, [&](cudaEvent_t e) { return events_.done_by(e, gen); });
-  if (last_h2d_ && events_.done_by(last_h2d_, gen)) last_h2d_ = nullptr;
-  if (last_d2h_ && events_.done_by(last_d2h_, gen)) last_d2h_ = nullptr;
-}
-
-void Executor::drain() {
-  while (!pending_.empty()) harvest_front();
-  if (io_) io_->wait_all();
-  TCB_CK(cudaDeviceSynchronize());
-  scrub(events_.generation());
-  events_.recycle_all();
-}
-
-// ZeRO-3: attach a NCCL communicator and precompute, per parameter chunk, the
-// fragment list between the rank-major gathered buffer [r0 S | r1 S | ...] and
-// the flat layer view (same list reversed packs the full-layer gradient for
-// the reduce-scatter).
-void Executor::enable_zero3(int world, int rank, const ncclUniqueId& id, const std::uint64_t* layer_elems,
-                            const std::uint64_t* layer_per, std::uint32_t n_layers) {
-  TCB_CK(cudaSetDevice(device_));
-  auto z = std::make_unique<Zero3>();
-  z->world = world;
-  z->rank = rank;
-  z->layer_elems.assign(layer_elems, layer_elems + n_layers);
-  z->layer_per.assign(layer_per, layer_per + n_layers);
-  std::map<std::uint32_t, std::vector<std::int32_t>> by_layer;
-  std::uint64_t S = 0;
-  for (const auto& t : trace_.tensors)
-    if (t.kind == TensorKind::ParamFP16) {
-      if (S != 0 && t.size_bytes != S) throw ConfigError("ZeRO-3 exchange needs uniform parameter chunks");
-      S = t.size_bytes;
-      if (t.layer >= n_layers) throw ConfigError("ZeRO-3 layer table shorter than the trace's layers");
-      by_layer[t.layer].push_back(index_of(t.id));
-    }
-  z->S = S;
-  std::uint64_t max_layer = 0;
-  for (std::uint32_t l = 0; l < n_layers; ++l) max_layer = std::max(max_layer, 2 * layer_elems[l]);
-  for (auto& [layer, idxs] : by_layer) {
-    std::sort(idxs.begin(), idxs.end(), [&](std::int32_t a, std::int32_t b) { return recs_[a].id < recs_[b].id; });
-    const std::uint64_t E = layer_elems[layer], per = layer_per[layer];
-    if (per * static_cast<std::uint64_t>(world) < E) throw ConfigError("ZeRO-3: per * world < layer elements");
-    for (std::size_t c = 0; c < idxs.size(); ++c) {
-      Zero3::ChunkPlan cp;
-      cp.layer = layer;
-      cp.rank_bytes.assign(world, 0);
-      cp.rank_view_off.assign(world, 0);
-      std::vector<PackSeg> segs;
-      std::uint64_t v = 0;
-      for (int r = 0; r < world; ++r) {
-        const std::uint64_t lo = std::min<std::uint64_t>(static_cast<std::uint64_t>(r) * per, E);
-        const std::uint64_t shard = 2 * (std::min<std::uint64_t>(lo + per, E) - lo);
-        const std::uint64_t start = c * S;
-        if (shard <= start) continue;
-        const std::uint64_t nb = std::min<std::uint64_t>(S, shard - start);
-        segs.push_back(PackSeg{static_cast<std::uint64_t>(r) * S, 2 * lo + start, nb, v});
-        cp.pieces.emplace_back(2 * lo + start, nb);
-        cp.rank_bytes[r] = nb;
-        cp.rank_view_off[r] = 2 * lo + start;
-        cp.vec = cp.vec && ((2 * lo + start) % 16 == 0) && nb % 16 == 0;
-        v += nb;
-      }
-      cp.nseg = static_cast<std::uint32_t>(segs.size());
-      cp.total = v;
-      if (!segs.empty()) {
-        TCB_CK(cudaMalloc(&cp.segs, sizeof(PackSeg) * segs.size()));
-        TCB_CK(cudaMemcpy(cp.segs, segs.data(), sizeof(PackSeg) * segs.size(), cudaMemcpyHostToDevice));
-      }
-      z->plans[idxs[c]] = std::move(cp);
-    }
-  }
-  {
-    std::vector<std::int32_t> order;
-    for (auto& [idx, cp] : z->plans) order.push_back(idx);
-    std::sort(order.begin(), order.end(), [&](std::int32_t a, std::int32_t b) { return recs_[a].id < recs_[b].id; });
-    for (std::size_t k = 0; k < order.size(); ++k) z->plans[order[k]].chunk = static_cast<std::uint32_t>(k);
-    if (order.size() > static_cast<std::size_t>(P2PCtl::kMaxChunks))
-      throw ConfigError("ZeRO-3: more chunks than the p2p control block holds");
-    z->access_epoch.assign(order.size(), 0);
-  }
-  TCB_CK(cudaMalloc(&z->gather, world * S));
-  TCB_CK(cudaMalloc(&z->view, std::max<std::uint64_t>(max_layer, 16)));
-  TCB_CK(cudaMalloc(&z->gview, std::max<std::uint64_t>(max_layer, 16)));
-  TCB_CK(cudaMalloc(&z->gpad, world * S));
-  TCB_CK(cudaMemset(z->gpad, 0, world * S));
-  bool id_zero = true;  // an all-zero id: p2p-only exchange, no NCCL communicator
-  for (char ch : id.internal) id_zero = id_zero && ch == 0;
-  if (!id_zero) nccl_check(nccl().CommInitRank(&z->comm, world, id, rank), "ncclCommInitRank");
-  z3_ = std::move(z);
-}
-
-// One parameter access under ZeRO-3, on the compute stream: all-gather the
-// chunk from every rank, unpack into the flat layer view, checksum the view's
-// pieces (the layer compute reads exactly those). Backward also produces the
-// full-layer gradient of those pieces (stand-in: seeded per rank), packs it
-// rank-major and reduce-scatters it (sum) into this rank's gradient chunk.
-void Executor::zero3_access(TensorRec& x, bool backward, cudaStream_t cs) {
-  Zero3& z = *z3_;
-  const Zero3::ChunkPlan& cp = z.plans.at(index_of(x.id));
-  const unsigned peers_n = static_cast<unsigned>(z.world - 1);
-  if (z.p2p) {  // fused all-gather + unpack straight from the peers' HBM slots
-    const std::uint32_t a = ++z.access_epoch[cp.chunk];
-    Slot& sl = slot_of(x);
-    TCB_CK(launch_p2p_publish(z.ctl, cp.chunk, static_cast<std::uint64_t>(sl.ptr - gpu_.base()), a, cs));
-    TCB_CK(launch_p2p_gather_unpack(z.peers, cp.chunk, a, cp.rank_bytes.data(), cp.rank_view_off.data(), z.view, cs));
-    stats_.kernel_launches += 2;
-    // peers read the slot from now on: its next writer waits for all of them
-    sl.sync.peer_cnt = &z.ctl->cnt[cp.chunk];
-    sl.sync.peer_target = a * peers_n;
-  } else {
-    nccl_check(nccl().AllGather(where(x), z.gather, z.S, ncclUint8, z.comm, cs), "ncclAllGather");
-    TCB_CK(launch_pack(cp.segs, cp.nseg, cp.total, z.gather, z.view, false, cp.vec, cs));
-    stats_.kernel_launches += 1;
-  }
-  z.gathered_bytes += z.S * static_cast<std::uint64_t>(z.world);
-  if (access_cursor_ < n_accesses_) {
-    for (const auto& [off, nb] : cp.pieces) {
-      TCB_CK(launch_checksum(z.view + off, nb & ~3ull, reinterpret_cast<unsigned long long*>(cks_base_ + access_cursor_),
-                             cs));
-      ++stats_.kernel_launches;
-    }
-    ++access_cursor_;
-  }
-  if (!backward) return;
-  if (z.p2p) {  // my gradient view is refilled only after every peer pulled the previous one
-    const std::uint32_t g = ++z.grad_epoch;
-    if (peers_n && g > 1) stream_wait_value32(cs, &z.ctl->gcnt, (g - 1) * peers_n);
-  }
-  for (const auto& [off, nb] : cp.pieces) {
-    TCB_CK(launch_fill_normal_bf16(reinterpret_cast<std::uint16_t*>(z.gview + off), nb / 2, 1e-3f,
-                                   static_cast<std::uint64_t>(adam_step_) * 1000003ull + static_cast<std::uint64_t>(z.rank),
-                                   (static_cast<std::uint64_t>(cp.layer) << 40) + off / 2, cs));
-    ++stats_.kernel_launches;
-  }
-  if (z.p2p) {  // fused pack + reduce-scatter: pull my piece from every rank's view and sum
-    TCB_CK(launch_p2p_publish_grad(z.ctl, z.grad_epoch, cs));
-    TCB_CK(launch_p2p_pull_reduce(z.peers, z.grad_epoch, cp.rank_view_off[z.rank], cp.rank_bytes[z.rank], z.S,
-                                  reinterpret_cast<std::uint16_t*>(x.grad), cs));
-    stats_.kernel_launches += 2;
-  } else {
-    if (cp.total < z.S * static_cast<std::uint64_t>(z.world))  // padded chunk: padding gradient is zero
-      TCB_CK(cudaMemsetAsync(z.gpad, 0, z.S * static_cast<std::uint64_t>(z.world), cs));
-    TCB_CK(launch_pack(cp.segs, cp.nseg, cp.total, z.gview, z.gpad, true, cp.vec, cs));
-    ++stats_.kernel_launches;
-    nccl_check(nccl().ReduceScatter(z.gpad, x.grad, z.S / 2, ncclBfloat16, ncclSum, z.comm, cs),
-               "ncclReduceScatter");
-  }
-  z.reduced_bytes += z.S * static_cast<std::uint64_t>(z.world);
-  cudaEvent_t e = events_.get(false);
-  TCB_CK(cudaEventRecord(e, cs));
-  x.grad_ready = e;
-}
-
-// This rank's IPC handles: HBM parameter pool, control block, gradient view.
-std::vector<std::uint8_t> Executor::p2p_handles() {
-  if (!z3_) throw ConfigError("p2p exchange needs tc_engine_enable_zero3 first");
-  Zero3& z = *z3_;
-  if (!z.ctl) {
-    TCB_CK(cudaMalloc(&z.ctl, sizeof(P2PCtl)));
-    TCB_CK(cudaMemset(z.ctl, 0, sizeof(P2PCtl)));
-  }
-  std::vector<std::uint8_t> blob(3 * sizeof(cudaIpcMemHandle_t));
-  cudaIpcMemHandle_t h[3];
-  TCB_CK(cudaIpcGetMemHandle(&h[0], gpu_.base()));
-  TCB_CK(cudaIpcGetMemHandle(&h[1], z.ctl));
-  TCB_CK(cudaIpcGetMemHandle(&h[2], z.gview));
-  std::memcpy(blob.data(), h, sizeof(h));
-  return blob;
-}
-
-// Map every peer's pool, control block and gradient view (self: local
-// pointers) and switch the exchange to the fused p2p kernels.
-void Executor::enable_p2p(const std::uint8_t* all_blobs) {
-  if (!z3_) throw ConfigError("p2p exchange needs tc_engine_enable_zero3 first");
-  Zero3& z = *z3_;
-  if (z.world > kMaxPeers) throw ConfigError("p2p exchange supports up to 8 ranks");
-  if (!z.ctl) p2p_handles();
-  z.peers.world = z.world;
-  z.peers.rank = z.rank;
-  for (int q = 0; q < z.world; ++q) {
-    if (q == z.rank) {
-      z.peers.pool[q] = gpu_.base();
-      z.peers.ctl[q] = z.ctl;
-      z.peers.gview[q] = z.gview;
-      continue;
-    }
-    cudaIpcMemHandle_t h[3];
-    std::memcpy(h, all_blobs + static_cast<std::size_t>(q) * sizeof(h), sizeof(h));
-    void* ptr[3];
-    for (int k = 0; k < 3; ++k) {
-      TCB_CK(cudaIpcOpenMemHandle(&ptr[k], h[k], cudaIpcMemLazyEnablePeerAccess));
-      z.opened.push_back(ptr[k]);
-    }
-    z.peers.pool[q] = static_cast<const std::uint8_t*>(ptr[0]);
-    z.peers.ctl[q] = static_cast<P2PCtl*>(ptr[1]);
-    z.peers.gview[q] = static_cast<const std::uint8_t*>(ptr[2]);
-  }
-  z.p2p = true;
-}
-
 void Executor::set_event_log(const std::string& path) {
   drain();
   if (path.empty()) {
@@ -1662,6 +873,7 @@ std::vector<std::uint64_t> Executor::step_result() {
   if (!have_result_) throw DeviceError(TC_EARG, "no iteration has been run");
   const std::size_t k = static_cast<std::size_t>(result_gen_ % 2);
   TCB_CK(cudaEventSynchronize(result_ev_[k]));
+  if (io_) io_->check();  // the result may have consumed bytes of a failed NVMe job
   const std::uint64_t* r = h_result_ + k * std::max<std::size_t>(n_accesses_, 1);
   return std::vector<std::uint64_t>(r, r + n_accesses_);
 }
@@ -1760,210 +972,3 @@ void* Executor::gpu_ptr(TensorId id) {
 void* Executor::grad_ptr(TensorId id) { return rec(id).grad; }
 
 }  // namespace tcb
-
-// ------------------------------------------------------------------ C-ABI
-struct tc_engine {
-  std::unique_ptr<tcb::Executor> ex;
-};
-
-using namespace tcb;
-
-extern "C" {
-
-int tc_engine_create(const char* trace_path, const char* machine_path, const char* cfg_json,
-                     const tc_engine_options* opts, tc_engine** out) {
-  TC_GUARD({
-    if (out == nullptr || trace_path == nullptr) return set_error(TC_EARG, "tc_engine_create: null argument");
-    tc_engine_options o{};
-    o.gpu_spare_slots = 16;
-    o.host_spare_slots = 1;
-    o.opt_stage_slots = 0;  // auto (Executor::auto_stage_slots)
-    o.grad_bytes_per_param_byte = 1;
-    if (opts) o = *opts;
-    auto e = std::make_unique<tc_engine>();
-    e->ex = std::make_unique<Executor>(trace_path, machine_path ? machine_path : "", cfg_json ? cfg_json : "", o);
-    *out = e.release();
-    return TC_OK;
-  })
-}
-
-void tc_engine_destroy(tc_engine* e) { delete e; }
-
-int tc_engine_seed(tc_engine* e, uint64_t seed) {
-  TC_GUARD({
-    e->ex->seed(seed);
-    return TC_OK;
-  })
-}
-
-int tc_engine_read_tensor(tc_engine* e, uint32_t tensor, void* host_dst, uint64_t bytes) {
-  TC_GUARD({
-    e->ex->read_tensor(tensor, host_dst, bytes);
-    return TC_OK;
-  })
-}
-
-int tc_engine_write_tensor(tc_engine* e, uint32_t tensor, const void* host_src, uint64_t bytes) {
-  TC_GUARD({
-    e->ex->write_tensor(tensor, host_src, bytes);
-    return TC_OK;
-  })
-}
-
-int tc_engine_read_grad(tc_engine* e, uint32_t tensor, void* host_dst, uint64_t bytes) {
-  TC_GUARD({
-    void* g = e->ex->grad_ptr(tensor);
-    if (g == nullptr) return set_error(TC_EARG, "tensor has no gradient");
-    e->ex->sync();
-    TCB_CK(cudaMemcpy(host_dst, g, bytes, cudaMemcpyDeviceToHost));
-    return TC_OK;
-  })
-}
-
-void* tc_engine_gpu_ptr(tc_engine* e, uint32_t tensor) {
-  try {
-    return e->ex->gpu_ptr(tensor);
-  } catch (...) {
-    return nullptr;
-  }
-}
-
-void* tc_engine_grad_ptr(tc_engine* e, uint32_t tensor) {
-  try {
-    return e->ex->grad_ptr(tensor);
-  } catch (...) {
-    return nullptr;
-  }
-}
-
-int tc_engine_iteration(tc_engine* e, const tc_step_options* so, void* compute_stream) {
-  TC_GUARD({
-    StepOptions o;
-    if (so) {
-      o.lr = so->lr;
-      o.beta1 = so->beta1;
-      o.beta2 = so->beta2;
-      o.eps = so->eps;
-      o.weight_decay = so->weight_decay;
-      o.grad_scale = so->grad_scale;
-      o.compute_mode = so->compute_mode;
-      o.spin_ctas = so->spin_ctas;
-      o.hoist_optimizer = (so->flags & 1) == 0;
-      o.prestage = (so->flags & 2) == 0;
-      o.prologue = (so->flags & 4) == 0;
-    }
-    e->ex->iteration(o, static_cast<cudaStream_t>(compute_stream));
-    return TC_OK;
-  })
-}
-
-int tc_engine_sync(tc_engine* e) {
-  TC_GUARD({
-    e->ex->sync();
-    return TC_OK;
-  })
-}
-
-int tc_nccl_unique_id(uint8_t out[128]) {
-  TC_GUARD({
-    ncclUniqueId id;
-    nccl_check(nccl().GetUniqueId(&id), "ncclGetUniqueId");
-    std::memcpy(out, id.internal, sizeof(id.internal));
-    return TC_OK;
-  })
-}
-
-int tc_engine_enable_zero3(tc_engine* e, int world, int rank, const uint8_t id[128], const uint64_t* layer_elems,
-                           const uint64_t* layer_per, uint32_t n_layers) {
-  TC_GUARD({
-    if (!e || world < 1 || rank < 0 || rank >= world) return set_error(TC_EARG, "tc_engine_enable_zero3: bad arguments");
-    ncclUniqueId nid;
-    std::memcpy(nid.internal, id, sizeof(nid.internal));
-    e->ex->enable_zero3(world, rank, nid, layer_elems, layer_per, n_layers);
-    return TC_OK;
-  })
-}
-
-uint64_t tc_engine_exchanged_bytes(tc_engine* e) { return e ? e->ex->exchanged_bytes() : 0; }
-
-int tc_engine_p2p_handles(tc_engine* e, uint8_t* out, size_t cap, size_t* n) {
-  TC_GUARD({
-    if (!e) return set_error(TC_EARG, "null engine");
-    const std::vector<std::uint8_t> b = e->ex->p2p_handles();
-    if (n) *n = b.size();
-    if (out && cap >= b.size()) std::memcpy(out, b.data(), b.size());
-    return TC_OK;
-  })
-}
-
-int tc_engine_enable_p2p(tc_engine* e, const uint8_t* all_blobs) {
-  TC_GUARD({
-    if (!e || !all_blobs) return set_error(TC_EARG, "null argument");
-    e->ex->enable_p2p(all_blobs);
-    return TC_OK;
-  })
-}
-
-int tc_engine_event_log(tc_engine* e, const char* path) {
-  TC_GUARD({
-    if (!e) return set_error(TC_EARG, "null engine");
-    e->ex->set_event_log(path ? path : "");
-    return TC_OK;
-  })
-}
-
-int tc_engine_stats_get(tc_engine* e, tc_engine_stats* out) {
-  TC_GUARD({
-    if (!e || !out) return set_error(TC_EARG, "null argument");
-    e->ex->sync();
-    *out = e->ex->stats();
-    return TC_OK;
-  })
-}
-
-int tc_engine_phase_ms(tc_engine* e, double* out, size_t cap, size_t* n) {
-  if (!e) return set_error(TC_EARG, "null argument");
-  try {
-    e->ex->sync();
-  } catch (const std::exception& ex) {
-    return set_error(TC_ECUDA, ex.what());
-  }
-  const auto& v = e->ex->phase_ms();
-  for (std::size_t i = 0; i < v.size() && i < cap; ++i) out[i] = v[i];
-  if (n) *n = v.size();
-  return TC_OK;
-}
-
-int tc_engine_stats_reset(tc_engine* e) {
-  TC_GUARD({
-    if (!e) return set_error(TC_EARG, "null argument");
-    e->ex->sync();
-    e->ex->reset_stats();
-    return TC_OK;
-  })
-}
-
-int tc_engine_step_result(tc_engine* e, uint64_t* out, size_t cap, size_t* n) {
-  TC_GUARD({
-    if (!e) return set_error(TC_EARG, "null argument");
-    if (out == nullptr || cap == 0) {  // size query: no wait
-      if (n) *n = e->ex->n_accesses();
-      return TC_OK;
-    }
-    const auto v = e->ex->step_result();
-    for (std::size_t i = 0; i < v.size() && i < cap; ++i) out[i] = v[i];
-    if (n) *n = v.size();
-    return TC_OK;
-  })
-}
-
-int tc_engine_access_checksums(tc_engine* e, uint64_t* out, size_t cap, size_t* n) {
-  TC_GUARD({
-    const auto& v = e->ex->access_checksums();
-    for (std::size_t i = 0; i < v.size() && i < cap; ++i) out[i] = v[i];
-    if (n) *n = v.size();
-    return TC_OK;
-  })
-}
-
-}  // extern "C"

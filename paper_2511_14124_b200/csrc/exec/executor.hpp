@@ -34,6 +34,7 @@
 #include <cuda_runtime.h>
 
 #include "capi_common.hpp"
+#include "compute_standin.hpp"
 #include "dataplane.cuh"
 #include "nccl_dyn.hpp"
 #include "nvme_io.hpp"
@@ -191,6 +192,7 @@ class Executor {
   void write_tensor(tencache::TensorId id, const void* src, std::uint64_t bytes);
   void* gpu_ptr(tencache::TensorId id);
   void* grad_ptr(tencache::TensorId id);
+  std::uint64_t tensor_bytes(tencache::TensorId id) { return rec(id).bytes; }
   void enable_zero3(int world, int rank, const ncclUniqueId& id, const std::uint64_t* layer_elems,
                     const std::uint64_t* layer_per, std::uint32_t n_layers);
   std::uint64_t exchanged_bytes() const { return z3_ ? z3_->gathered_bytes + z3_->reduced_bytes : 0; }
@@ -368,6 +370,10 @@ class Executor {
   void set_event_log(const std::string& path);
  private:
   std::unique_ptr<Zero3> z3_;
+  std::unique_ptr<GemmStandin> standin_;  // compute_mode 2 (created on first use)
+ public:
+  std::string standin_info() const { return standin_ ? standin_->describe() : "{}"; }
+ private:
   std::vector<double> phase_ms_;
   StepOptions so_;
   tc_engine_stats stats_{};

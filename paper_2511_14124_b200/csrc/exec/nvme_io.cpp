@@ -273,7 +273,15 @@ void NvmeQueue::dispatch() {
     }
     Job j = std::move(*it);
     q_.erase(it);
-    if (st < 0) error_ = "event wait failed before NVMe I/O";
+    if (st < 0) {  // never touch a buffer whose producer failed; complete the job so no stream hangs,
+                   // the error surfaces at the engine's next host-side check (check())
+      error_ = "event wait failed before NVMe I/O (job " + std::to_string(j.seq) + ")";
+      remaining_[j.seq] = 1;
+      g.unlock();
+      piece_done(j.seq, true);
+      g.lock();
+      continue;
+    }
     (j.write ? wait_w_ : wait_r_) += now_s() - j.t_submit;
     ++(j.write ? jobs_w_ : jobs_r_);
     const std::uint64_t n = std::max<std::uint64_t>(1, (j.bytes + kPiece - 1) / kPiece);
@@ -297,7 +305,10 @@ void NvmeQueue::work() {
       p = pieces_.front();
       pieces_.pop_front();
     }
-    piece_done(p.seq, file_->io(p.write, p.buf, p.bytes, p.off));
+    // fault injection for tests: TC_NVME_FAIL_JOB=k fails job k's I/O
+    const char* fe = std::getenv("TC_NVME_FAIL_JOB");
+    const std::uint64_t fail_job = fe ? std::strtoull(fe, nullptr, 10) : 0ull;
+    piece_done(p.seq, p.seq != fail_job && file_->io(p.write, p.buf, p.bytes, p.off));
   }
 }
 
@@ -305,9 +316,14 @@ void NvmeQueue::work() {
 // and the watermark advances over every contiguous complete job. Both are
 // stored under the lock (a watermark must never regress: a GPU stream waiting
 // for a value above a regressed word hangs).
+void NvmeQueue::check() const {
+  std::lock_guard<std::mutex> g(mu_);
+  if (!error_.empty()) throw DeviceError(TC_EIO, error_);
+}
+
 void NvmeQueue::piece_done(std::uint64_t seq, bool ok) {
   std::lock_guard<std::mutex> g(mu_);
-  if (!ok) error_ = "NVMe tier I/O failed";
+  if (!ok && error_.empty()) error_ = "NVMe tier I/O failed (job " + std::to_string(seq) + ")";
   if (--remaining_[seq] != 0) return;
   remaining_.erase(seq);
   completed_.insert(seq);

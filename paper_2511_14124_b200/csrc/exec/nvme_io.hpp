@@ -65,6 +65,10 @@ class NvmeQueue {
   void wait_upto(std::uint64_t seq);                         // host-side wait for every job <= seq
   void wait_all() { wait_upto(submitted()); }
   std::uint64_t done() const;  // watermark: every job <= done() is complete
+  // Throws DeviceError(TC_EIO) once any job failed. A failed job is still
+  // published complete (a GPU stream waiting on it must not hang), so every
+  // result that may have consumed its bytes is checked through this.
+  void check() const;
   std::uint64_t submitted() const;
   std::uint64_t bytes_read() const { return bytes_read_; }
   std::string describe();  // state dump for hang diagnostics

@@ -77,6 +77,13 @@ class Engine:
         N.check(N.lib().tc_engine_phase_ms(self._h, out, 8, C.byref(n)))
         return list(out[: n.value])
 
+    def standin_info(self):
+        """compute_mode 2's GEMM shape and calibrated throughput (dict; {} before first use)."""
+        import json
+        buf = C.create_string_buffer(1024)
+        N.check(N.lib().tc_engine_standin_info(self._h, buf, 1024))
+        return json.loads(buf.value.decode())
+
     def event_log(self, path):
         """Measured per-copy timeline (JSONL, reference event-log schema + timings); None/'' = off."""
         N.check(N.lib().tc_engine_event_log(self._h, N.b(path or "")))

@@ -22,7 +22,7 @@ from . import _native as N
 TIERS = ("gpu", "cpu", "nvme")
 KINDS = ("prefetch", "evict", "restore")
 F_STAGING, F_INSTANT, F_SRC_RETAINS, F_DST_HAS_COPY, F_BLOCKING = 1, 2, 4, 8, 16
-HOOK_BEGIN, HOOK_END, HOOK_RESTORE, HOOK_ITER_END, HOOK_RESET = range(5)
+HOOK_BEGIN, HOOK_END, HOOK_RESTORE, HOOK_ITER_END, HOOK_RESET, HOOK_DRAIN = range(6)
 
 
 @dataclass(frozen=True)
@@ -72,10 +72,11 @@ class Policy:
 
     def _call(self, hook, step=0):
         n = C.c_size_t()
-        N.check(N.lib().tc_policy_call(self._h, hook, step, self._buf, len(self._buf), C.byref(n)))
-        if n.value > len(self._buf):
+        rc = N.lib().tc_policy_call(self._h, hook, step, self._buf, len(self._buf), C.byref(n))
+        if rc == N.TC_ERANGE:  # the hook ran; its requests wait in the handle (hook 5 drains them)
             self._buf = (N.tc_request * (2 * n.value))()
-            raise RuntimeError("request buffer too small; state already advanced")
+            rc = N.lib().tc_policy_call(self._h, HOOK_DRAIN, 0, self._buf, len(self._buf), C.byref(n))
+        N.check(rc)
         return [TransferRequest(r.tensor_id, r.src, r.dst, r.size_bytes, r.kind, r.flags)
                 for r in self._buf[: n.value]]
 

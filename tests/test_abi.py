@@ -46,3 +46,34 @@ def test_data_plane_fails_loudly_without_gpu():
     seg = (N.tc_segment * 1)(N.tc_segment(0, 0, 16))
     plan = C.c_void_p()
     assert L.tc_pack_plan_create(seg, 1, C.byref(plan)) == N.TC_ECUDA
+
+
+def test_policy_call_overflow_is_not_lost(tmpd):
+    """A request buffer that is too small: TC_ERANGE, nothing written, the
+    requests wait in the handle (the hook already advanced the policy) and
+    hook 5 drains them; any other hook is refused until then."""
+    import cases
+    from paper_2511_14124_b200 import policy as P
+    tr, m = cases.fig8(tmpd)
+    L = N.lib()
+    h = C.c_void_p()
+    info = (C.c_uint64 * 4)()
+    assert L.tc_policy_create(tr.encode(), m.encode(), b"{}", C.byref(h), info) == N.TC_OK
+    calls = P.decisions(tr, m, {}, with_pools=False)["calls"]  # [iteration, step, hook, requests]
+    k = next(i for i, c in enumerate(calls) if c[3])
+    buf = (N.tc_request * 64)()
+    n = C.c_size_t()
+    code = {"B": 0, "E": 1, "R": 2, "I": 3, "Z": 4}
+    for _, step, hook, reqs in calls[:k]:
+        assert L.tc_policy_call(h, code[hook], step, buf, 64, C.byref(n)) == N.TC_OK
+    _, step, hook, reqs = calls[k]
+    assert L.tc_policy_call(h, code[hook], step, buf, 0, C.byref(n)) == N.TC_ERANGE
+    assert n.value == len(reqs)
+    assert L.tc_policy_call(h, 0, step + 1, buf, 64, C.byref(n)) == N.TC_ERANGE  # not drained yet
+    assert L.tc_policy_call(h, 5, 0, buf, 64, C.byref(n)) == N.TC_OK
+    got = [[r.tensor_id, r.src, r.dst, r.size_bytes, r.kind, r.flags] for r in buf[: n.value]]
+    assert got == [list(q) for q in reqs]
+    # the sequence continues where it stopped
+    _, step, hook, reqs = calls[k + 1]
+    assert L.tc_policy_call(h, code[hook], step, buf, 64, C.byref(n)) == N.TC_OK and n.value == len(reqs)
+    L.tc_policy_destroy(h)

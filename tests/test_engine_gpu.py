@@ -18,7 +18,6 @@ import numpy as np
 import pytest
 
 import cases
-from paper_2511_14124_b200 import policy as P
 from paper_2511_14124_b200 import traces as T
 from paper_2511_14124_b200.engine import Engine
 
@@ -91,7 +90,7 @@ def test_fig8_shape(tmpd, pol, ro, hoist):
     tr, m = write_with_states(tmpd, "f8", [4096] * 6, 3 * 4096, 3 * 4096 + 6 * 6 * 4096)
     cfg = {"policy": pol, "restore_overlap": ro}
     st = check_engine(tr, m, cfg, hoist=hoist)
-    rep = P.run(tr, m, cfg)
+    rep = ref.run(tr, m, cfg)
     assert st["param_accesses"] == rep["param_accesses"] and st["param_hits"] == rep["param_hits"]
 
 
@@ -105,7 +104,7 @@ def test_nvme_tiers(tmpd, pol, io, monkeypatch):
     tr, m = write_with_states(tmpd, "f9", [4096] * 7, 3 * 4096, 3 * 4096 + 2 * 6 * 4096, iters=3)
     cfg = {"policy": pol}
     st = check_engine(tr, m, cfg, iters=3, nvme_dir=tmpd)
-    rep = P.run(tr, m, cfg)
+    rep = ref.run(tr, m, cfg)
     assert st["param_hits"] == rep["param_hits"]
     assert st["nvme_read_bytes"] > 0 and st["nvme_write_bytes"] > 0
 
@@ -136,7 +135,7 @@ def test_random_traces(tmpd, seed):
         cpu = int(total * rng.uniform(0.3, 1.0)) + int(6 * total * rng.uniform(0.0, 1.2))
         m = cases.write_machine(os.path.join(tmpd, "m.json"), gpu, cpu)
         try:
-            rep = P.run(tr, m, cfg)
+            rep = ref.run(tr, m, cfg)
             break
         except Exception:
             continue
@@ -160,7 +159,7 @@ def test_comparison_policies_on_the_executor(tmpd, pol, k):
     tr, m = write_with_states(tmpd, "b", sizes, gpu, 10 ** 6, iters=2)
     cfg = {"policy": pol, "zero_lookahead_k": k}
     st = check_engine(tr, m, cfg, iters=2, nvme_dir=tmpd)
-    rep = P.run(tr, m, cfg)
+    rep = ref.run(tr, m, cfg)
     assert st["param_accesses"] == rep["param_accesses"] and st["param_hits"] == rep["param_hits"]
 
 
@@ -172,7 +171,7 @@ def test_chunk_trace_c2_mini(tmpd):
     g = int(0.4 * n)
     mp = T.write_machine(os.path.join(tmpd, "m.json"), g * S, (n - g) * S + n * 6 * S)
     st = check_engine(tp, mp, {"policy": "tencache"}, iters=3)
-    rep = P.run(tp, mp, {"policy": "tencache"})
+    rep = ref.run(tp, mp, {"policy": "tencache"})
     assert st["param_hits"] == rep["param_hits"]
     assert st["h2d_bytes"] > 0 and st["d2h_bytes"] > 0
     # every state crosses PCIe exactly once each way per iteration (the next
@@ -256,7 +255,7 @@ def test_captured_model_trace_runs_on_engine(tmpd):
     n, S = ct.n_chunks, ct.chunk_bytes
     mp = T.write_machine(os.path.join(tmpd, "m.json"), max(2, n // 2) * S, n * 7 * S)
     st = check_engine(tp, mp, {"policy": "tencache"}, iters=2)
-    rep = P.run(tp, mp, {"policy": "tencache"})
+    rep = ref.run(tp, mp, {"policy": "tencache"})
     assert st["param_hits"] == rep["param_hits"]
 
 
@@ -277,7 +276,7 @@ def test_measured_event_log(tmpd):
         if "end_us" in x:  # next iteration's states may legitimately start earlier (pipelining)
             assert x["end_us"] >= x["us"]
     # the decision copies of one iteration are exactly the model clock's non-instant requests
-    _, ev = P.run(tr, m, {"policy": "tencache"}, events=True)
+    _, ev = ref.run(tr, m, {"policy": "tencache"}, events=True)
     model = [json.loads(x) for x in ev if json.loads(x)["kind"] in ("prefetch", "evict", "restore")]
     real = [x for x in lines if x["kind"] in ("prefetch", "evict", "restore")]
     assert sorted((x["tensor"], x["src"], x["dst"]) for x in real) == \
@@ -297,7 +296,7 @@ def test_tied_weight_reuse_and_duplicate_access(tmpd):
     m = cases.write_machine(os.path.join(tmpd, "tied_m.json"), 2 * 4096, 10 ** 6)
     for pol in ("tencache", "tencache+opt"):
         stt = check_engine(tr, m, {"policy": pol}, iters=3)
-        rep = P.run(tr, m, {"policy": pol})
+        rep = ref.run(tr, m, {"policy": pol})
         assert stt["param_hits"] == rep["param_hits"]
 
 
@@ -344,7 +343,7 @@ def test_many_iterations_pipelined(tmpd):
     m = cases.write_machine(os.path.join(tmpd, "long_m.json"), int(0.6 * total), int(0.5 * total) + 3 * total)
     for pol in ("tencache", "tencache+opt"):
         st = check_engine(tr, m, {"policy": pol}, iters=8, nvme_dir=tmpd, stages=3)
-        assert st["param_hits"] == P.run(tr, m, {"policy": pol})["param_hits"]
+        assert st["param_hits"] == ref.run(tr, m, {"policy": pol})["param_hits"]
 
 
 def test_back_to_back_iterations_with_prologue(tmpd):
@@ -425,6 +424,39 @@ def test_full_size_c2_bit_exact(tmpd):
         assert np.array_equal(e.read_tensor(n + i, 6 * S).view(np.uint32), states[n + i].view(np.uint32)), \
             f"state {n + i}"
     st = e.stats()
-    assert st["param_hits"] == P.run(info["trace"], info["machine"], {"policy": "tencache"})["param_hits"]
+    assert st["param_hits"] == ref.run(info["trace"], info["machine"], {"policy": "tencache"})["param_hits"]
     assert st["opt_h2d_bytes"] == 2 * n * 6 * S and st["opt_d2h_bytes"] == 2 * n * 6 * S
+    e.close()
+
+
+def test_read_grad_checks_size(tmpd):
+    """tc_engine_read_grad refuses a size other than the parameter's (the
+    gradients are carved back to back: a larger read would return a
+    neighbour's gradient)."""
+    from paper_2511_14124_b200 import _native as N
+    tr, m = write_with_states(tmpd, "g", [4096] * 4, 2 * 4096, 2 * 4096 + 4 * 6 * 4096)
+    e = Engine(tr, m, {"policy": "tencache"})
+    e.seed(1)
+    assert e.read_grad(1, 4096).size == 2048
+    with pytest.raises(N.TencacheError) as ei:
+        e.read_grad(1, 8192)
+    assert ei.value.code == N.TC_EARG
+    e.close()
+
+
+def test_nvme_failure_surfaces(tmpd, monkeypatch):
+    """A failed NVMe job is still published (no stream may hang on it), but the
+    step's result and the next iteration fail with TC_EIO instead of returning
+    values computed from bytes that were never read."""
+    from paper_2511_14124_b200 import _native as N
+    tr, m = write_with_states(tmpd, "f9", [4096] * 7, 3 * 4096, 3 * 4096 + 2 * 6 * 4096, iters=3)
+    e = Engine(tr, m, {"policy": "tencache"}, nvme_dir=tmpd)
+    e.seed(7)
+    monkeypatch.setenv("TC_NVME_FAIL_JOB", "1")  # the first job after the seed's synchronous writes
+    e.iteration(**HP)
+    with pytest.raises(N.TencacheError) as ei:
+        e.step_result()  # fails here when the failed job fed this iteration's compute,
+        e.sync()         # else when the queue drains
+    assert ei.value.code == N.TC_EIO
+    monkeypatch.delenv("TC_NVME_FAIL_JOB")
     e.close()
