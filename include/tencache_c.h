@@ -203,6 +203,11 @@ int tc_engine_read_grad(tc_engine* e, uint32_t tensor, void* host_dst, uint64_t 
 void* tc_engine_gpu_ptr(tc_engine* e, uint32_t tensor);
 /* Gradient buffer (bf16, on GPU) of a parameter tensor. */
 void* tc_engine_grad_ptr(tc_engine* e, uint32_t tensor);
+/* The engine's HBM parameter pool (every GPU slot tc_engine_gpu_ptr and
+ * tc_engine_step_begin return lies inside it) and its gradient region (every
+ * tc_engine_grad_ptr), so a framework can alias them once as tensors and
+ * slice per step instead of wrapping raw pointers every step. */
+int tc_engine_regions(tc_engine* e, void** hbm_pool, uint64_t* hbm_pool_bytes, void** grads, uint64_t* grad_bytes);
 
 typedef struct {
   double lr, beta1, beta2, eps, weight_decay;
@@ -224,6 +229,49 @@ typedef struct {
  * enqueueing (call tc_engine_sync to wait). */
 int tc_engine_iteration(tc_engine* e, const tc_step_options* so, void* compute_stream);
 int tc_engine_sync(tc_engine* e);
+
+/* Per-step execution driven by a training loop: the same iteration, but the
+ * caller computes each forward/backward step on `compute_stream` between
+ * step_begin and step_end, at the reference engine's call points
+ * (engine.cpp:119-131 on_step_begin, :157-168 on_step_end, :170-187 restore
+ * point / iteration end / reset; PAPER.md:599 drives them from module hooks).
+ *
+ *   tc_engine_iteration_begin(e, so, stream)      decisions of the iteration,
+ *                                                 optimizer pre-staging
+ *   for step i in trace order:
+ *     tc_engine_step_begin(e, i, ptrs, cap, &n)   [restore point,] on_step_begin's
+ *                                                 moves; `stream` is ordered after
+ *                                                 the step tensors' arrivals;
+ *                                                 ptrs[k] = HBM address of the
+ *                                                 step's k-th tensor (fwd/bwd
+ *                                                 steps; n = 0 for optimizer steps)
+ *     ... caller's kernels on `stream` read the chunks; a backward step
+ *         writes each parameter's bf16 gradient at tc_engine_grad_ptr ...
+ *     tc_engine_step_end(e, i)                    the chunks are released to the
+ *                                                 policy after the caller's work;
+ *                                                 a backward step's gradients are
+ *                                                 final: the fused AdamW of every
+ *                                                 update hoisted behind it runs
+ *                                                 (after the gradient lands);
+ *                                                 on_step_end's moves
+ *   tc_engine_iteration_end(e)                    remaining restore point,
+ *                                                 on_iteration_end, reset
+ *
+ * Steps run exactly once each, in order (TC_EARG otherwise, nothing done).
+ * so->compute_mode 0 also checksums every accessed chunk (tc_engine_step_result);
+ * 3 = the caller's compute only. The engine's own stand-ins (modes 1, 2) do
+ * not run. A backward step's gradient writes are ordered after the previous
+ * update that read them. Not available with a ZeRO-3 exchange (TC_ECONFIG).
+ * tc_engine_step_begin with too small a `ptrs` returns TC_ERANGE with the step
+ * open (*n = its tensor count; read the addresses with tc_engine_gpu_ptr). */
+int tc_engine_iteration_begin(tc_engine* e, const tc_step_options* so, void* compute_stream);
+int tc_engine_step_begin(tc_engine* e, uint32_t step, void** ptrs, size_t cap, size_t* n);
+int tc_engine_step_end(tc_engine* e, uint32_t step);
+int tc_engine_iteration_end(tc_engine* e);
+/* Give up an open iteration (the caller's step failed): the remaining moves
+ * still run so placement and the next iteration's decisions stay consistent;
+ * updates not yet run are skipped. No-op when no iteration is open. */
+int tc_engine_iteration_abort(tc_engine* e);
 
 /* Counters of the last iteration(s) since the previous reset_stats. */
 typedef struct {

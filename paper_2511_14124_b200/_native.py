@@ -133,6 +133,14 @@ _SIGS = {
     "tc_engine_gpu_ptr": ([C.c_void_p, C.c_uint32], C.c_void_p),
     "tc_engine_grad_ptr": ([C.c_void_p, C.c_uint32], C.c_void_p),
     "tc_engine_iteration": ([C.c_void_p, C.POINTER(tc_step_options), C.c_void_p], C.c_int),
+    "tc_engine_iteration_begin": ([C.c_void_p, C.POINTER(tc_step_options), C.c_void_p], C.c_int),
+    "tc_engine_step_begin": ([C.c_void_p, C.c_uint32, C.POINTER(C.c_void_p), C.c_size_t, C.POINTER(C.c_size_t)],
+                             C.c_int),
+    "tc_engine_step_end": ([C.c_void_p, C.c_uint32], C.c_int),
+    "tc_engine_regions": ([C.c_void_p, C.POINTER(C.c_void_p), C.POINTER(C.c_uint64), C.POINTER(C.c_void_p),
+                           C.POINTER(C.c_uint64)], C.c_int),
+    "tc_engine_iteration_end": ([C.c_void_p], C.c_int),
+    "tc_engine_iteration_abort": ([C.c_void_p], C.c_int),
     "tc_engine_sync": ([C.c_void_p], C.c_int),
     "tc_engine_stats_get": ([C.c_void_p, C.POINTER(tc_engine_stats)], C.c_int),
     "tc_engine_stats_reset": ([C.c_void_p], C.c_int),

@@ -80,23 +80,90 @@ void* tc_engine_grad_ptr(tc_engine* e, uint32_t tensor) {
   }
 }
 
+namespace {
+StepOptions step_options(const tc_step_options* so) {
+  StepOptions o;
+  if (so) {
+    o.lr = so->lr;
+    o.beta1 = so->beta1;
+    o.beta2 = so->beta2;
+    o.eps = so->eps;
+    o.weight_decay = so->weight_decay;
+    o.grad_scale = so->grad_scale;
+    o.compute_mode = so->compute_mode;
+    o.spin_ctas = so->spin_ctas;
+    o.hoist_optimizer = (so->flags & 1) == 0;
+    o.prestage = (so->flags & 2) == 0;
+    o.prologue = (so->flags & 4) == 0;
+  }
+  return o;
+}
+}  // namespace
+
 int tc_engine_iteration(tc_engine* e, const tc_step_options* so, void* compute_stream) {
   TC_GUARD({
-    StepOptions o;
-    if (so) {
-      o.lr = so->lr;
-      o.beta1 = so->beta1;
-      o.beta2 = so->beta2;
-      o.eps = so->eps;
-      o.weight_decay = so->weight_decay;
-      o.grad_scale = so->grad_scale;
-      o.compute_mode = so->compute_mode;
-      o.spin_ctas = so->spin_ctas;
-      o.hoist_optimizer = (so->flags & 1) == 0;
-      o.prestage = (so->flags & 2) == 0;
-      o.prologue = (so->flags & 4) == 0;
-    }
-    e->ex->iteration(o, static_cast<cudaStream_t>(compute_stream));
+    if (!e) return set_error(TC_EARG, "null engine");
+    e->ex->iteration(step_options(so), static_cast<cudaStream_t>(compute_stream));
+    return TC_OK;
+  })
+}
+
+int tc_engine_iteration_begin(tc_engine* e, const tc_step_options* so, void* compute_stream) {
+  TC_GUARD({
+    if (!e) return set_error(TC_EARG, "null engine");
+    e->ex->iteration_begin(step_options(so), static_cast<cudaStream_t>(compute_stream), true);
+    return TC_OK;
+  })
+}
+
+int tc_engine_step_begin(tc_engine* e, uint32_t step, void** ptrs, size_t cap, size_t* n) {
+  TC_GUARD({
+    if (!e) return set_error(TC_EARG, "null engine");
+    const std::vector<void*> v = e->ex->step_begin(step);
+    if (n) *n = v.size();
+    if (v.size() > cap || (!v.empty() && ptrs == nullptr))
+      return set_error(TC_ERANGE, "tc_engine_step_begin: the step has " + std::to_string(v.size()) +
+                                      " tensors; the step is open, read them with tc_engine_gpu_ptr");
+    for (std::size_t i = 0; i < v.size(); ++i) ptrs[i] = v[i];
+    return TC_OK;
+  })
+}
+
+int tc_engine_step_end(tc_engine* e, uint32_t step) {
+  TC_GUARD({
+    if (!e) return set_error(TC_EARG, "null engine");
+    e->ex->step_end(step);
+    return TC_OK;
+  })
+}
+
+int tc_engine_iteration_end(tc_engine* e) {
+  TC_GUARD({
+    if (!e) return set_error(TC_EARG, "null engine");
+    e->ex->iteration_end();
+    return TC_OK;
+  })
+}
+
+int tc_engine_iteration_abort(tc_engine* e) {
+  TC_GUARD({
+    if (!e) return set_error(TC_EARG, "null engine");
+    e->ex->iteration_abort();
+    return TC_OK;
+  })
+}
+
+int tc_engine_regions(tc_engine* e, void** hbm_pool, uint64_t* hbm_pool_bytes, void** grads, uint64_t* grad_bytes) {
+  TC_GUARD({
+    if (!e) return set_error(TC_EARG, "null engine");
+    void* pb = nullptr;
+    void* gb = nullptr;
+    std::uint64_t pn = 0, gn = 0;
+    e->ex->regions(&pb, &pn, &gb, &gn);
+    if (hbm_pool) *hbm_pool = pb;
+    if (hbm_pool_bytes) *hbm_pool_bytes = pn;
+    if (grads) *grads = gb;
+    if (grad_bytes) *grad_bytes = gn;
     return TC_OK;
   })
 }

@@ -16,13 +16,20 @@ namespace tcb {
 
 using namespace tencache;
 
-void Executor::param_step(const TraceStep& step, std::size_t, cudaStream_t cs) {
+// A forward/backward step's tensors become readable on the compute stream:
+// wait for their slots' writers (arrivals) and pending barriers, count hits
+// (engine_internal.hpp:98-102), and run the access-side data work (ZeRO-3
+// gather, or the checksum of the migrated bytes when compute_mode is 0).
+void Executor::param_enter(const TraceStep& step, cudaStream_t cs, bool external) {
   cudaEvent_t reach = events_.get(true), go = events_.get(true);
   TCB_CK(cudaEventRecord(reach, cs));
   for (TensorId id : step.tensor_ids) {
     TensorRec& x = rec(id);
     if (x.tier != PTier::Gpu) throw DeviceError(TC_EINTERNAL, "step tensor " + std::to_string(id) + " not GPU-resident");
     wait_for_read(cs, slot_of(x).sync);
+    // the caller writes this step's gradients: not before the previous
+    // update that read them is done
+    if (external && step.phase == Phase::Backward && x.grad_reader) TCB_CK(cudaStreamWaitEvent(cs, x.grad_reader, 0));
   }
   wait_barriers(cs);
   TCB_CK(cudaEventRecord(go, cs));
@@ -38,12 +45,18 @@ void Executor::param_step(const TraceStep& step, std::size_t, cudaStream_t cs) {
     if (z3_) {
       zero3_access(x, step.phase == Phase::Backward, cs);
     } else if (access_cursor_ < n_accesses_) {
-      TCB_CK(launch_checksum(where(x), x.bytes & ~3ull,
-                             reinterpret_cast<unsigned long long*>(cks_base_ + access_cursor_), cs));
+      if (so_.compute_mode == 0 || !external)
+        TCB_CK(launch_checksum(where(x), x.bytes & ~3ull,
+                               reinterpret_cast<unsigned long long*>(cks_base_ + access_cursor_), cs));
       ++stats_.kernel_launches;
       ++access_cursor_;
     }
   }
+}
+
+// The layer-compute stand-in of iteration(): a 1-CTA spin or bf16 GEMMs over
+// the migrated chunk for the step's compute_us (trace.hpp:38).
+void Executor::param_compute(const TraceStep& step, cudaStream_t cs) {
   const double us = step.compute_us * cfg_.batch_scale;
   if (so_.compute_mode == 1) {
     TCB_CK(launch_spin(static_cast<std::uint64_t>(us * 1000.0), so_.spin_ctas, cs));
@@ -59,9 +72,18 @@ void Executor::param_step(const TraceStep& step, std::size_t, cudaStream_t cs) {
     stats_.compute_gemms += static_cast<std::uint64_t>(standin_->run(cs, where(rec(step.tensor_ids.front())), us));
     stats_.compute_flops += standin_->flops_issued() - f0;
   }
+}
+
+// Everything the step computes is enqueued: its slots are read until here,
+// and a caller-computed backward step's gradients are final here.
+void Executor::param_exit(const TraceStep& step, cudaStream_t cs, bool external) {
   cudaEvent_t done = events_.get(false);
   TCB_CK(cudaEventRecord(done, cs));
-  for (TensorId id : step.tensor_ids) slot_of(rec(id)).sync.readers.push_back(done);
+  for (TensorId id : step.tensor_ids) {
+    TensorRec& x = rec(id);
+    slot_of(x).sync.readers.push_back(done);
+    if (external && step.phase == Phase::Backward) x.grad_ready = done;
+  }
 }
 
 // One optimizer update, data side: state chunk H2D into an HBM stage, fused
@@ -151,6 +173,7 @@ void Executor::optimizer_work(TensorRec& s, TensorRec& p) {
   ++stats_.adam_launches;
   stats_.adam_elems += n;
   *psync = SlotSync{a1, {}};
+  p.grad_reader = a1;
   p.nvme_valid = false;  // any NVMe replica of the parameter is now stale
   if (p.has_home) p.home_valid = false;
   if (on_gpu) p.arrival = nullptr;
@@ -299,8 +322,24 @@ std::size_t Executor::forward_prestage_budget(const std::vector<Hook>& hooks) co
   return std::max<std::size_t>(1, static_cast<std::size_t>(spare / sbytes));
 }
 
+// An iteration is opened (decisions, hoisting plan, pre-staging), then driven
+// step by step -- by iteration() itself, or by a training loop through
+// tc_engine_step_begin / tc_engine_step_end, which run the same hooks at the
+// reference's fixed call points (engine.cpp:119-131 begin, :157-168 end) --
+// and closed (restore point, iteration end, harvest).
 void Executor::iteration(const StepOptions& so, cudaStream_t compute) {
+  iteration_begin(so, compute, false);
+  for (std::size_t i = 0; i < trace_.steps.size(); ++i) {
+    step_begin(i);
+    step_end(i);
+  }
+  iteration_end();
+}
+
+void Executor::iteration_begin(const StepOptions& so, cudaStream_t compute, bool external) {
   TCB_CK(cudaSetDevice(device_));
+  if (open_) throw DeviceError(TC_EARG, "iteration_begin: an iteration is already open");
+  if (external && z3_) throw DeviceError(TC_ECONFIG, "per-step execution with a ZeRO-3 exchange is not supported");
   if (compute == nullptr) {
     if (!compute_owned_) TCB_CK(cudaStreamCreateWithFlags(&compute_owned_, cudaStreamNonBlocking));
     compute = compute_owned_;
@@ -321,25 +360,26 @@ void Executor::iteration(const StepOptions& so, cudaStream_t compute) {
   }
   TCB_CK(launch_fill_u64(reinterpret_cast<unsigned long long*>(cks_base_), 0ull, std::max<std::size_t>(n_accesses_, 1),
                          compute));
-  std::vector<Hook> hooks;
+  OpenIter it;
+  it.external = external;
   if (ahead_) {  // decided (and its first states staged) at the end of the previous iteration
-    hooks = std::move(*ahead_);
+    it.hooks = std::move(*ahead_);
     ahead_.reset();
   } else {
     nvtxRangePushA("tencache.decide");
-    hooks = decide_iteration();
+    it.hooks = decide_iteration();
     nvtxRangePop();
     drop_staged();
   }
-  const std::vector<std::size_t> hoist = plan_hoisting(hooks);
+  it.hoist = plan_hoisting(it.hooks);
   const std::size_t n = trace_.steps.size();
-  std::vector<std::vector<std::size_t>> after(n);
+  it.after.assign(n, {});
   for (std::size_t j = 0; j < n; ++j)
-    if (hoist[j] < n) after[hoist[j]].push_back(j);
+    if (it.hoist[j] < n) it.after[it.hoist[j]].push_back(j);
   // Hoisted updates in execution order; their states can be staged any time
   // (no decision touches them before their update, plan_hoisting). States
   // staged by the prologue are skipped by refill_stages.
-  set_prestage_order(hooks, hoist);
+  set_prestage_order(it.hooks, it.hoist);
   // states the prologue staged come first in the order: continue after them
   while (prestage_next_ < prestage_order_.size() && staged_.count(prestage_order_[prestage_next_])) ++prestage_next_;
   if (so_.prestage) {
@@ -348,56 +388,119 @@ void Executor::iteration(const StepOptions& so, cudaStream_t compute) {
     // prefetch so it never competes with t's critical H2D traffic.
     if (prestage_gate_ && last_h2d_) TCB_CK(cudaStreamWaitEvent(h2d_opt_, last_h2d_, 0));
     refill_stages(prestage_fwd_override_ >= 0 ? static_cast<std::size_t>(prestage_fwd_override_)
-                                              : forward_prestage_budget(hooks));
+                                              : forward_prestage_budget(it.hooks));
   }
-  auto mark = [&] {
-    cudaEvent_t e = events_.get(true);
-    TCB_CK(cudaEventRecord(e, compute));
-    phase_marks_.push_back(e);
-  };
-  mark();
-  Phase prev = Phase::Forward;
-  for (const Hook& h : hooks) {
-    if (h.kind == 0) {
-      const TraceStep& step = trace_.steps[h.step];
-      if (step.phase != prev) {
-        mark();
-        if (prev == Phase::Forward && so_.prestage && edge_fill_) {
-          // Forward -> backward edge: the forward's cache prefetches are all
-          // issued and no backward prefetch exists yet, so the H2D link
-          // would idle until the first update frees a stage. Fill the rest
-          // of the ring, starting when the forward's last prefetch lands.
-          if (last_h2d_) TCB_CK(cudaStreamWaitEvent(h2d_opt_, last_h2d_, 0));
-          refill_stages(stage_.size());
-        }
-        prev = step.phase;
-      }
-      nvtxRangePushA(step.phase == Phase::Forward ? "tencache.fwd" : step.phase == Phase::Backward ? "tencache.bwd"
-                                                                                                   : "tencache.opt");
-      execute(h.reqs);
-      if (step.phase == Phase::OptimizerUpdate) {
-        if (hoist[h.step] == n) {  // in place: waits for the state's decisions
-          TensorRec& s = rec(step.tensor_ids.front());
-          if (s.partner < 0) throw DeviceError(TC_EINTERNAL, "optimizer step without a paired state");
-          wait_barriers(adam_stream());
-          optimizer_work(s, recs_[static_cast<std::size_t>(s.partner)]);
-        }
-      } else {
-        param_step(step, h.step, compute);
-        for (std::size_t j : after[h.step]) {
-          TensorRec& s = rec(trace_.steps[j].tensor_ids.front());
-          optimizer_work(s, recs_[static_cast<std::size_t>(s.partner)]);
-          if (so_.prestage) refill_stages(prestage_lookahead_);
-        }
-      }
-      nvtxRangePop();
-    } else {
-      execute(h.reqs);
+  open_ = std::move(it);
+  mark_phase();
+}
+
+void Executor::mark_phase() {
+  cudaEvent_t e = events_.get(true);
+  TCB_CK(cudaEventRecord(e, compute_));
+  phase_marks_.push_back(e);
+}
+
+// Hooks up to and including step i's begin hook (a restore point placed
+// before the first optimizer step runs here, engine.cpp:125-131), then the
+// compute stream is ordered after the step's tensors' arrivals. Returns the
+// device address of every tensor of a forward/backward step, in step order.
+std::vector<void*> Executor::step_begin(std::size_t i) {
+  if (!open_) throw DeviceError(TC_EARG, "step_begin: no open iteration (call iteration_begin)");
+  OpenIter& it = *open_;
+  if (it.in_step || i != it.next)
+    throw DeviceError(TC_EARG, "step_begin(" + std::to_string(i) + "): steps run in trace order, begin then end; expected " +
+                                   (it.in_step ? "step_end(" : "step_begin(") +
+                                   std::to_string(it.in_step ? it.next - 1 : it.next) + ")");
+  TCB_CK(cudaSetDevice(device_));
+  while (it.hk < it.hooks.size() && it.hooks[it.hk].kind == 2) execute(it.hooks[it.hk++].reqs);
+  if (it.hk >= it.hooks.size() || it.hooks[it.hk].kind != 0 || it.hooks[it.hk].step != i)
+    throw DeviceError(TC_EINTERNAL, "step_begin: hook sequence out of step");
+  const TraceStep& step = trace_.steps[i];
+  if (step.phase != it.prev) {
+    mark_phase();
+    if (it.prev == Phase::Forward && so_.prestage && edge_fill_) {
+      // Forward -> backward edge: the forward's cache prefetches are all
+      // issued and no backward prefetch exists yet, so the H2D link
+      // would idle until the first update frees a stage. Fill the rest
+      // of the ring, starting when the forward's last prefetch lands.
+      if (last_h2d_) TCB_CK(cudaStreamWaitEvent(h2d_opt_, last_h2d_, 0));
+      refill_stages(stage_.size());
+    }
+    it.prev = step.phase;
+  }
+  nvtxRangePushA(step.phase == Phase::Forward ? "tencache.fwd" : step.phase == Phase::Backward ? "tencache.bwd"
+                                                                                               : "tencache.opt");
+  execute(it.hooks[it.hk++].reqs);
+  it.in_step = true;
+  ++it.next;
+  std::vector<void*> ptrs;
+  if (step.phase != Phase::OptimizerUpdate) {
+    param_enter(step, compute_, it.external);
+    if (!it.external) param_compute(step, compute_);
+    for (TensorId id : step.tensor_ids) ptrs.push_back(where(rec(id)));
+  }
+  return ptrs;
+}
+
+// The step's compute is enqueued (by the caller, on the compute stream): its
+// tensors' slots are read until here, a backward step's gradients are final,
+// the updates hoisted behind this step run, then the step's end hook.
+void Executor::step_end(std::size_t i) {
+  if (!open_ || !open_->in_step || open_->next != i + 1)
+    throw DeviceError(TC_EARG, "step_end(" + std::to_string(i) + "): no such open step");
+  OpenIter& it = *open_;
+  TCB_CK(cudaSetDevice(device_));
+  const TraceStep& step = trace_.steps[i];
+  const std::size_t n = trace_.steps.size();
+  if (step.phase == Phase::OptimizerUpdate) {
+    if (it.hoist[i] == n) {  // in place: waits for the state's decisions
+      TensorRec& s = rec(step.tensor_ids.front());
+      if (s.partner < 0) throw DeviceError(TC_EINTERNAL, "optimizer step without a paired state");
+      wait_barriers(adam_stream());
+      optimizer_work(s, recs_[static_cast<std::size_t>(s.partner)]);
+    }
+  } else {
+    param_exit(step, compute_, it.external);
+    for (std::size_t j : it.after[i]) {
+      TensorRec& s = rec(trace_.steps[j].tensor_ids.front());
+      optimizer_work(s, recs_[static_cast<std::size_t>(s.partner)]);
+      if (so_.prestage) refill_stages(prestage_lookahead_);
     }
   }
-  mark();
+  nvtxRangePop();
+  if (it.hk >= it.hooks.size() || it.hooks[it.hk].kind != 1 || it.hooks[it.hk].step != i)
+    throw DeviceError(TC_EINTERNAL, "step_end: hook sequence out of step");
+  execute(it.hooks[it.hk++].reqs);
+  it.in_step = false;
+}
+
+void Executor::iteration_end() {
+  if (!open_) throw DeviceError(TC_EARG, "iteration_end: no open iteration");
+  if (open_->in_step || open_->next != trace_.steps.size())
+    throw DeviceError(TC_EARG, "iteration_end: " + std::to_string(trace_.steps.size() - open_->next) +
+                                   " step(s) not run" + (open_->in_step ? " (a step is still open)" : ""));
+  TCB_CK(cudaSetDevice(device_));
+  OpenIter& it = *open_;
+  while (it.hk < it.hooks.size()) execute(it.hooks[it.hk++].reqs);  // restore point (if not yet), iteration end
+  open_.reset();
+  mark_phase();
   finish_iteration();
   if (lookahead_ && so_.prestage && so_.prologue) prologue_next();
+}
+
+// Abandon an open iteration (the caller's step failed): the remaining hooks
+// still run so that tensors end at the policy's final placement and the
+// next iteration's decisions hold; no further compute is ordered.
+void Executor::iteration_abort() {
+  if (!open_) return;
+  if (open_->in_step) {
+    nvtxRangePop();
+    open_->in_step = false;
+  }
+  while (open_->hk < open_->hooks.size()) execute(open_->hooks[open_->hk++].reqs);
+  open_.reset();
+  mark_phase();
+  finish_iteration();
 }
 
 // Hoisted updates of an iteration in execution order = the order their
@@ -618,6 +721,7 @@ void Executor::scrub(std::uint64_t gen) {
   for (auto& r : recs_) {
     if (r.arrival && events_.done_by(r.arrival, gen)) r.arrival = nullptr;
     if (r.grad_ready && events_.done_by(r.grad_ready, gen)) r.grad_ready = nullptr;
+    if (r.grad_reader && events_.done_by(r.grad_reader, gen)) r.grad_reader = nullptr;
   }
   std::erase_if(barriers_, [&](cudaEvent_t e) { return events_.done_by(e, gen); });
   if (last_h2d_ && events_.done_by(last_h2d_, gen)) last_h2d_ = nullptr;

@@ -376,6 +376,7 @@ Executor::~Executor() {
                  static_cast<double>(stamps_), stamp_pre_ns_ / stamps_ * 1e-3, stamp_post_ns_ / stamps_ * 1e-3);
   cudaSetDevice(device_);
   try {
+    iteration_abort();
     drain();
   } catch (...) {
   }
@@ -849,7 +850,7 @@ void Executor::wait_barriers(cudaStream_t cs) {
 }
 
 void Executor::set_event_log(const std::string& path) {
-  drain();
+  sync();
   if (path.empty()) {
     event_log_.reset();
     return;
@@ -860,11 +861,12 @@ void Executor::set_event_log(const std::string& path) {
 
 void Executor::sync() {
   TCB_CK(cudaSetDevice(device_));
+  if (open_) throw DeviceError(TC_EARG, "an iteration is open: finish it with iteration_end (or abort it) first");
   drain();
 }
 
 const std::vector<std::uint64_t>& Executor::access_checksums() {
-  drain();
+  sync();
   return h_checksums_;
 }
 
@@ -970,5 +972,15 @@ void* Executor::gpu_ptr(TensorId id) {
 }
 
 void* Executor::grad_ptr(TensorId id) { return rec(id).grad; }
+
+void Executor::regions(void** pool, std::uint64_t* pool_bytes, void** grads, std::uint64_t* grad_bytes) {
+  *pool = gpu_.base();
+  *pool_bytes = gpu_.bytes();
+  *grads = grads_;
+  std::uint64_t g = 0;
+  for (const auto& r : recs_)
+    if (!r.is_state) g += r.bytes;
+  *grad_bytes = g;
+}
 
 }  // namespace tcb

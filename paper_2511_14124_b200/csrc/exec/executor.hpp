@@ -128,7 +128,8 @@ struct TensorRec {
   std::uint8_t* grad = nullptr;    // params: bf16 gradient in HBM
   int issued_since_access = 0;     // P7b hit definition
   cudaEvent_t arrival = nullptr;   // last H2D into its GPU slot (for on-time)
-  cudaEvent_t grad_ready = nullptr;  // ZeRO-3: reduce-scatter that produced its gradient
+  cudaEvent_t grad_ready = nullptr;  // producer of its gradient (ZeRO-3 reduce-scatter, or the caller's backward step)
+  cudaEvent_t grad_reader = nullptr; // last fused AdamW that read its gradient
   // A retained home copy (comparison policies fetch with src_retains and drop
   // instantly): the host slot stays allocated while the GPU copy is primary.
   bool has_home = false, home_valid = false;
@@ -187,11 +188,19 @@ class Executor {
 
   void seed(std::uint64_t seed);
   void iteration(const StepOptions& so, cudaStream_t compute);
+  // per-step execution (tc_engine_iteration_begin / step_begin / step_end / iteration_end)
+  void iteration_begin(const StepOptions& so, cudaStream_t compute, bool external);
+  std::vector<void*> step_begin(std::size_t i);
+  void step_end(std::size_t i);
+  void iteration_end();
+  void iteration_abort();
+  bool iteration_open() const { return open_.has_value(); }
   void sync();
   void read_tensor(tencache::TensorId id, void* dst, std::uint64_t bytes);
   void write_tensor(tencache::TensorId id, const void* src, std::uint64_t bytes);
   void* gpu_ptr(tencache::TensorId id);
   void* grad_ptr(tencache::TensorId id);
+  void regions(void** pool, std::uint64_t* pool_bytes, void** grads, std::uint64_t* grad_bytes);
   std::uint64_t tensor_bytes(tencache::TensorId id) { return rec(id).bytes; }
   void enable_zero3(int world, int rank, const ncclUniqueId& id, const std::uint64_t* layer_elems,
                     const std::uint64_t* layer_per, std::uint32_t n_layers);
@@ -256,7 +265,21 @@ class Executor {
   };
   std::vector<Hook> decide_iteration();
   std::vector<std::size_t> plan_hoisting(const std::vector<Hook>& hooks);
-  void param_step(const tencache::TraceStep& step, std::size_t step_idx, cudaStream_t cs);
+  void param_enter(const tencache::TraceStep& step, cudaStream_t cs, bool external);
+  void param_compute(const tencache::TraceStep& step, cudaStream_t cs);
+  void param_exit(const tencache::TraceStep& step, cudaStream_t cs, bool external);
+  void mark_phase();
+  struct OpenIter {  // the iteration between iteration_begin and iteration_end
+    std::vector<Hook> hooks;
+    std::vector<std::size_t> hoist;
+    std::vector<std::vector<std::size_t>> after;  // hoisted updates run after each step
+    std::size_t hk = 0;    // next hook
+    std::size_t next = 0;  // next step to begin
+    bool in_step = false;
+    bool external = false;  // the caller computes between step_begin and step_end
+    tencache::Phase prev = tencache::Phase::Forward;
+  };
+  std::optional<OpenIter> open_;
   void zero3_access(TensorRec& x, bool backward, cudaStream_t cs);
   void optimizer_work(TensorRec& s, TensorRec& p);
   std::size_t stage_state(TensorRec& s);

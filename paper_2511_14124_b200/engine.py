@@ -51,6 +51,13 @@ class Engine:
     def grad_ptr(self, tensor_id):
         return N.lib().tc_engine_grad_ptr(self._h, tensor_id)
 
+    def regions(self):
+        """(hbm_pool_ptr, bytes, grad_region_ptr, bytes) -- tc_engine_regions."""
+        pb, gb = C.c_void_p(), C.c_void_p()
+        pn, gn = C.c_uint64(), C.c_uint64()
+        N.check(N.lib().tc_engine_regions(self._h, C.byref(pb), C.byref(pn), C.byref(gb), C.byref(gn)))
+        return pb.value, pn.value, gb.value, gn.value
+
     # -- execution --------------------------------------------------------
     def iteration(self, lr=1e-4, beta1=0.9, beta2=0.999, eps=1e-8, weight_decay=0.01, grad_scale=1.0,
                   compute_mode=0, spin_ctas=1, stream=None, hoist=True, prestage=True, last=False):
@@ -60,6 +67,36 @@ class Engine:
         flags = (0 if hoist else 1) | (0 if prestage else 2) | (4 if last else 0)
         so = N.tc_step_options(lr, beta1, beta2, eps, weight_decay, grad_scale, compute_mode, spin_ctas, flags)
         N.check(N.lib().tc_engine_iteration(self._h, C.byref(so), C.c_void_p(stream or 0)))
+
+    # -- per-step execution (a training loop computes between the calls) --
+    def iteration_begin(self, lr=1e-4, beta1=0.9, beta2=0.999, eps=1e-8, weight_decay=0.01, grad_scale=1.0,
+                        checksums=False, stream=None, hoist=True, prestage=True, last=False):
+        """Open an iteration whose forward/backward steps the caller computes
+        (tc_engine_iteration_begin). checksums=True also checksums every
+        accessed chunk (compute_mode 0) for step_result()."""
+        flags = (0 if hoist else 1) | (0 if prestage else 2) | (4 if last else 0)
+        so = N.tc_step_options(lr, beta1, beta2, eps, weight_decay, grad_scale, 0 if checksums else 3, 1, flags)
+        N.check(N.lib().tc_engine_iteration_begin(self._h, C.byref(so), C.c_void_p(stream or 0)))
+
+    def step_begin(self, step):
+        """[restore point,] on_step_begin's moves; returns the HBM address of
+        each of the step's tensors (empty for an optimizer step)."""
+        ptrs = (C.c_void_p * 64)()
+        n = C.c_size_t()
+        rc = N.lib().tc_engine_step_begin(self._h, step, ptrs, 64, C.byref(n))
+        if rc == N.TC_ERANGE:
+            raise N.TencacheError(rc, "step has more than 64 tensors")
+        N.check(rc)
+        return [ptrs[i] for i in range(n.value)]
+
+    def step_end(self, step):
+        N.check(N.lib().tc_engine_step_end(self._h, step))
+
+    def iteration_end(self):
+        N.check(N.lib().tc_engine_iteration_end(self._h))
+
+    def iteration_abort(self):
+        N.check(N.lib().tc_engine_iteration_abort(self._h))
 
     def sync(self):
         N.check(N.lib().tc_engine_sync(self._h))

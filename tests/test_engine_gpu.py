@@ -453,10 +453,10 @@ def test_nvme_failure_surfaces(tmpd, monkeypatch):
     e = Engine(tr, m, {"policy": "tencache"}, nvme_dir=tmpd)
     e.seed(7)
     monkeypatch.setenv("TC_NVME_FAIL_JOB", "1")  # the first job after the seed's synchronous writes
-    e.iteration(**HP)
     with pytest.raises(N.TencacheError) as ei:
-        e.step_result()  # fails here when the failed job fed this iteration's compute,
-        e.sync()         # else when the queue drains
+        e.iteration(**HP)  # fails here when the job failed before the enqueue finished (the prologue checks),
+        e.step_result()    # here when the failed job fed this iteration's compute,
+        e.sync()           # else when the queue drains
     assert ei.value.code == N.TC_EIO
     monkeypatch.delenv("TC_NVME_FAIL_JOB")
     e.close()
