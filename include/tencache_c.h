@@ -145,11 +145,18 @@ int tc_adamw(float* state, const void* grad, void* param_out, uint64_t n, double
 int tc_adamw_split(float* p32, float* m, float* v, const void* grad, void* param_out, uint64_t n, double lr,
                    double beta1, double beta2, double eps, double weight_decay, int64_t step, float grad_scale,
                    void* stream);
-/* Select the AdamW kernel implementation (all are bit-identical): 0 register-
- * unrolled, 1 register-lean one-wave, 2 TMA bulk-copy pipeline 256 thr x 3 stages
- * (default), 3 TMA 512 thr x 3 stages, 4 TMA 512 thr x 6 stages, 5 TMA 1024 thr x 6.
- * Returns the previous selection. */
-int tc_set_adamw_variant(int variant);
+/* Up to 8 chunks updated in ONE launch (same hyper-parameters and step; each
+ * chunk's n a multiple of 8 with 16-byte aligned pointers, else TC_EARG):
+ * what the executor uses for consecutive hoisted updates, so k chunks pay one
+ * launch's front-end latency instead of k. state = [p32 | m | v] of n each. */
+typedef struct {
+  float* state;
+  const void* grad;
+  void* param_out;
+  uint64_t n;
+} tc_adam_chunk;
+int tc_adamw_batch(const tc_adam_chunk* chunks, uint32_t count, double lr, double beta1, double beta2, double eps,
+                   double weight_decay, int64_t step, float grad_scale, void* stream);
 /* The 8 fp32 scalars the update uses, for parity tests. */
 int tc_adamw_scalars(double lr, double beta1, double beta2, double eps, double weight_decay, int64_t step,
                      float out[8]);
@@ -165,6 +172,65 @@ int tc_fill_normal_bf16(void* out, uint64_t n, float sigma, uint64_t seed, uint6
 /* Busy the compute stream for `us` microseconds on `ctas` CTAs (the layer
  * compute stand-in; trace compute_us, trace.hpp:38). */
 int tc_spin(double us, int ctas, void* stream);
+
+/* =========== executor building blocks (SURVEY.md §8(b) primitives) ====== */
+/* What a host runtime with its own executor composes (the reference's
+ * decisions, engine.hpp:52-71 / scheduler.hpp:20-33, turned into data
+ * movement); tc_engine_* below is the same machinery driven by this repo's
+ * executor. */
+
+/* A region carved into size classes like the policy's BufferPool
+ * (bufpool.cpp:47-66): classes in ascending size, chunks of a class back to
+ * back. device >= 0: HBM of that device; device < 0: pinned host memory
+ * (transparent huge pages + cudaHostRegister, portable). Class sizes are
+ * non-zero multiples of 16 (TC_EARG). */
+typedef struct tc_pool tc_pool;
+int tc_pool_create(int device, const uint64_t* class_sizes, const uint32_t* counts, uint32_t n_classes,
+                   tc_pool** out);
+void tc_pool_destroy(tc_pool* p);
+/* Address of chunk `index` of class `size` (TC_EPOOL: no such chunk, the
+ * reference's PoolError UnknownSizeClass, bufpool.hpp:18-21). */
+int tc_pool_chunk(tc_pool* p, uint64_t size, uint32_t index, void** out);
+uint64_t tc_pool_bytes(const tc_pool* p);
+
+/* Copy-engine copies between pinned host memory and HBM on `stream`. */
+int tc_copy_h2d(void* dst, const void* src, uint64_t bytes, void* stream);
+int tc_copy_d2h(void* dst, const void* src, uint64_t bytes, void* stream);
+
+/* Events: the ordering primitive between copy streams and compute. */
+typedef struct tc_event tc_event;
+int tc_event_create(int timing, tc_event** out);
+void tc_event_destroy(tc_event* e);
+int tc_event_record(tc_event* e, void* stream);
+int tc_event_wait(void* stream, tc_event* e);  /* `stream` waits for `e` */
+int tc_event_query(tc_event* e, int* done);
+int tc_event_synchronize(tc_event* e);
+int tc_event_elapsed_ms(tc_event* start, tc_event* end, float* ms);
+
+/* The ZeRO-3 exchange's collectives: all-gather of each
+ * rank's bytes, reduce-scatter (sum) of bf16 gradients. The id comes from
+ * tc_nccl_unique_id on one rank, broadcast by the caller. */
+typedef struct tc_comm tc_comm;
+int tc_nccl_comm_create(const uint8_t id[128], int world, int rank, int device, tc_comm** out);
+void tc_nccl_comm_destroy(tc_comm* c);
+int tc_nccl_allgather(tc_comm* c, const void* send, void* recv, uint64_t bytes_per_rank, void* stream);
+int tc_nccl_reducescatter(tc_comm* c, const void* send, void* recv, uint64_t elems_per_rank, void* stream);
+
+/* The NVMe tier: one logical byte range over `files` files (16 MiB stripes),
+ * O_DIRECT when `direct` (offsets, sizes and buffers 4 KiB-aligned), reached
+ * through pinned bounce buffers (the staging slot of engine.cpp:214-221).
+ * Jobs run in submission order on a worker pool; a job may first wait for
+ * `after` (e.g. the D2H copy that filled the bounce buffer). *job identifies
+ * it for tc_nvme_wait (host) / tc_nvme_stream_wait (a GPU stream waits, no
+ * host thread blocks). A failed job fails tc_nvme_wait with TC_EIO. */
+typedef struct tc_nvme tc_nvme;
+int tc_nvme_open(const char* dir, uint64_t bytes, int files, int direct, int device, tc_nvme** out);
+void tc_nvme_close(tc_nvme* f);
+int tc_nvme_write(tc_nvme* f, uint64_t offset, const void* pinned_src, uint64_t bytes, tc_event* after,
+                  uint64_t* job);
+int tc_nvme_read(tc_nvme* f, uint64_t offset, void* pinned_dst, uint64_t bytes, tc_event* after, uint64_t* job);
+int tc_nvme_wait(tc_nvme* f, uint64_t job);
+int tc_nvme_stream_wait(tc_nvme* f, uint64_t job, void* stream);
 
 /* ====================== migration executor (real mode) ================= */
 /* A per-GPU engine: pinned host pools and an HBM pool carved exactly like the

@@ -56,6 +56,10 @@ class tc_segment(C.Structure):
     _fields_ = [("src_off", C.c_uint64), ("dst_off", C.c_uint64), ("bytes", C.c_uint64)]
 
 
+class tc_adam_chunk(C.Structure):
+    _fields_ = [("state", C.c_void_p), ("grad", C.c_void_p), ("param_out", C.c_void_p), ("n", C.c_uint64)]
+
+
 class tc_engine_options(C.Structure):
     _fields_ = [("device", C.c_int), ("nvme_dir", C.c_char_p), ("gpu_spare_slots", C.c_int),
                 ("host_spare_slots", C.c_int), ("opt_stage_slots", C.c_int), ("direct_io", C.c_int),
@@ -117,11 +121,36 @@ _SIGS = {
                   C.c_double, C.c_int64, C.c_float, C.c_void_p], C.c_int),
     "tc_adamw_split": ([C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_uint64, C.c_double,
                         C.c_double, C.c_double, C.c_double, C.c_double, C.c_int64, C.c_float, C.c_void_p], C.c_int),
-    "tc_set_adamw_variant": ([C.c_int], C.c_int),
+    "tc_adamw_batch": ([C.c_void_p, C.c_uint32] + [C.c_double] * 5 + [C.c_int64, C.c_float, C.c_void_p], C.c_int),
     "tc_adamw_scalars": ([C.c_double] * 5 + [C.c_int64, C.POINTER(C.c_float)], C.c_int),
     "tc_checksum": ([C.c_void_p, C.c_uint64, C.c_void_p, C.c_void_p], C.c_int),
     "tc_spin": ([C.c_double, C.c_int, C.c_void_p], C.c_int),
     "tc_fill_normal_bf16": ([C.c_void_p, C.c_uint64, C.c_float, C.c_uint64, C.c_uint64, C.c_void_p], C.c_int),
+    # executor building blocks (SURVEY.md §8(b) primitives)
+    "tc_pool_create": ([C.c_int, C.POINTER(C.c_uint64), C.POINTER(C.c_uint32), C.c_uint32, C.POINTER(C.c_void_p)],
+                       C.c_int),
+    "tc_pool_destroy": ([C.c_void_p], None),
+    "tc_pool_chunk": ([C.c_void_p, C.c_uint64, C.c_uint32, C.POINTER(C.c_void_p)], C.c_int),
+    "tc_pool_bytes": ([C.c_void_p], C.c_uint64),
+    "tc_copy_h2d": ([C.c_void_p, C.c_void_p, C.c_uint64, C.c_void_p], C.c_int),
+    "tc_copy_d2h": ([C.c_void_p, C.c_void_p, C.c_uint64, C.c_void_p], C.c_int),
+    "tc_event_create": ([C.c_int, C.POINTER(C.c_void_p)], C.c_int),
+    "tc_event_destroy": ([C.c_void_p], None),
+    "tc_event_record": ([C.c_void_p, C.c_void_p], C.c_int),
+    "tc_event_wait": ([C.c_void_p, C.c_void_p], C.c_int),
+    "tc_event_query": ([C.c_void_p, C.POINTER(C.c_int)], C.c_int),
+    "tc_event_synchronize": ([C.c_void_p], C.c_int),
+    "tc_event_elapsed_ms": ([C.c_void_p, C.c_void_p, C.POINTER(C.c_float)], C.c_int),
+    "tc_nccl_comm_create": ([C.c_void_p, C.c_int, C.c_int, C.c_int, C.POINTER(C.c_void_p)], C.c_int),
+    "tc_nccl_comm_destroy": ([C.c_void_p], None),
+    "tc_nccl_allgather": ([C.c_void_p, C.c_void_p, C.c_void_p, C.c_uint64, C.c_void_p], C.c_int),
+    "tc_nccl_reducescatter": ([C.c_void_p, C.c_void_p, C.c_void_p, C.c_uint64, C.c_void_p], C.c_int),
+    "tc_nvme_open": ([C.c_char_p, C.c_uint64, C.c_int, C.c_int, C.c_int, C.POINTER(C.c_void_p)], C.c_int),
+    "tc_nvme_close": ([C.c_void_p], None),
+    "tc_nvme_write": ([C.c_void_p, C.c_uint64, C.c_void_p, C.c_uint64, C.c_void_p, C.POINTER(C.c_uint64)], C.c_int),
+    "tc_nvme_read": ([C.c_void_p, C.c_uint64, C.c_void_p, C.c_uint64, C.c_void_p, C.POINTER(C.c_uint64)], C.c_int),
+    "tc_nvme_wait": ([C.c_void_p, C.c_uint64], C.c_int),
+    "tc_nvme_stream_wait": ([C.c_void_p, C.c_uint64, C.c_void_p], C.c_int),
     # executor
     "tc_engine_create": ([C.c_char_p, C.c_char_p, C.c_char_p, C.POINTER(tc_engine_options), C.POINTER(C.c_void_p)],
                          C.c_int),

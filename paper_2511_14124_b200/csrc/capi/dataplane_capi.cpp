@@ -106,10 +106,23 @@ int tc_adamw(float* state, const void* grad, void* param_out, uint64_t n, double
                         step, grad_scale, stream);
 }
 
-int tc_set_adamw_variant(int variant) {
-  const int prev = adamw_variant();
-  set_adamw_variant(variant);
-  return prev;
+int tc_adamw_batch(const tc_adam_chunk* chunks, uint32_t count, double lr, double beta1, double beta2, double eps,
+                   double weight_decay, int64_t step, float grad_scale, void* stream) {
+  if (count > static_cast<uint32_t>(kMaxAdamChunks) || (count && chunks == nullptr))
+    return set_error(TC_EARG, "tc_adamw_batch: 0..8 chunks");
+  AdamChunk c[kMaxAdamChunks];
+  for (uint32_t k = 0; k < count; ++k) {
+    const std::uint64_t n = chunks[k].n;
+    c[k] = AdamChunk{chunks[k].state, chunks[k].state + n, chunks[k].state + 2 * n,
+                     static_cast<const std::uint16_t*>(chunks[k].grad), static_cast<std::uint16_t*>(chunks[k].param_out), n};
+  }
+  const cudaError_t e = launch_adamw_batch(c, static_cast<int>(count), adam_scalars(lr, beta1, beta2, eps, weight_decay, step),
+                                           grad_scale, as_stream(stream));
+  if (e == cudaErrorInvalidValue) {
+    cudaGetLastError();
+    return set_error(TC_EARG, "tc_adamw_batch: every chunk needs n % 8 == 0 and 16-byte aligned pointers");
+  }
+  return cuda_status(e, "tc_adamw_batch");
 }
 
 int tc_adamw_scalars(double lr, double beta1, double beta2, double eps, double weight_decay, int64_t step,

@@ -17,13 +17,35 @@ struct AdamScalars {
 
 AdamScalars adam_scalars(double lr, double b1, double b2, double eps, double wd, std::int64_t step);
 
+// One chunk of a batched AdamW launch: n elements (a multiple of 8) at
+// 16-byte aligned addresses; pout may be null.
+struct AdamChunk {
+  float* p;
+  float* m;
+  float* v;
+  const std::uint16_t* g;
+  std::uint16_t* pout;
+  std::uint64_t n;
+};
+constexpr int kMaxAdamChunks = 8;
+struct AdamBatch {  // kernel parameter: the chunks and their first tile in the launch's tile space
+  AdamChunk chunk[kMaxAdamChunks];
+  std::uint64_t tile_begin[kMaxAdamChunks + 1];
+  int count;
+};
+
 // All launchers return cudaGetLastError() of the launch.
-// span_min/span_max (optional, TMA variants): atomicMin'd with the first
+// span_min/span_max (optional): atomicMin'd with the first
 // CTA's start and atomicMax'd with the last CTA's end (%globaltimer ns) — the
 // kernel's resident span, free of launch and queueing gaps.
 cudaError_t launch_adamw(float* p, float* m, float* v, const std::uint16_t* g, std::uint16_t* pout, std::uint64_t n,
                          const AdamScalars& s, float grad_scale, cudaStream_t st,
                          unsigned long long* span_min = nullptr, unsigned long long* span_max = nullptr);
+// Up to kMaxAdamChunks chunks in one launch (same hyper-parameters and step);
+// cudaErrorInvalidValue for an unaligned chunk or a count out of range.
+cudaError_t launch_adamw_batch(const AdamChunk* chunks, int count, const AdamScalars& s, float grad_scale,
+                               cudaStream_t st, unsigned long long* span_min = nullptr,
+                               unsigned long long* span_max = nullptr);
 cudaError_t launch_cast_bf16_to_f32(const std::uint16_t* in, float* out, std::uint64_t n, cudaStream_t st);
 cudaError_t launch_cast_f32_to_bf16(const float* in, std::uint16_t* out, std::uint64_t n, cudaStream_t st);
 // inverse = false: dst[dst_off..] <- src[src_off..]; true: dst[src_off..] <- src[dst_off..]
@@ -44,9 +66,6 @@ cudaError_t launch_fill_normal_bf16(std::uint16_t* out, std::uint64_t n, float s
 cudaError_t launch_init_state(const std::uint16_t* param, float* state, std::uint64_t n, cudaStream_t st);
 
 int num_sms();
-// AdamW kernel variant: 0 register-unrolled, 1 register-lean one wave, 2 TMA bulk pipeline.
-void set_adamw_variant(int v);
-int adamw_variant();
 
 }  // namespace tcb
 

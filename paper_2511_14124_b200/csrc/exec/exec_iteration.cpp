@@ -98,7 +98,6 @@ std::size_t Executor::stage_state(TensorRec& s) {
   stage_free_.pop_front();
   Slot& h = slot_of(s);
   tag_ = CopyTag{"opt_load", s.id, 1, 0};
-  if (opt_yield_ && last_h2d_) TCB_CK(cudaStreamWaitEvent(h2d_opt_, last_h2d_, 0));
   wait_for_write(h2d_opt_, stage_sync_[b]);
   wait_for_read(h2d_opt_, h.sync);
   cudaEvent_t e1 = copy(h2d_opt_, stage_[b], h.ptr, s.bytes, true);
@@ -116,86 +115,105 @@ void Executor::refill_stages(std::size_t want_staged) {
   }
 }
 
-void Executor::optimizer_work(TensorRec& s, TensorRec& p) {
+// One optimizer update, data side, in three parts so that consecutive
+// hoisted updates share one fused AdamW launch: prepare (the state's HBM
+// stage and the bf16 destination, every wait on the optimizer stream), one
+// launch for the batch, then per update the state's write-back and the
+// parameter's.
+Executor::UpdateJob Executor::prepare_update(TensorRec& s, TensorRec& p) {
   cudaStream_t ost = adam_stream();
-  const bool state_on_gpu = s.tier == PTier::Gpu;  // no-offload posture: update in place in HBM
-  if (!state_on_gpu && s.tier != PTier::HostOpt)
+  UpdateJob j;
+  j.s = &s;
+  j.p = &p;
+  j.state_on_gpu = s.tier == PTier::Gpu;  // no-offload posture: update in place in HBM
+  if (!j.state_on_gpu && s.tier != PTier::HostOpt)
     throw DeviceError(TC_EINTERNAL, "optimizer state not in host memory at its update");
-  const std::uint64_t n = p.bytes / 2;
-  std::uint8_t* stg;
-  std::size_t b = 0;
-  if (state_on_gpu) {
+  j.n = p.bytes / 2;
+  if (j.state_on_gpu) {
     Slot& gs = slot_of(s);
-    stg = gs.ptr;
+    j.stg = gs.ptr;
     wait_for_write(ost, gs.sync);
   } else {
     auto it = staged_.find(index_of(s.id));
-    b = it != staged_.end() ? it->second : stage_state(s);
+    j.b = it != staged_.end() ? it->second : stage_state(s);
     staged_.erase(index_of(s.id));
     stats_.opt_h2d_bytes += s.bytes;  // counted at the update it feeds (staging may be a prologue)
-    stg = stage_[b];
+    j.stg = stage_[j.b];
     // (null once a drain between the prologue's staging and this update completed it)
-    if (stage_sync_[b].writer) TCB_CK(cudaStreamWaitEvent(ost, stage_sync_[b].writer, 0));
+    if (stage_sync_[j.b].writer) TCB_CK(cudaStreamWaitEvent(ost, stage_sync_[j.b].writer, 0));
   }
   if (p.grad_ready) TCB_CK(cudaStreamWaitEvent(ost, p.grad_ready, 0));
-  std::uint8_t* pout;
-  SlotSync* psync;
-  const bool on_gpu = p.tier == PTier::Gpu;
-  if (on_gpu) {
+  j.on_gpu = p.tier == PTier::Gpu;
+  if (j.on_gpu) {
     Slot& g = slot_of(p);
-    pout = g.ptr;
-    psync = &g.sync;
-  } else {
+    j.pout = g.ptr;
+    j.psync = &g.sync;
+  } else {  // a ring of at least adam_batch_ scratch buffers: a batch never reuses one
     std::size_t& k = pout_next_[p.bytes];
-    pout = pout_scratch_[p.bytes][k];
-    psync = &pout_sync_[p.bytes][k];
+    j.pout = pout_scratch_[p.bytes][k];
+    j.psync = &pout_sync_[p.bytes][k];
     k = (k + 1) % pout_scratch_[p.bytes].size();
   }
-  wait_for_write(ost, *psync);
+  wait_for_write(ost, *j.psync);
+  return j;
+}
+
+void Executor::run_updates(std::vector<UpdateJob>& jobs) {
+  if (jobs.empty()) return;
+  cudaStream_t ost = adam_stream();
   cudaEvent_t a0 = events_.get(true), a1 = events_.get(true);
   TCB_CK(cudaEventRecord(a0, ost));
-  auto* st = reinterpret_cast<float*>(stg);
   const AdamScalars sc = adam_scalars(so_.lr, so_.beta1, so_.beta2, so_.eps, so_.weight_decay, adam_step_);
   unsigned long long *smin = nullptr, *smax = nullptr;
   const std::size_t cap = std::max<std::size_t>(recs_.size(), 1);
-  if (span_cursor_ < cap && adamw_variant() >= 2) {  // in-kernel resident span (TMA variants)
+  if (span_cursor_ < cap) {  // in-kernel resident span of this launch
     smin = span_base_ + span_cursor_;
     smax = span_base_ + cap + span_cursor_;
     ++span_cursor_;
   }
   if (adam_stamps_ && smin) TCB_CK(launch_stamp(smin + 2 * cap, ost));
-  TCB_CK(launch_adamw(st, st + n, st + 2 * n, reinterpret_cast<const std::uint16_t*>(p.grad),
-                      reinterpret_cast<std::uint16_t*>(pout), n, sc, so_.grad_scale, ost, smin, smax));
+  std::vector<AdamChunk> chunks;
+  for (const UpdateJob& j : jobs) {
+    auto* st = reinterpret_cast<float*>(j.stg);
+    chunks.push_back(AdamChunk{st, st + j.n, st + 2 * j.n, reinterpret_cast<const std::uint16_t*>(j.p->grad),
+                               reinterpret_cast<std::uint16_t*>(j.pout), j.n});
+    stats_.adam_elems += j.n;
+  }
+  TCB_CK(launch_adamw_batch(chunks.data(), static_cast<int>(chunks.size()), sc, so_.grad_scale, ost, smin, smax));
   if (adam_stamps_ && smin) TCB_CK(launch_stamp(smin + 3 * cap, ost));
   TCB_CK(cudaEventRecord(a1, ost));
   adam_.emplace_back(a0, a1);
   ++stats_.kernel_launches;
   ++stats_.adam_launches;
-  stats_.adam_elems += n;
-  *psync = SlotSync{a1, {}};
+  for (UpdateJob& j : jobs) finish_update(j, a1);
+}
+
+void Executor::finish_update(UpdateJob& j, cudaEvent_t a1) {
+  TensorRec& s = *j.s;
+  TensorRec& p = *j.p;
+  *j.psync = SlotSync{a1, {}};
   p.grad_reader = a1;
   p.nvme_valid = false;  // any NVMe replica of the parameter is now stale
   if (p.has_home) p.home_valid = false;
-  if (on_gpu) p.arrival = nullptr;
+  if (j.on_gpu) p.arrival = nullptr;
 
-  if (state_on_gpu) {
+  if (j.state_on_gpu) {
     slot_of(s).sync = SlotSync{a1, {}};
   } else {
     Slot& h = slot_of(s);
-    stage_sync_[b].readers.push_back(a1);
-    wait_for_read(d2h_opt_, stage_sync_[b]);
+    stage_sync_[j.b].readers.push_back(a1);
+    wait_for_read(d2h_opt_, stage_sync_[j.b]);
     wait_for_write(d2h_opt_, h.sync);
     TCB_CK(cudaStreamWaitEvent(d2h_opt_, a1, 0));
-    if (opt_yield_ && last_d2h_) TCB_CK(cudaStreamWaitEvent(d2h_opt_, last_d2h_, 0));
     tag_ = CopyTag{"opt_store", s.id, 0, 1};
-    cudaEvent_t e3 = copy(d2h_opt_, h.ptr, stg, s.bytes, false);
+    cudaEvent_t e3 = copy(d2h_opt_, h.ptr, j.stg, s.bytes, false);
     h.sync = SlotSync{e3, {}};
-    stage_sync_[b].readers.push_back(e3);
-    stage_free_.push_back(b);
+    stage_sync_[j.b].readers.push_back(e3);
+    stage_free_.push_back(j.b);
     stats_.opt_d2h_bytes += s.bytes;
   }
 
-  if (!on_gpu) {  // updated-parameter write-back to its home tier (category iii)
+  if (!j.on_gpu) {  // updated-parameter write-back to its home tier (category iii)
     tag_ = CopyTag{"writeback", p.id, 0, static_cast<std::uint8_t>(p.tier == PTier::Nvme ? 2 : 1)};
     if (p.tier == PTier::Nvme) {
       std::uint8_t* bb = bounce_.at(p.bytes);
@@ -203,14 +221,14 @@ void Executor::optimizer_work(TensorRec& s, TensorRec& p) {
       if (io_) {
         wait_for_write(d2h_opt_, bs);
         TCB_CK(cudaStreamWaitEvent(d2h_opt_, a1, 0));
-        cudaEvent_t e4 = copy(d2h_opt_, bb, pout, p.bytes, false);
-        psync->readers.push_back(e4);
+        cudaEvent_t e4 = copy(d2h_opt_, bb, j.pout, p.bytes, false);
+        j.psync->readers.push_back(e4);
         bs = SlotSync{e4, {}};
         nvme_write_async(p, bb, bs);
       } else {
         TCB_CK(cudaEventSynchronize(a1));
         host_wait_all(bs);
-        TCB_CK(cudaMemcpy(bb, pout, p.bytes, cudaMemcpyDeviceToHost));
+        TCB_CK(cudaMemcpy(bb, j.pout, p.bytes, cudaMemcpyDeviceToHost));
         bs = SlotSync{};
         nvme_write(p, bb);
       }
@@ -218,12 +236,54 @@ void Executor::optimizer_work(TensorRec& s, TensorRec& p) {
       Slot& ph = slot_of(p);
       wait_for_write(d2h_opt_, ph.sync);
       TCB_CK(cudaStreamWaitEvent(d2h_opt_, a1, 0));
-      cudaEvent_t e4 = copy(d2h_opt_, ph.ptr, pout, p.bytes, false);
+      cudaEvent_t e4 = copy(d2h_opt_, ph.ptr, j.pout, p.bytes, false);
       ph.sync = SlotSync{e4, {}};
-      psync->readers.push_back(e4);
+      j.psync->readers.push_back(e4);
     }
     stats_.writeback_bytes += p.bytes;
   }
+}
+
+void Executor::optimizer_work(TensorRec& s, TensorRec& p) {
+  std::vector<UpdateJob> one{prepare_update(s, p)};
+  run_updates(one);
+}
+
+// A hoisted update waits in the batch until adam_batch_ are ready or
+// anything could observe its results (a decision moving its tensors, an
+// in-place update, the end of the iteration): the data dependencies are all
+// event-based, so deferring within those bounds changes no result.
+void Executor::defer_update(TensorRec& s, TensorRec& p) {
+  deferred_.emplace_back(index_of(s.id), index_of(p.id));
+  if (deferred_.size() >= adam_batch_) flush_updates();
+}
+
+void Executor::flush_updates() {
+  if (deferred_.empty()) return;
+  std::vector<UpdateJob> jobs;
+  for (const auto& [si, pi] : deferred_) {
+    TensorRec& s = recs_[static_cast<std::size_t>(si)];
+    const bool needs_stage = s.tier == PTier::HostOpt && !staged_.count(si);
+    if (needs_stage && stage_free_.empty() && !jobs.empty()) {  // the batch so far frees its stages first
+      run_updates(jobs);
+      jobs.clear();
+    }
+    jobs.push_back(prepare_update(s, recs_[static_cast<std::size_t>(pi)]));
+  }
+  deferred_.clear();
+  run_updates(jobs);
+  if (so_.prestage) refill_stages(prestage_lookahead_ + adam_batch_);
+}
+
+// Flush before `reqs` run if any of them moves a tensor of a deferred update.
+void Executor::flush_if_touched(const std::vector<Req>& reqs) {
+  if (deferred_.empty()) return;
+  for (const Req& r : reqs)
+    for (const auto& [si, pi] : deferred_)
+      if (recs_[static_cast<std::size_t>(si)].id == r.tensor_id || recs_[static_cast<std::size_t>(pi)].id == r.tensor_id) {
+        flush_updates();
+        return;
+      }
 }
 
 // The whole iteration's decisions, made up front in the reference's call
@@ -383,10 +443,6 @@ void Executor::iteration_begin(const StepOptions& so, cudaStream_t compute, bool
   // states the prologue staged come first in the order: continue after them
   while (prestage_next_ < prestage_order_.size() && staged_.count(prestage_order_[prestage_next_])) ++prestage_next_;
   if (so_.prestage) {
-    // The forward refill of iteration t+1 is issued while iteration t's tail
-    // may still be moving; gated, it starts only after t's last cache
-    // prefetch so it never competes with t's critical H2D traffic.
-    if (prestage_gate_ && last_h2d_) TCB_CK(cudaStreamWaitEvent(h2d_opt_, last_h2d_, 0));
     refill_stages(prestage_fwd_override_ >= 0 ? static_cast<std::size_t>(prestage_fwd_override_)
                                               : forward_prestage_budget(it.hooks));
   }
@@ -412,24 +468,21 @@ std::vector<void*> Executor::step_begin(std::size_t i) {
                                    (it.in_step ? "step_end(" : "step_begin(") +
                                    std::to_string(it.in_step ? it.next - 1 : it.next) + ")");
   TCB_CK(cudaSetDevice(device_));
-  while (it.hk < it.hooks.size() && it.hooks[it.hk].kind == 2) execute(it.hooks[it.hk++].reqs);
+  while (it.hk < it.hooks.size() && it.hooks[it.hk].kind == 2) {
+    flush_updates();  // the restore point moves tensors wholesale
+    execute(it.hooks[it.hk++].reqs);
+  }
   if (it.hk >= it.hooks.size() || it.hooks[it.hk].kind != 0 || it.hooks[it.hk].step != i)
     throw DeviceError(TC_EINTERNAL, "step_begin: hook sequence out of step");
   const TraceStep& step = trace_.steps[i];
   if (step.phase != it.prev) {
     mark_phase();
-    if (it.prev == Phase::Forward && so_.prestage && edge_fill_) {
-      // Forward -> backward edge: the forward's cache prefetches are all
-      // issued and no backward prefetch exists yet, so the H2D link
-      // would idle until the first update frees a stage. Fill the rest
-      // of the ring, starting when the forward's last prefetch lands.
-      if (last_h2d_) TCB_CK(cudaStreamWaitEvent(h2d_opt_, last_h2d_, 0));
-      refill_stages(stage_.size());
-    }
     it.prev = step.phase;
   }
   nvtxRangePushA(step.phase == Phase::Forward ? "tencache.fwd" : step.phase == Phase::Backward ? "tencache.bwd"
                                                                                                : "tencache.opt");
+  if (step.phase == Phase::OptimizerUpdate) flush_updates();
+  flush_if_touched(it.hooks[it.hk].reqs);
   execute(it.hooks[it.hk++].reqs);
   it.in_step = true;
   ++it.next;
@@ -463,13 +516,13 @@ void Executor::step_end(std::size_t i) {
     param_exit(step, compute_, it.external);
     for (std::size_t j : it.after[i]) {
       TensorRec& s = rec(trace_.steps[j].tensor_ids.front());
-      optimizer_work(s, recs_[static_cast<std::size_t>(s.partner)]);
-      if (so_.prestage) refill_stages(prestage_lookahead_);
+      defer_update(s, recs_[static_cast<std::size_t>(s.partner)]);
     }
   }
   nvtxRangePop();
   if (it.hk >= it.hooks.size() || it.hooks[it.hk].kind != 1 || it.hooks[it.hk].step != i)
     throw DeviceError(TC_EINTERNAL, "step_end: hook sequence out of step");
+  flush_if_touched(it.hooks[it.hk].reqs);
   execute(it.hooks[it.hk++].reqs);
   it.in_step = false;
 }
@@ -481,6 +534,7 @@ void Executor::iteration_end() {
                                    " step(s) not run" + (open_->in_step ? " (a step is still open)" : ""));
   TCB_CK(cudaSetDevice(device_));
   OpenIter& it = *open_;
+  flush_updates();
   while (it.hk < it.hooks.size()) execute(it.hooks[it.hk++].reqs);  // restore point (if not yet), iteration end
   open_.reset();
   mark_phase();
@@ -497,6 +551,7 @@ void Executor::iteration_abort() {
     nvtxRangePop();
     open_->in_step = false;
   }
+  deferred_.clear();  // abandoned with the rest of the iteration's updates
   while (open_->hk < open_->hooks.size()) execute(open_->hooks[open_->hk++].reqs);
   open_.reset();
   mark_phase();
@@ -535,7 +590,6 @@ void Executor::prologue_next() {
   std::vector<Hook> hooks = decide_iteration();
   nvtxRangePop();
   set_prestage_order(hooks, plan_hoisting(hooks));
-  if (prestage_gate_ && last_h2d_) TCB_CK(cudaStreamWaitEvent(h2d_opt_, last_h2d_, 0));
   refill_stages(prestage_fwd_override_ >= 0 ? static_cast<std::size_t>(prestage_fwd_override_)
                                             : forward_prestage_budget(hooks));
   ahead_ = std::move(hooks);
@@ -724,8 +778,6 @@ void Executor::scrub(std::uint64_t gen) {
     if (r.grad_reader && events_.done_by(r.grad_reader, gen)) r.grad_reader = nullptr;
   }
   std::erase_if(barriers_, [&](cudaEvent_t e) { return events_.done_by(e, gen); });
-  if (last_h2d_ && events_.done_by(last_h2d_, gen)) last_h2d_ = nullptr;
-  if (last_d2h_ && events_.done_by(last_d2h_, gen)) last_d2h_ = nullptr;
 }
 
 void Executor::drain() {

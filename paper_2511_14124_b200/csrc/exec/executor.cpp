@@ -263,10 +263,7 @@ Executor::Executor(const std::string& trace_path, const std::string& machine_pat
     const char* nf = std::getenv("TC_NVME_FILES");
     nvme_ = std::make_unique<StripedFile>(dir, off, nf ? std::atoi(nf) : 16, opts.direct_io && all_aligned);
   }
-  if (const char* c = std::getenv("TC_OPT_YIELD")) opt_yield_ = std::atoi(c) != 0;
   if (const char* c = std::getenv("TC_PRESTAGE_FWD")) prestage_fwd_override_ = std::atoi(c);
-  if (const char* c = std::getenv("TC_PRESTAGE_GATE")) prestage_gate_ = std::atoi(c) != 0;
-  if (const char* c = std::getenv("TC_EDGE_FILL")) edge_fill_ = std::atoi(c) != 0;
   if (const char* c = std::getenv("TC_LOOKAHEAD")) lookahead_ = std::atoi(c) != 0;
   if (const char* c = std::getenv("TC_ADAM_STAMPS")) adam_stamps_ = std::atoi(c) != 0;
   {  // migration-bound? trace compute time vs the optimizer states' H2D time alone (machine.cpp:101-111)
@@ -312,8 +309,10 @@ Executor::Executor(const std::string& trace_path, const std::string& machine_pat
     stage_sync_.emplace_back();
     stage_free_.push_back(static_cast<std::size_t>(i));
   }
+  if (const char* c = std::getenv("TC_ADAM_BATCH"))
+    adam_batch_ = static_cast<std::size_t>(std::clamp(std::atoi(c), 1, kMaxAdamChunks));
   for (const auto& [size, _] : pclass) {
-    for (int i = 0; i < 2; ++i) {
+    for (std::size_t i = 0; i < std::max<std::size_t>(2, adam_batch_); ++i) {
       void* p = nullptr;
       TCB_CK(cudaMalloc(&p, size));
       pout_scratch_[size].push_back(static_cast<std::uint8_t*>(p));
@@ -348,8 +347,7 @@ Executor::Executor(const std::string& trace_path, const std::string& machine_pat
   TCB_CK(cudaStreamCreateWithFlags(&d2h_, cudaStreamNonBlocking));
   int lo_prio = 0, hi_prio = 0;  // the fused AdamW gets the highest stream priority
   TCB_CK(cudaDeviceGetStreamPriorityRange(&lo_prio, &hi_prio));
-  const char* op = std::getenv("TC_OPT_PRIORITY");  // diagnostic: 0 = default priority for the AdamW stream
-  TCB_CK(cudaStreamCreateWithPriority(&opt_, cudaStreamNonBlocking, (op && std::atoi(op) == 0) ? lo_prio : hi_prio));
+  TCB_CK(cudaStreamCreateWithPriority(&opt_, cudaStreamNonBlocking, hi_prio));
   TCB_CK(cudaStreamCreateWithFlags(&h2d_opt_, cudaStreamNonBlocking));
   TCB_CK(cudaStreamCreateWithFlags(&d2h_opt_, cudaStreamNonBlocking));
 
@@ -839,7 +837,6 @@ void Executor::apply(const Req& r) {
     throw DeviceError(TC_EINTERNAL, "unsupported transfer direction");
   }
   if (r.blocking && done) barriers_.push_back(done);
-  if (done && !r.instant) (r.dst == Tier::Gpu ? last_h2d_ : last_d2h_) = done;
 }
 
 void Executor::wait_barriers(cudaStream_t cs) {

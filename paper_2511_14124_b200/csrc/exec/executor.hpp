@@ -282,6 +282,24 @@ class Executor {
   std::optional<OpenIter> open_;
   void zero3_access(TensorRec& x, bool backward, cudaStream_t cs);
   void optimizer_work(TensorRec& s, TensorRec& p);
+  struct UpdateJob {
+    TensorRec* s = nullptr;
+    TensorRec* p = nullptr;
+    bool state_on_gpu = false, on_gpu = false;
+    std::uint64_t n = 0;
+    std::uint8_t* stg = nullptr;  // [p32 | m | v] in HBM (stage or GPU slot)
+    std::size_t b = 0;            // stage index (host-resident states)
+    std::uint8_t* pout = nullptr;  // bf16 result (the parameter's GPU slot or a scratch buffer)
+    SlotSync* psync = nullptr;
+  };
+  UpdateJob prepare_update(TensorRec& s, TensorRec& p);
+  void run_updates(std::vector<UpdateJob>& jobs);
+  void finish_update(UpdateJob& j, cudaEvent_t a1);
+  void defer_update(TensorRec& s, TensorRec& p);
+  void flush_updates();
+  void flush_if_touched(const std::vector<Req>& reqs);
+  std::vector<std::pair<std::int32_t, std::int32_t>> deferred_;  // hoisted updates waiting for a batch
+  std::size_t adam_batch_ = 4;  // TC_ADAM_BATCH: hoisted updates per fused AdamW launch (1..8)
   std::size_t stage_state(TensorRec& s);
   void refill_stages(std::size_t want_staged);
   std::size_t forward_prestage_budget(const std::vector<Hook>& hooks) const;
@@ -326,7 +344,6 @@ class Executor {
   std::size_t prestage_next_ = 0;
   std::size_t prestage_lookahead_ = 2;
   int prestage_fwd_override_ = -1;  // TC_PRESTAGE_FWD: states staged for the forward (-1: bandwidth model)
-  bool prestage_gate_ = false;      // TC_PRESTAGE_GATE: forward refill waits for the last cache prefetch
   bool adam_stamps_ = false;        // TC_ADAM_STAMPS: %globaltimer stamps around each AdamW (diagnostic)
   // Updates on the compute stream when the trace is migration-bound (the
   // compute stream idles on copies anyway, and a same-stream launch skips the
@@ -339,7 +356,6 @@ class Executor {
   double stamp_pre_ns_ = 0, stamp_post_ns_ = 0, stamps_ = 0;
   bool lookahead_ = true;           // TC_LOOKAHEAD: decide + pre-stage iteration t+1 at the end of t
   std::optional<std::vector<Hook>> ahead_;
-  bool edge_fill_ = false;          // TC_EDGE_FILL: fill the stage ring at the forward->backward edge (neutral on C2)
   std::uint64_t stage_bytes_ = 0;
   std::map<std::uint64_t, std::vector<std::uint8_t*>> pout_scratch_;  // HBM updated-param scratch
   std::map<std::uint64_t, std::vector<SlotSync>> pout_sync_;
@@ -358,8 +374,6 @@ class Executor {
   unsigned long long* d_span_ = nullptr;  // 2 parities x n_params x (min, max) AdamW kernel spans
   unsigned long long* span_base_ = nullptr;
   std::size_t span_cursor_ = 0;
-  bool opt_yield_ = false;                 // optimizer copies queue behind earlier decision copies (env TC_OPT_YIELD)
-  cudaEvent_t last_h2d_ = nullptr, last_d2h_ = nullptr;  // most recent decision copy per direction
   std::size_t n_accesses_ = 0, access_cursor_ = 0;
   std::unique_ptr<StripedFile> nvme_;  // NVMe tier backing files
   std::unique_ptr<NvmeQueue> io_;  // async NVMe tier I/O (null: synchronous fallback)

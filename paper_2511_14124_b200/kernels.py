@@ -75,9 +75,14 @@ def adamw_split(p32, m, v, grad, param_out, lr, beta1, beta2, eps, weight_decay,
                                    weight_decay, step, grad_scale, _stream(stream)))
 
 
-def set_adamw_variant(v):
-    """0 register-unrolled, 1 register-lean, 2 TMA bulk pipeline; returns previous."""
-    return N.lib().tc_set_adamw_variant(int(v))
+def adamw_batch(chunks, lr, beta1, beta2, eps, weight_decay, step, grad_scale=1.0, stream=None):
+    """One launch over up to 8 (state [3n], grad [n] bf16, param_out [n] bf16 or None) chunks."""
+    arr = (N.tc_adam_chunk * max(len(chunks), 1))()
+    for k, (st, g, po) in enumerate(chunks):
+        assert st.numel() == 3 * g.numel()
+        arr[k] = N.tc_adam_chunk(_dev(st), _dev(g), _dev(po) if po is not None else None, g.numel())
+    N.check(N.lib().tc_adamw_batch(arr, len(chunks), lr, beta1, beta2, eps, weight_decay, step, grad_scale,
+                                   _stream(stream)))
 
 
 def adamw_scalars(lr, beta1, beta2, eps, weight_decay, step):

@@ -98,7 +98,6 @@ def run_copy(name, background=None):
 
 run_copy("torch_copy_alone")
 run_copy("torch_copy_with_pcie_copies", copies)
-K.set_adamw_variant(int(os.environ.get("VARIANT", "2")))
 run("alone")
 run("with_h2d_only", lambda: copies(True, False))
 run("with_d2h_only", lambda: copies(False, True))
@@ -108,11 +107,6 @@ run("with_spin_1cta", spin)
 run("with_checksums", checksums)
 run("with_copies_spin", lambda: (copies(), spin()))
 run("with_copies_spin_b2b8", lambda: (copies(), spin()), back_to_back=8)
-for v in (0, 1, 4, 5):
-    K.set_adamw_variant(v)
-    run(f"v{v}_alone")
-    run(f"v{v}_with_pcie_copies", copies)
-K.set_adamw_variant(2)
 
 
 def run_graph(name, background=None):

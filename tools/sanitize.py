@@ -12,14 +12,14 @@ from paper_2511_14124_b200 import kernels as K  # noqa: E402
 from paper_2511_14124_b200 import traces as T  # noqa: E402
 from paper_2511_14124_b200.engine import Engine  # noqa: E402
 
-for v in range(6):
-    K.set_adamw_variant(v)
-    for n in (1, 9, 2048 * 2 + 8, 70001):
-        st = torch.rand(3 * n, device="cuda")
-        g = torch.rand(n, device="cuda").to(torch.bfloat16)
-        po = torch.empty(n, dtype=torch.bfloat16, device="cuda")
-        K.adamw(st, g, po, 1e-3, 0.9, 0.999, 1e-8, 0.01, 1)
-K.set_adamw_variant(2)
+for n in (1, 9, 2048 * 2 + 8, 70001):
+    st = torch.rand(3 * n, device="cuda")
+    g = torch.rand(n, device="cuda").to(torch.bfloat16)
+    po = torch.empty(n, dtype=torch.bfloat16, device="cuda")
+    K.adamw(st, g, po, 1e-3, 0.9, 0.999, 1e-8, 0.01, 1)
+chunks = [(torch.rand(3 * n, device="cuda"), torch.rand(n, device="cuda").to(torch.bfloat16),
+           torch.empty(n, dtype=torch.bfloat16, device="cuda")) for n in (8, 2048 * 3 + 16, 40)]
+K.adamw_batch(chunks, 1e-3, 0.9, 0.999, 1e-8, 0.01, 1)
 x = torch.randn(12345, device="cuda")
 K.cast_bf16_to_f32(K.cast_f32_to_bf16(x))
 src = torch.randint(0, 255, (1 << 20,), dtype=torch.uint8, device="cuda")
