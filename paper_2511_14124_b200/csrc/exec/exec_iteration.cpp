@@ -148,7 +148,7 @@ Executor::UpdateJob Executor::prepare_update(TensorRec& s, TensorRec& p) {
     Slot& g = slot_of(p);
     j.pout = g.ptr;
     j.psync = &g.sync;
-  } else {  // a ring of at least adam_batch_ scratch buffers: a batch never reuses one
+  } else {  // a ring of at least the batch size: a batch never reuses a buffer
     std::size_t& k = pout_next_[p.bytes];
     j.pout = pout_scratch_[p.bytes][k];
     j.psync = &pout_sync_[p.bytes][k];
@@ -249,13 +249,13 @@ void Executor::optimizer_work(TensorRec& s, TensorRec& p) {
   run_updates(one);
 }
 
-// A hoisted update waits in the batch until adam_batch_ are ready or
+// A hoisted update waits in the batch until adam_batch() are ready or
 // anything could observe its results (a decision moving its tensors, an
 // in-place update, the end of the iteration): the data dependencies are all
 // event-based, so deferring within those bounds changes no result.
 void Executor::defer_update(TensorRec& s, TensorRec& p) {
   deferred_.emplace_back(index_of(s.id), index_of(p.id));
-  if (deferred_.size() >= adam_batch_) flush_updates();
+  if (deferred_.size() >= adam_batch()) flush_updates();
 }
 
 void Executor::flush_updates() {
@@ -272,7 +272,7 @@ void Executor::flush_updates() {
   }
   deferred_.clear();
   run_updates(jobs);
-  if (so_.prestage) refill_stages(prestage_lookahead_ + adam_batch_);
+  if (so_.prestage) refill_stages(prestage_lookahead_ + adam_batch());
 }
 
 // Flush before `reqs` run if any of them moves a tensor of a deferred update.

@@ -310,9 +310,9 @@ Executor::Executor(const std::string& trace_path, const std::string& machine_pat
     stage_free_.push_back(static_cast<std::size_t>(i));
   }
   if (const char* c = std::getenv("TC_ADAM_BATCH"))
-    adam_batch_ = static_cast<std::size_t>(std::clamp(std::atoi(c), 1, kMaxAdamChunks));
+    adam_batch_env_ = static_cast<std::size_t>(std::clamp(std::atoi(c), 1, kMaxAdamChunks));
   for (const auto& [size, _] : pclass) {
-    for (std::size_t i = 0; i < std::max<std::size_t>(2, adam_batch_); ++i) {
+    for (std::size_t i = 0; i < std::max<std::size_t>({2, adam_batch_env_, kAdamBatchConcurrent}); ++i) {
       void* p = nullptr;
       TCB_CK(cudaMalloc(&p, size));
       pout_scratch_[size].push_back(static_cast<std::uint8_t*>(p));

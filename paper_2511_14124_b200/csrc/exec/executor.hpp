@@ -299,7 +299,16 @@ class Executor {
   void flush_updates();
   void flush_if_touched(const std::vector<Req>& reqs);
   std::vector<std::pair<std::int32_t, std::int32_t>> deferred_;  // hoisted updates waiting for a batch
-  std::size_t adam_batch_ = 4;  // TC_ADAM_BATCH: hoisted updates per fused AdamW launch (1..8)
+  // Hoisted updates per fused AdamW launch. On its own stream (compute-bound
+  // traces, ZeRO-3) each launch waits for SMs behind the concurrent layer
+  // compute and pays the front-end latency of a second stream: batches of 4
+  // amortise that (C3: event-timed 0.45 -> 0.71 of the HBM peak, step time
+  // unchanged). On the compute stream (migration-bound) single updates keep
+  // each state's write-back earliest (C2 steps 2-4 % shorter,
+  // profiles/r02_adam_batch_ab.json). TC_ADAM_BATCH overrides (1..8).
+  static constexpr std::size_t kAdamBatchConcurrent = 4;
+  std::size_t adam_batch_env_ = 0;
+  std::size_t adam_batch() const { return adam_batch_env_ ? adam_batch_env_ : adam_stream() == opt_ ? kAdamBatchConcurrent : 1; }
   std::size_t stage_state(TensorRec& s);
   void refill_stages(std::size_t want_staged);
   std::size_t forward_prestage_budget(const std::vector<Hook>& hooks) const;

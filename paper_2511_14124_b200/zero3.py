@@ -166,145 +166,3 @@ def bind_to_gpu_numa(dev: int) -> bool:
         pass
     return False
 
-
-def bench_rank(args):
-    """bench.py under torchrun (N>1, or --zero3): each rank runs its own
-    engine on its ZeRO-3 shard with the exchange inside the step; step time is
-    the max over ranks (CUDA events on each rank's compute stream).
-
-    --config c2 (default): OPT-1.3B — the N=1 workload, sharded (strong
-    scaling: the model and the global batch are fixed, each rank holds 1/N);
-    the GPU parameter tier is 40 % of the rank's chunks, every optimizer state
-    in pinned host memory. --config c3: Llama-2 7B with the whole shard on the
-    GPU (BASELINE configs[2]). More ranks than GPUs (a functional check on a
-    small box) share devices round-robin: gloo for the host-side collectives
-    and the fused peer-memory exchange (NCCL cannot put two ranks on one GPU);
-    timings are then not meaningful."""
-    import tempfile
-    import time
-
-    import torch
-    import torch.distributed as dist
-
-    from .engine import Engine
-    from . import policy as P
-
-    rank, world = int(os.environ.get("RANK", 0)), int(os.environ.get("WORLD_SIZE", 1))
-    local = int(os.environ.get("LOCAL_RANK", rank))
-    os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
-    os.environ.setdefault("MASTER_PORT", "29517")
-    os.environ.setdefault("RANK", str(rank))
-    os.environ.setdefault("WORLD_SIZE", str(world))
-    ndev = max(1, torch.cuda.device_count())
-    dev = local % ndev
-    shared = world > ndev
-    torch.cuda.set_device(dev)
-    if not shared:
-        bind_to_gpu_numa(dev)
-    if shared:
-        dist.init_process_group("gloo")
-        exchange = "p2p"
-    else:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", dev))
-        exchange = args.exchange
-    red_dev = "cpu" if shared else "cuda"
-
-    def reduce(x, op):
-        t = torch.tensor([float(x)], dtype=torch.float64, device=red_dev)
-        dist.all_reduce(t, op=op)
-        return float(t.item())
-
-    model = "llama2-7b" if args.config == "c3" else "opt-1.3b"
-    layout = shard_layout(model, world)
-    wd = tempfile.mkdtemp(dir="/dev/shm" if os.path.isdir("/dev/shm") else None)
-    tp = os.path.join(wd, f"r{rank}.jsonl")
-    write_rank_trace(tp, layout, rank, tokens=args.tokens, effective_tflops=args.tflops)
-    n, S = layout.chunks_per_rank, layout.chunk_bytes
-    g = n if args.config == "c3" else int(0.4 * n)
-    mp = T.write_machine(os.path.join(wd, "m.json"), g * S, (n - g) * S + n * 6 * S + 1,
-                         pinned_overrides={"cpu->gpu": args.pcie_h2d, "gpu->cpu": args.pcie_d2h})
-    cfg = {"policy": "tencache"}
-    rep = P.run(tp, mp, cfg)
-    dec_bytes = sum(rep["transfer_bytes"].values())
-    eng = Engine(tp, mp, cfg, device=dev, nvme_dir=wd, opt_stage_slots=args.stages,
-                 gpu_spare_slots=args.gpu_spares)
-    eng.seed(rank)
-    enable(eng, layout, rank, world, exchange=exchange)
-    stream = torch.cuda.current_stream()
-    kw = dict(lr=1e-4, compute_mode=1 if args.compute == "spin" else 0, stream=stream.cuda_stream)
-    for _ in range(args.warmup):
-        eng.iteration(**kw)
-    eng.reset_stats()
-    x0 = exchanged_bytes(eng)
-    dist.barrier()
-    torch.cuda.synchronize()
-    clock_cls = getattr(args, "clock_sampler", None)
-    clk = clock_cls(dev) if (clock_cls is not None and rank == 0) else None
-    if clk:
-        clk.__enter__()
-    s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    s.record(stream)
-    for k in range(args.steps):
-        eng.iteration(last=k == args.steps - 1, **kw)
-    eng.sync()
-    e.record(stream)
-    torch.cuda.synchronize()
-    if clk:
-        clk.__exit__(None, None, None)
-    ms = reduce(s.elapsed_time(e) / args.steps, dist.ReduceOp.MAX)
-    st = eng.stats()
-    per_rank = dec_bytes if args.config != "c3" else (st["opt_h2d_bytes"] + st["opt_d2h_bytes"]) / args.steps
-    total = reduce(per_rank, dist.ReduceOp.SUM)
-    xb = (exchanged_bytes(eng) - x0) / args.steps
-    launches = max(1, n * args.steps)  # every state chunk of the shard is updated once per step
-    adam_us = reduce(st["adam_ms"] * 1e3 / launches, dist.ReduceOp.MAX)
-    adam_elems = st["adam_elems"] / launches
-    # e2e through the public API: per step the rank's input batch goes H2D from
-    # pinned host memory and the step's result (per-access checksums) comes back.
-    tok_h = torch.randint(0, 50000, (max(1, args.tokens // world),), dtype=torch.int32).pin_memory()
-    tok_d = torch.empty_like(tok_h, device="cuda")
-    e2e_steps = args.steps
-    dist.barrier()
-    t0 = time.perf_counter()
-    for k in range(e2e_steps):
-        tok_d.copy_(tok_h, non_blocking=True)
-        eng.iteration(last=k == e2e_steps - 1, **kw)
-        cks = eng.step_result()
-    eng.sync()  # the last step's write-back tail (incl. NVMe writes) is part of the step
-    torch.cuda.synchronize()
-    e2e_ms = reduce((time.perf_counter() - t0) * 1e3 / e2e_steps, dist.ReduceOp.MAX)
-    line = None
-    if rank == 0:
-        hbm = getattr(args, "hbm_peak", None) or 6554.9
-        achieved = 28 * adam_elems / (adam_us * 1e-6) / 1e9 if adam_us else 0.0
-        line = {"metric": "step time & migrated GB/s per GPU vs PCIe roofline; GPU cache hit rate",
-                "value": round(total / (ms * 1e-3) / 1e9, 4), "unit": "GB/s", "n_gpus": world,
-                "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms, 3), "higher_is_better": True,
-                "scaling": "strong", "vs_baseline": None, "dtype": "bf16/fp32", "data": "synthetic",
-                "config": {"workload": (f"{model} ZeRO-3 over {world} GPU(s), per-rank engine, per-chunk-access "
-                                        + ("fused peer-memory gather+unpack / pull-reduce kernels"
-                                           if exchange == "p2p" else "NCCL all-gather / reduce-scatter")
-                                        + ", optimizer states in pinned host memory"
-                                        + (f" [{world} ranks sharing {ndev} GPU(s): functional run, timings not "
-                                           "meaningful]" if shared else "")),
-                           "trace_of": model, "chunks_per_rank": n, "gpu_chunks_per_rank": g, "chunk_bytes": S,
-                           "parallelism": f"zero3 x{world}", "exchange": exchange,
-                           "l2": "inputs larger than L2 (GBs streamed per step)"},
-                "value_definition": ("sum over ranks of cache-decision bytes per step / max-over-ranks step time"
-                                     if args.config != "c3" else
-                                     "sum over ranks of optimizer-state PCIe bytes per step / step time"),
-                "exchange_bytes_per_step_per_rank": int(xb),
-                "hit_rate": {"exact_rank0": rep["hit_rate"]}, "gpu_launches": int(st["kernel_launches"]),
-                "roofline": {"kernel": "fused AdamW (adamw_tma_kernel<256,3>)", "bound": "hbm",
-                             "achieved": round(achieved, 1), "peak": hbm, "unit": "GB/s",
-                             "frac": round(achieved / hbm, 4), "traffic": None,
-                             "avg_launch_us": round(adam_us, 2), "note": "max over ranks of the event-timed "
-                                                                        "average launch on each rank's opt stream"},
-                "e2e": {"value": round(total / (e2e_ms * 1e-3) / 1e9, 4), "unit": "GB/s",
-                        "ms_per_step": round(e2e_ms, 3), "h2d_bytes_per_step": int(tok_h.numel() * 4 * world),
-                        "d2h_bytes_per_step": int(len(cks) * 8 * world)}}
-        if clk:
-            line["clocks"] = clk.summary()
-    eng.close()
-    dist.destroy_process_group()
-    return line
