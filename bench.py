@@ -47,6 +47,9 @@ sys.path.insert(0, ROOT)
 
 METRIC = "step time & migrated GB/s per GPU vs PCIe roofline; GPU cache hit rate"
 ADAM_BYTES_PER_ELEM = 28  # read p32,m,v (12) + g bf16 (2); write p32,m,v (12) + p bf16 (2)
+# split-master states (tc_adamw_split_master): read lo (2) + round bit (1/8) + bf16 param (2) + m,v (8) + g (2);
+# write lo (2) + round bit (1/8) + param (2) + m,v (8)
+ADAM_SPLIT_BYTES_PER_ELEM = 26.25
 WORKLOADS = {
     "c2": "C2: OPT-1.3B offloaded training step, GPU->pinned-CPU tier, size-class buffer reuse (BASELINE.json "
           "configs[1])",
@@ -240,7 +243,8 @@ def run_ours(args, name, secondary=False):
     W = workload_bytes(rep, info["trace"])
     t0 = time.perf_counter()
     eng = Engine(info["trace"], info["machine"], cfg, device=dev, nvme_dir=info["nvme_dir"], direct_io=args.direct_io,
-                 opt_stage_slots=args.stages, gpu_spare_slots=args.gpu_spares, host_spare_slots=args.host_spares)
+                 opt_stage_slots=args.stages, gpu_spare_slots=args.gpu_spares, host_spare_slots=args.host_spares,
+                 full_master=args.full_master)
     t_create = time.perf_counter() - t0
     eng.seed(rank)
     t_seed = time.perf_counter() - t0 - t_create
@@ -326,8 +330,10 @@ def run_ours(args, name, secondary=False):
     if rank == 0:
         pk = peaks()
         hbm = pk.get("hbm_gbs", 6650.0)
-        achieved = ADAM_BYTES_PER_ELEM * elems_per_launch / (adam_us * 1e-6) / 1e9 if adam_us else 0.0
-        traffic = dram_traffic(elems_per_launch)
+        split_share = st["split_elems"] / st["adam_elems"] if st["adam_elems"] else 0.0
+        bpe = ADAM_BYTES_PER_ELEM * (1 - split_share) + ADAM_SPLIT_BYTES_PER_ELEM * split_share
+        achieved = bpe * elems_per_launch / (adam_us * 1e-6) / 1e9 if adam_us else 0.0
+        traffic = dram_traffic(elems_per_launch, bpe)
         line = {
             "metric": METRIC, "value": round(W_total / (ms * 1e-3) / 1e9, 4), "unit": "GB/s", "n_gpus": world,
             "steps": K, "warmup": args.warmup, "ms_per_step": round(ms, 3), "higher_is_better": True,
@@ -371,10 +377,11 @@ def run_ours(args, name, secondary=False):
                          "achieved": round(achieved, 1), "peak": hbm, "unit": "GB/s", "frac": round(achieved / hbm, 4),
                          "traffic": traffic,
                          "frac_dram": (round(traffic / (adam_us * 1e-6) / 1e9 / hbm, 4) if traffic and adam_us else None),
-                         "algorithmic_bytes_per_launch": int(ADAM_BYTES_PER_ELEM * elems_per_launch),
+                         "algorithmic_bytes_per_launch": int(bpe * elems_per_launch),
+                         "algorithmic_bytes_per_elem": round(bpe, 3),
                          "avg_launch_us": round(adam_us, 2), "launches_per_step_rank0": round(launches / K, 1),
                          "resident_span": ({"avg_us": round(st["adam_span_ms"] * 1e3 / st["adam_spans"], 2),
-                                            "achieved": round(ADAM_BYTES_PER_ELEM * st["adam_elems"] /
+                                            "achieved": round(bpe * st["adam_elems"] /
                                                               (st["adam_span_ms"] * 1e-3) / 1e9, 1)}
                                            if st["adam_spans"] else None),
                          "peak_source": "MEASURED_PEAKS.json hbm_gbs (burst copy)",
@@ -384,6 +391,16 @@ def run_ours(args, name, secondary=False):
             "e2e": {"value": round(W_total / (e2e_ms * 1e-3) / 1e9, 4), "unit": "GB/s", "ms_per_step": round(e2e_ms, 3),
                     "h2d_bytes_per_step": int(tokens_h.numel() * 4 * world), "d2h_bytes_per_step": int(len(cks) * 8 * world),
                     "path": "Engine.iteration (ctypes C-ABI tc_engine_iteration) + step_result, host wall clock"},
+            "state_codec": {
+                "split_master": not args.full_master,
+                "split_updates_per_step_rank0": st["split_updates"] // K,
+                "opt_bytes_per_step_rank0": {"logical_12B_per_param": st["opt_logical_bytes"] // K,
+                                             "over_pcie": (st["opt_h2d_bytes"] + st["opt_d2h_bytes"]) // K},
+                "note": "optimizer states whose parameter never lives in NVMe cross PCIe as the fp32 master's low "
+                        "half + a round bit + m + v (10.125 B/param each way instead of 12): the high half is the "
+                        "bf16 parameter the update itself rounds from the master (lossless, bit-exact; "
+                        "tests/test_split_master_gpu.py). W (the value numerator) keeps the full 12 B/param, "
+                        "the PCIe fractions use the bytes that crossed the link"},
             "gpu_launches": int(launches_total),
             "setup_s": round(setup_s, 2),
             "setup_breakdown_s": {"engine_create_pin_and_carve": round(t_create, 2), "seed": round(t_seed, 2)},
@@ -435,11 +452,11 @@ def nvlink_peer_peak(dev, ndev):
         return None
 
 
-def dram_traffic(elems_per_launch):
+def dram_traffic(elems_per_launch, bytes_per_elem=ADAM_BYTES_PER_ELEM):
     tf = os.path.join(ROOT, "profiles", "adamw_dram_bytes.json")
     try:  # ncu --set full capture of one launch, scaled to this config's launch size
         tj = json.load(open(tf))
-        return int(tj["dram_bytes_per_launch"] * ADAM_BYTES_PER_ELEM * elems_per_launch /
+        return int(tj["dram_bytes_per_launch"] * bytes_per_elem * elems_per_launch /
                    tj["algorithmic_bytes_per_launch"])
     except Exception:
         return None
@@ -688,6 +705,8 @@ def main():
                     help="cache policy on the same executor (the paper's baselines for comparison)")
     ap.add_argument("--nvme-dir", default="/tmp", help="directory of the NVMe tier files (c4)")
     ap.add_argument("--direct-io", action="store_true", help="O_DIRECT NVMe tier I/O")
+    ap.add_argument("--full-master", action="store_true",
+                    help="keep the whole fp32 master in host memory (12 B/param each way; default: split master)")
     ap.add_argument("--cpu-state-fraction", type=float, default=0.6,
                     help="c4: share of the rank's optimizer states the CPU tier holds (the rest in NVMe); "
                          "1.0 = the 13B ZeRO-3 rank with every state in pinned host memory")

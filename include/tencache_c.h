@@ -157,6 +157,26 @@ typedef struct {
 } tc_adam_chunk;
 int tc_adamw_batch(const tc_adam_chunk* chunks, uint32_t count, double lr, double beta1, double beta2, double eps,
                    double weight_decay, int64_t step, float grad_scale, void* stream);
+/* Split-master optimizer state (what the engine keeps on the host for a
+ * parameter that never leaves HBM): n % 2048 == 0 elements laid out as
+ * [lo: u16 x n][rb: n/8 bytes][m: f32 x n][v: f32 x n] = tc_split_state_bytes(n)
+ * = 10.125 n bytes instead of the full 12 n. The fp32 master is
+ * (hi << 16) | lo with hi = the bf16 parameter B minus the round bit rb_i
+ * (for a NaN B: B with its quiet bit cleared when rb_i is set) -- exact for
+ * every fp32 value, because the update writes B = RNE(master) itself.
+ * tc_adamw_split_master updates such a state in place, reading the current
+ * `param` (bf16, n) and writing the new one; results are bit-identical to
+ * tc_adamw on the expanded state (same arithmetic). */
+uint64_t tc_split_state_bytes(uint64_t n);
+int tc_adamw_split_master(void* split_state, const void* grad, void* param, uint64_t n, double lr, double beta1,
+                          double beta2, double eps, double weight_decay, int64_t step, float grad_scale,
+                          void* stream);
+/* Codec between the split and the full [p32|m|v] layouts (device buffers,
+ * out of place). compress sets *d_mismatch (a device u32, never cleared) to
+ * nonzero when some p32 does not round to its bf16 param: not representable. */
+int tc_state_expand(const void* split_state, const void* param, float* full_state, uint64_t n, void* stream);
+int tc_state_compress(const float* full_state, const void* param, void* split_state, uint64_t n,
+                      uint32_t* d_mismatch, void* stream);
 /* The 8 fp32 scalars the update uses, for parity tests. */
 int tc_adamw_scalars(double lr, double beta1, double beta2, double eps, double weight_decay, int64_t step,
                      float out[8]);
@@ -249,6 +269,12 @@ typedef struct {
                               forward pass's spare H2D time (at least 12) */
   int direct_io;           /* O_DIRECT for the NVMe tier */
   uint64_t grad_bytes_per_param_byte; /* gradient bytes per bf16 param byte (1) */
+  int full_master;         /* nonzero: host optimizer states keep the whole fp32 master (12 B/param each
+                              way). 0 (default): a state whose parameter never leaves HBM keeps only the
+                              master's low half + a round bit on the host (10.125 B/param each way): the
+                              high half is the parameter's bf16 value, which the update rounds from it.
+                              Lossless; states read/written through tc_engine_read/write_tensor in the
+                              full [p32|m|v] layout either way. */
 } tc_engine_options;
 
 int tc_engine_create(const char* trace_path, const char* machine_path, const char* cfg_json,
@@ -357,6 +383,9 @@ typedef struct {
   uint64_t adam_launches;                /* fused AdamW kernel launches (one may cover several chunks) */
   uint64_t compute_gemms;                /* stand-in GEMM launches (compute_mode 2) */
   double compute_flops;                  /* stand-in GEMM FLOPs issued */
+  uint64_t split_updates;                /* updates of states held split (full_master = 0) */
+  uint64_t split_elems;                  /* ... their elements (part of adam_elems) */
+  uint64_t opt_logical_bytes;            /* optimizer round trip in the full 12 B/param layout, both ways */
 } tc_engine_stats;
 
 int tc_engine_stats_get(tc_engine* e, tc_engine_stats* out);

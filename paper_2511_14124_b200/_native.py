@@ -63,7 +63,7 @@ class tc_adam_chunk(C.Structure):
 class tc_engine_options(C.Structure):
     _fields_ = [("device", C.c_int), ("nvme_dir", C.c_char_p), ("gpu_spare_slots", C.c_int),
                 ("host_spare_slots", C.c_int), ("opt_stage_slots", C.c_int), ("direct_io", C.c_int),
-                ("grad_bytes_per_param_byte", C.c_uint64)]
+                ("grad_bytes_per_param_byte", C.c_uint64), ("full_master", C.c_int)]
 
 
 class tc_step_options(C.Structure):
@@ -79,7 +79,8 @@ class tc_engine_stats(C.Structure):
                                           "kernel_launches", "copies")] + \
               [(n, C.c_double) for n in ("h2d_busy_ms", "d2h_busy_ms", "stall_ms", "adam_ms")] + \
               [("adam_elems", C.c_uint64), ("adam_span_ms", C.c_double), ("adam_spans", C.c_uint64),
-               ("adam_launches", C.c_uint64), ("compute_gemms", C.c_uint64), ("compute_flops", C.c_double)]
+               ("adam_launches", C.c_uint64), ("compute_gemms", C.c_uint64), ("compute_flops", C.c_double),
+               ("split_updates", C.c_uint64), ("split_elems", C.c_uint64), ("opt_logical_bytes", C.c_uint64)]
 
     def as_dict(self):
         return {n: getattr(self, n) for n, _ in self._fields_}
@@ -122,6 +123,11 @@ _SIGS = {
     "tc_adamw_split": ([C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_uint64, C.c_double,
                         C.c_double, C.c_double, C.c_double, C.c_double, C.c_int64, C.c_float, C.c_void_p], C.c_int),
     "tc_adamw_batch": ([C.c_void_p, C.c_uint32] + [C.c_double] * 5 + [C.c_int64, C.c_float, C.c_void_p], C.c_int),
+    "tc_split_state_bytes": ([C.c_uint64], C.c_uint64),
+    "tc_adamw_split_master": ([C.c_void_p, C.c_void_p, C.c_void_p, C.c_uint64] + [C.c_double] * 5 +
+                              [C.c_int64, C.c_float, C.c_void_p], C.c_int),
+    "tc_state_expand": ([C.c_void_p, C.c_void_p, C.c_void_p, C.c_uint64, C.c_void_p], C.c_int),
+    "tc_state_compress": ([C.c_void_p, C.c_void_p, C.c_void_p, C.c_uint64, C.c_void_p, C.c_void_p], C.c_int),
     "tc_adamw_scalars": ([C.c_double] * 5 + [C.c_int64, C.POINTER(C.c_float)], C.c_int),
     "tc_checksum": ([C.c_void_p, C.c_uint64, C.c_void_p, C.c_void_p], C.c_int),
     "tc_spin": ([C.c_double, C.c_int, C.c_void_p], C.c_int),

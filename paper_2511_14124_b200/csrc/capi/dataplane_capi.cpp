@@ -125,6 +125,45 @@ int tc_adamw_batch(const tc_adam_chunk* chunks, uint32_t count, double lr, doubl
   return cuda_status(e, "tc_adamw_batch");
 }
 
+uint64_t tc_split_state_bytes(uint64_t n) { return split_layout(n).bytes; }
+
+int tc_adamw_split_master(void* split_state, const void* grad, void* param, uint64_t n, double lr, double beta1,
+                          double beta2, double eps, double weight_decay, int64_t step, float grad_scale,
+                          void* stream) {
+  if (step < 1) return set_error(TC_EARG, "tc_adamw_split_master: step must be >= 1");
+  if (n % kSplitTile) return set_error(TC_EARG, "tc_adamw_split_master: n must be a multiple of 2048");
+  if (n == 0) return TC_OK;
+  if (!split_state || !grad || !param) return set_error(TC_EARG, "tc_adamw_split_master: null buffer");
+  auto* b = static_cast<std::uint8_t*>(split_state);
+  const SplitLayout L = split_layout(n);
+  AdamChunk c{nullptr, reinterpret_cast<float*>(b + L.m), reinterpret_cast<float*>(b + L.v),
+              static_cast<const std::uint16_t*>(grad), static_cast<std::uint16_t*>(param), n,
+              reinterpret_cast<std::uint16_t*>(b + L.lo), reinterpret_cast<std::uint32_t*>(b + L.rb)};
+  const cudaError_t e = launch_adamw_batch(&c, 1, adam_scalars(lr, beta1, beta2, eps, weight_decay, step), grad_scale,
+                                           as_stream(stream));
+  if (e == cudaErrorInvalidValue) {
+    cudaGetLastError();
+    return set_error(TC_EARG, "tc_adamw_split_master: buffers must be 16-byte aligned");
+  }
+  return cuda_status(e, "tc_adamw_split_master");
+}
+
+int tc_state_expand(const void* split_state, const void* param, float* full_state, uint64_t n, void* stream) {
+  if (n % kSplitTile) return set_error(TC_EARG, "tc_state_expand: n must be a multiple of 2048");
+  return cuda_status(launch_state_expand(static_cast<const std::uint8_t*>(split_state),
+                                         static_cast<const std::uint16_t*>(param), full_state, n, as_stream(stream)),
+                     "tc_state_expand");
+}
+
+int tc_state_compress(const float* full_state, const void* param, void* split_state, uint64_t n,
+                      uint32_t* d_mismatch, void* stream) {
+  if (n % kSplitTile || d_mismatch == nullptr)
+    return set_error(TC_EARG, "tc_state_compress: n must be a multiple of 2048 and d_mismatch non-null");
+  return cuda_status(launch_state_compress(full_state, static_cast<const std::uint16_t*>(param),
+                                           static_cast<std::uint8_t*>(split_state), n, d_mismatch, as_stream(stream)),
+                     "tc_state_compress");
+}
+
 int tc_adamw_scalars(double lr, double beta1, double beta2, double eps, double weight_decay, int64_t step,
                      float out[8]) {
   const AdamScalars s = adam_scalars(lr, beta1, beta2, eps, weight_decay, step);

@@ -19,6 +19,14 @@ AdamScalars adam_scalars(double lr, double b1, double b2, double eps, double wd,
 
 // One chunk of a batched AdamW launch: n elements (a multiple of 8) at
 // 16-byte aligned addresses; pout may be null.
+//
+// Split-master chunks (lo != null; n a multiple of kSplitTile): the fp32
+// master is not stored whole. Its high half is the bf16 parameter at `pout`
+// (the update's own RNE output, kept in HBM) up to one rounding step, so the
+// state carries only the low half `lo` (u16) and one round bit per element in
+// `rb` (bit i of word i/32): H = B - rb for a non-NaN B, H = rb ? B & ~0x40 : B
+// for a NaN B (the cast sets the quiet bit). Exact for every fp32 value; the
+// kernel reads (lo, rb, B) and writes (lo', rb', B'). p is unused.
 struct AdamChunk {
   float* p;
   float* m;
@@ -26,7 +34,25 @@ struct AdamChunk {
   const std::uint16_t* g;
   std::uint16_t* pout;
   std::uint64_t n;
+  std::uint16_t* lo = nullptr;
+  std::uint32_t* rb = nullptr;
 };
+constexpr std::uint64_t kSplitTile = 2048;  // elements per AdamW tile; split chunks hold whole tiles
+
+// Layout of a split state chunk of n parameters (n % kSplitTile == 0) inside
+// the state's 12n-byte slot: [lo: 2n][rb: n/8][m: 4n][v: 4n] — 10.125n bytes,
+// the prefix that crosses PCIe.
+struct SplitLayout {
+  std::uint64_t n, lo, rb, m, v, bytes;
+};
+#ifdef __CUDACC__
+#define TCB_HD __host__ __device__
+#else
+#define TCB_HD
+#endif
+TCB_HD inline SplitLayout split_layout(std::uint64_t n) {
+  return SplitLayout{n, 0, 2 * n, 2 * n + n / 8, 2 * n + n / 8 + 4 * n, 2 * n + n / 8 + 8 * n};
+}
 constexpr int kMaxAdamChunks = 8;
 struct AdamBatch {  // kernel parameter: the chunks and their first tile in the launch's tile space
   AdamChunk chunk[kMaxAdamChunks];
@@ -64,6 +90,15 @@ cudaError_t launch_fill_normal_bf16(std::uint16_t* out, std::uint64_t n, float s
                                     std::uint64_t stream_id, cudaStream_t st);
 // Optimizer-state init from bf16 params: p32 = float(param), m = v = 0.
 cudaError_t launch_init_state(const std::uint16_t* param, float* state, std::uint64_t n, cudaStream_t st);
+// Split-master codec (layout above), out of place, n % kSplitTile == 0:
+// expand: [lo|rb|m|v] + bf16 params -> full [p32|m|v];
+// compress: full + bf16 params -> [lo|rb|m|v]; *mismatch (device word, set
+// to nonzero, never cleared) when some p32 does not round to its bf16 param,
+// i.e. the state is not representable split.
+cudaError_t launch_state_expand(const std::uint8_t* split, const std::uint16_t* param, float* full, std::uint64_t n,
+                                cudaStream_t st);
+cudaError_t launch_state_compress(const float* full, const std::uint16_t* param, std::uint8_t* split, std::uint64_t n,
+                                  unsigned* mismatch, cudaStream_t st);
 
 int num_sms();
 

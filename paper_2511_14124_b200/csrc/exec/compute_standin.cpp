@@ -108,6 +108,7 @@ GemmStandin::GemmStandin(int device, std::uint64_t chunk_bytes, double max_us) :
     best = std::min(best, ms);
   }
   tflops_ = 2.0 * max_m_ * K_ * static_cast<double>(N_) / (best * 1e-3) / 1e12;
+  rate_tflops_ = tflops_;
   cudaEventDestroy(e0);
   cudaEventDestroy(e1);
   cudaStreamDestroy(s);
@@ -118,6 +119,12 @@ GemmStandin::GemmStandin(int device, std::uint64_t chunk_bytes, double max_us) :
 
 GemmStandin::~GemmStandin() {
   cudaSetDevice(device_);
+  for (const Sample& s : inflight_) {
+    cudaEventSynchronize(s.e1);
+    cudaEventDestroy(s.e0);
+    cudaEventDestroy(s.e1);
+  }
+  for (cudaEvent_t e : spare_events_) cudaEventDestroy(e);
   if (handle_) cublas().Destroy(static_cast<cublasHandle_t>(handle_));
   for (void* p : {x_, y_, ws_})
     if (p) cudaFree(p);
@@ -135,22 +142,72 @@ void GemmStandin::gemm(cudaStream_t s, const void* w, int M) {
   flops_ += 2.0 * M * K_ * static_cast<double>(N_);
 }
 
-// The FLOPs that occupy the GPU for `us` at the calibrated rate, in GEMMs of
-// at most max_M rows (multiples of 64, at least 64).
+cudaEvent_t GemmStandin::event() {
+  if (!spare_events_.empty()) {
+    cudaEvent_t e = spare_events_.front();
+    spare_events_.pop_front();
+    return e;
+  }
+  cudaEvent_t e = nullptr;
+  ck(cudaEventCreate(&e), "cudaEventCreate");
+  return e;
+}
+
+// Fold completed steps into the rate window (the last 256 steps); block on
+// the oldest only when too many are in flight.
+void GemmStandin::poll(bool block_oldest) {
+  constexpr std::size_t kWindow = 256, kMaxInflight = 4096;
+  while (!inflight_.empty()) {
+    Sample& f = inflight_.front();
+    if (block_oldest && inflight_.size() > kMaxInflight) ck(cudaEventSynchronize(f.e1), "cudaEventSynchronize");
+    const cudaError_t q = cudaEventQuery(f.e1);
+    if (q == cudaErrorNotReady) break;
+    ck(q, "cudaEventQuery");
+    float ms = 0;
+    ck(cudaEventElapsedTime(&ms, f.e0, f.e1), "cudaEventElapsedTime");
+    if (ms > 0) {
+      window_.emplace_back(f.flops, ms * 1e-3);
+      win_flops_ += f.flops;
+      win_s_ += ms * 1e-3;
+      while (window_.size() > kWindow) {
+        win_flops_ -= window_.front().first;
+        win_s_ -= window_.front().second;
+        window_.pop_front();
+      }
+    }
+    spare_events_.push_back(f.e0);
+    spare_events_.push_back(f.e1);
+    inflight_.pop_front();
+  }
+  if (window_.size() >= 8 && win_s_ > 0) rate_tflops_ = win_flops_ / win_s_ / 1e12;
+}
+
+// The FLOPs that occupy the GPU for `us` at the rate measured under load, in
+// GEMMs of at most max_M rows (multiples of 64, at least 64).
 int GemmStandin::run(cudaStream_t s, const void* weights, double us) {
   if (us <= 0) return 0;
+  poll(true);
   const double per_row = 2.0 * K_ * static_cast<double>(N_);
-  const double rows = us * 1e-6 * tflops_ * 1e12 / per_row;
+  const double rows = us * 1e-6 * rate_tflops_ * 1e12 / per_row;
   const int n = std::max(1, static_cast<int>(std::ceil(rows / max_m_)));
   const int M = std::clamp(static_cast<int>(std::lround(rows / n / 64.0)) * 64, 64, max_m_);
+  Sample smp{event(), event(), 0.0};
+  ck(cudaEventRecord(smp.e0, s), "cudaEventRecord");
+  const double f0 = flops_;
   for (int i = 0; i < n; ++i) gemm(s, weights, M);
+  ck(cudaEventRecord(smp.e1, s), "cudaEventRecord");
+  smp.flops = flops_ - f0;
+  inflight_.push_back(smp);
   return n;
 }
 
 std::string GemmStandin::describe() const {
   return "{\"kind\":\"cuBLAS bf16 GEMM, fp32 accumulate: Y[M,N] = X[M,K] * W[K,N], W = the migrated chunk\","
          "\"K\":" + std::to_string(K_) + ",\"N\":" + std::to_string(N_) + ",\"max_M\":" + std::to_string(max_m_) +
-         ",\"calibrated_tflops_alone\":" + std::to_string(tflops_) + "}";
+         ",\"calibrated_tflops_alone\":" + std::to_string(tflops_) +
+         ",\"tflops_under_load\":" + std::to_string(rate_tflops_) +
+         ",\"sizing\":\"closed loop: each step's GEMM rows = compute_us x the GEMM rate measured in this run "
+         "(CUDA events, last 256 steps)\"}";
 }
 
 }  // namespace tcb

@@ -6,9 +6,17 @@
 // overlap and the in-step AdamW are measured under contention (a nanosleep
 // spin occupies nothing). cuBLAS (a plain library GEMM) is loaded at run
 // time by soname, so the process shares torch's copy when one is loaded.
+//
+// Closed loop: the rows per step come from the GEMM rate measured in the run
+// itself (CUDA events around each step's GEMMs, read back without blocking a
+// few steps later), not from the rate alone at full clocks. Under concurrent
+// PCIe DMA, the AdamW kernels and the power cap that dense GEMMs drive the
+// B200 into, the alone rate would overshoot compute_us by ~30 %; the loop
+// keeps the GPU busy for the modelled compute_us.
 #pragma once
 
 #include <cstdint>
+#include <deque>
 #include <string>
 
 #include <cuda_runtime.h>
@@ -27,6 +35,7 @@ class GemmStandin {
   int run(cudaStream_t s, const void* weights, double us);
   double flops_issued() const { return flops_; }
   double calibrated_tflops() const { return tflops_; }
+  double loaded_tflops() const { return rate_tflops_; }
   int K() const { return K_; }
   int N() const { return N_; }
   int max_M() const { return max_m_; }
@@ -42,6 +51,19 @@ class GemmStandin {
   int K_ = 0, N_ = 0, max_m_ = 0;
   double tflops_ = 0;       // measured alone at construction
   double flops_ = 0;
+  // closed loop: (start, end, flops) of recent steps; the rate over the
+  // completed window sizes the next steps
+  struct Sample {
+    cudaEvent_t e0, e1;
+    double flops;
+  };
+  std::deque<Sample> inflight_;
+  std::deque<std::pair<double, double>> window_;  // (flops, seconds) of completed steps
+  double win_flops_ = 0, win_s_ = 0;
+  double rate_tflops_ = 0;  // current estimate under load (starts at the alone rate)
+  std::deque<cudaEvent_t> spare_events_;
+  void poll(bool block_oldest);
+  cudaEvent_t event();
 };
 
 }  // namespace tcb

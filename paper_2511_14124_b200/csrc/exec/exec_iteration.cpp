@@ -100,7 +100,7 @@ std::size_t Executor::stage_state(TensorRec& s) {
   tag_ = CopyTag{"opt_load", s.id, 1, 0};
   wait_for_write(h2d_opt_, stage_sync_[b]);
   wait_for_read(h2d_opt_, h.sync);
-  cudaEvent_t e1 = copy(h2d_opt_, stage_[b], h.ptr, s.bytes, true);
+  cudaEvent_t e1 = copy(h2d_opt_, stage_[b], h.ptr, state_xfer_bytes(s), true);
   h.sync.readers.push_back(e1);
   stage_sync_[b] = SlotSync{e1, {}};
   staged_[index_of(s.id)] = b;
@@ -137,7 +137,9 @@ Executor::UpdateJob Executor::prepare_update(TensorRec& s, TensorRec& p) {
     auto it = staged_.find(index_of(s.id));
     j.b = it != staged_.end() ? it->second : stage_state(s);
     staged_.erase(index_of(s.id));
-    stats_.opt_h2d_bytes += s.bytes;  // counted at the update it feeds (staging may be a prologue)
+    stats_.opt_h2d_bytes += state_xfer_bytes(s);  // counted at the update it feeds (staging may be a prologue)
+    stats_.opt_logical_bytes += s.bytes;
+    j.split = s.split;
     j.stg = stage_[j.b];
     // (null once a drain between the prologue's staging and this update completed it)
     if (stage_sync_[j.b].writer) TCB_CK(cudaStreamWaitEvent(ost, stage_sync_[j.b].writer, 0));
@@ -153,6 +155,19 @@ Executor::UpdateJob Executor::prepare_update(TensorRec& s, TensorRec& p) {
     j.pout = pout_scratch_[p.bytes][k];
     j.psync = &pout_sync_[p.bytes][k];
     k = (k + 1) % pout_scratch_[p.bytes].size();
+  }
+  if (j.state_on_gpu && s.split) throw DeviceError(TC_EINTERNAL, "split optimizer state moved into HBM");
+  if (j.split && !j.on_gpu) {  // the master's high half: the parameter's bytes from its host slot into the scratch
+    if (p.tier != PTier::HostParam)
+      throw DeviceError(TC_EINTERNAL, "split optimizer state " + std::to_string(s.id) + ": parameter in NVMe");
+    Slot& ph = slot_of(p);
+    wait_for_write(h2d_opt_, *j.psync);
+    wait_for_read(h2d_opt_, ph.sync);
+    tag_ = CopyTag{"param_hi", p.id, 1, 0};
+    cudaEvent_t e = copy(h2d_opt_, j.pout, ph.ptr, p.bytes, true);
+    ph.sync.readers.push_back(e);
+    *j.psync = SlotSync{e, {}};
+    stats_.opt_h2d_bytes += p.bytes;
   }
   wait_for_write(ost, *j.psync);
   return j;
@@ -175,8 +190,18 @@ void Executor::run_updates(std::vector<UpdateJob>& jobs) {
   std::vector<AdamChunk> chunks;
   for (const UpdateJob& j : jobs) {
     auto* st = reinterpret_cast<float*>(j.stg);
-    chunks.push_back(AdamChunk{st, st + j.n, st + 2 * j.n, reinterpret_cast<const std::uint16_t*>(j.p->grad),
-                               reinterpret_cast<std::uint16_t*>(j.pout), j.n});
+    const auto* g = reinterpret_cast<const std::uint16_t*>(j.p->grad);
+    auto* pout = reinterpret_cast<std::uint16_t*>(j.pout);
+    if (j.split) {
+      const SplitLayout L = split_layout(j.n);
+      chunks.push_back(AdamChunk{nullptr, reinterpret_cast<float*>(j.stg + L.m), reinterpret_cast<float*>(j.stg + L.v),
+                                 g, pout, j.n, reinterpret_cast<std::uint16_t*>(j.stg + L.lo),
+                                 reinterpret_cast<std::uint32_t*>(j.stg + L.rb)});
+      ++stats_.split_updates;
+      stats_.split_elems += j.n;
+    } else {
+      chunks.push_back(AdamChunk{st, st + j.n, st + 2 * j.n, g, pout, j.n});
+    }
     stats_.adam_elems += j.n;
   }
   TCB_CK(launch_adamw_batch(chunks.data(), static_cast<int>(chunks.size()), sc, so_.grad_scale, ost, smin, smax));
@@ -206,11 +231,12 @@ void Executor::finish_update(UpdateJob& j, cudaEvent_t a1) {
     wait_for_write(d2h_opt_, h.sync);
     TCB_CK(cudaStreamWaitEvent(d2h_opt_, a1, 0));
     tag_ = CopyTag{"opt_store", s.id, 0, 1};
-    cudaEvent_t e3 = copy(d2h_opt_, h.ptr, j.stg, s.bytes, false);
+    cudaEvent_t e3 = copy(d2h_opt_, h.ptr, j.stg, state_xfer_bytes(s), false);
     h.sync = SlotSync{e3, {}};
     stage_sync_[j.b].readers.push_back(e3);
     stage_free_.push_back(j.b);
-    stats_.opt_d2h_bytes += s.bytes;
+    stats_.opt_d2h_bytes += state_xfer_bytes(s);
+    stats_.opt_logical_bytes += s.bytes;
   }
 
   if (!j.on_gpu) {  // updated-parameter write-back to its home tier (category iii)
@@ -360,7 +386,12 @@ std::vector<std::size_t> Executor::plan_hoisting(const std::vector<Hook>& hooks)
 
 // How many optimizer states fit through the H2D link during the forward
 // pass on top of the forward's own parameter prefetches, by the machine's
-// bandwidth model (machine.cpp:101-111) and the trace's compute time.
+// bandwidth model (machine.cpp:101-111) and the trace's compute time. With no
+// forward prefetches to protect (every parameter resident: C3, C5's cached
+// shard) the whole stage ring is filled: the loads only queue behind each
+// other, and the forward under load runs longer than the model says (C3:
+// ~360 vs 313 ms), so a model-sized budget left the link idle ~100 ms per
+// step before the backward freed its first stage.
 std::size_t Executor::forward_prestage_budget(const std::vector<Hook>& hooks) const {
   double fwd_us = 0, fwd_h2d = 0;
   for (const Hook& h : hooks) {
@@ -376,9 +407,11 @@ std::size_t Executor::forward_prestage_budget(const std::vector<Hook>& hooks) co
   } catch (...) {
     return 0;
   }
+  if (fwd_h2d == 0 && !prestage_order_.empty()) return stage_.size() > 2 ? stage_.size() - 2 : 1;
   const double spare = fwd_us * bw - fwd_h2d;
   if (spare <= 0 || prestage_order_.empty()) return std::min<std::size_t>(1, prestage_order_.size());
-  const double sbytes = static_cast<double>(recs_[static_cast<std::size_t>(prestage_order_.front())].bytes);
+  const double sbytes =
+      static_cast<double>(state_xfer_bytes(recs_[static_cast<std::size_t>(prestage_order_.front())]));
   return std::max<std::size_t>(1, static_cast<std::size_t>(spare / sbytes));
 }
 

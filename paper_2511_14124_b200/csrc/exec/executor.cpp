@@ -218,8 +218,19 @@ Executor::Executor(const std::string& trace_path, const std::string& machine_pat
   // logical pool sizes, plus spare slots per class.
   const int gspare = std::max(opts.gpu_spare_slots, 1), hspare = std::max(opts.host_spare_slots, 1);
   double fwd_h2d = 0;
-  std::map<std::pair<int, std::uint64_t>, std::uint32_t> need = simulate_occupancy(&fwd_h2d);
+  std::set<TensorId> in_nvme, to_gpu;
+  std::map<std::pair<int, std::uint64_t>, std::uint32_t> need = simulate_occupancy(&fwd_h2d, &in_nvme, &to_gpu);
   lap("occupancy dry run");
+  {  // split-master eligibility (TensorRec::split_ok)
+    const char* fm = std::getenv("TC_FULL_MASTER");
+    const bool full_master = opts.full_master != 0 || (fm && std::atoi(fm) != 0);
+    for (auto& s : recs_) {
+      if (!s.is_state || s.partner < 0 || full_master) continue;
+      const TensorRec& p = recs_[static_cast<std::size_t>(s.partner)];
+      s.split_ok = !in_nvme.count(p.id) && policy_->initial_tier(s.id).value_or(Tier::Cpu) != Tier::Gpu &&
+                   !to_gpu.count(s.id) && (p.bytes / 2) % kSplitTile == 0;
+    }
+  }
   if (const SchedulerState* st = policy_->scheduler_state()) {
     std::map<std::pair<int, std::uint64_t>, std::uint32_t> logical;
     for (const Chunk& c : st->gpu_pool.chunks()) ++logical[{0, c.size}];
@@ -365,6 +376,7 @@ Executor::Executor(const std::string& trace_path, const std::string& machine_pat
     }
     r.nvme_valid = t == Tier::Nvme;
   }
+  TCB_CK(cudaMalloc(&codec_flag_, sizeof(unsigned)));
 }
 
 Executor::~Executor() {
@@ -396,6 +408,7 @@ Executor::~Executor() {
   for (auto& e : result_ev_)
     if (e) cudaEventDestroy(e);
   if (d_span_) cudaFree(d_span_);
+  if (codec_flag_) cudaFree(codec_flag_);
   if (h2d_) cudaStreamDestroy(h2d_);
   if (d2h_) cudaStreamDestroy(d2h_);
   if (opt_) cudaStreamDestroy(opt_);
@@ -420,7 +433,9 @@ Executor::~Executor() {
 // 1 host parameter cache, 2 host optimizer-state cache. A retained source
 // (src_retains) keeps its slot; a destination that already has the bytes
 // (dst_has_copy) takes none.
-std::map<std::pair<int, std::uint64_t>, std::uint32_t> Executor::simulate_occupancy(double* fwd_h2d) const {
+std::map<std::pair<int, std::uint64_t>, std::uint32_t> Executor::simulate_occupancy(double* fwd_h2d,
+                                                                                    std::set<TensorId>* in_nvme,
+                                                                                    std::set<TensorId>* to_gpu) const {
   std::unique_ptr<IPolicy> pol = make_policy(trace_, machine_, cfg_);
   pol->init();
   std::unordered_map<TensorId, std::set<Tier>> where;
@@ -441,10 +456,13 @@ std::map<std::pair<int, std::uint64_t>, std::uint32_t> Executor::simulate_occupa
     info[t.id] = {t.size_bytes, t.kind == TensorKind::OptStateFP32};
     const Tier tier = pol->initial_tier(t.id).value_or(Tier::Cpu);
     where[t.id] = {tier};
+    if (in_nvme && tier == Tier::Nvme) in_nvme->insert(t.id);
     add(t.id, tier, +1);
   }
   auto apply_reqs = [&](const std::vector<TransferRequest>& reqs) {
     for (const TransferRequest& r : reqs) {
+      if (in_nvme && r.dst == Tier::Nvme) in_nvme->insert(r.tensor_id);
+      if (to_gpu && r.dst == Tier::Gpu) to_gpu->insert(r.tensor_id);
       auto& w = where[r.tensor_id];
       if (!r.src_retains && w.erase(r.src)) add(r.tensor_id, r.src, -1);
       if (w.insert(r.dst).second) add(r.tensor_id, r.dst, +1);
@@ -490,15 +508,18 @@ std::map<std::pair<int, std::uint64_t>, std::uint32_t> Executor::simulate_occupa
 // compute time x the machine model's CPU->GPU bandwidth minus the forward's
 // own cache prefetches), plus the backward's lookahead; at least 12, at most
 // half the free HBM. Measured optima it reproduces: 12 on C2 at 16k tokens,
-// ~118 on C5 (profiles/r01_stage_sweep.json).
+// ~118 on C5 (profiles/r01_stage_sweep.json). Without forward prefetches the
+// forward's time is taken 1.5x the model's (it runs longer under load, and
+// the prologue then fills the ring: forward_prestage_budget).
 int Executor::auto_stage_slots(double fwd_h2d) const {
-  double fwd_us = 0, sbytes = 0;
+  double fwd_us = 0, sbytes = 0, alloc = 0;
   std::size_t nstates = 0;
   for (const TraceStep& st : trace_.steps)
     if (st.phase == Phase::Forward) fwd_us += st.compute_us * cfg_.batch_scale;
   for (const auto& r : recs_)
-    if (r.is_state) {
-      sbytes = std::max(sbytes, static_cast<double>(r.bytes));
+    if (r.is_state) {  // bytes a load moves (split-master prefix where eligible)
+      sbytes = std::max(sbytes, static_cast<double>(r.split_ok ? split_layout(r.bytes / 12).bytes : r.bytes));
+      alloc = std::max(alloc, static_cast<double>(r.bytes));
       ++nstates;
     }
   if (nstates == 0 || sbytes == 0) return 12;
@@ -508,11 +529,11 @@ int Executor::auto_stage_slots(double fwd_h2d) const {
   } catch (...) {
     return 12;
   }
-  const double spare = std::max(0.0, fwd_us * bw - fwd_h2d);
+  const double spare = std::max(0.0, (fwd_h2d == 0 ? 1.5 : 1.0) * fwd_us * bw - fwd_h2d);
   std::size_t n = static_cast<std::size_t>(spare / sbytes) + 4;
   std::size_t free_b = 0, total_b = 0;
   if (cudaMemGetInfo(&free_b, &total_b) == cudaSuccess)
-    n = std::min<std::size_t>(n, static_cast<std::size_t>(0.5 * static_cast<double>(free_b) / sbytes));
+    n = std::min<std::size_t>(n, static_cast<std::size_t>(0.5 * static_cast<double>(free_b) / alloc));
   n = std::min(n, nstates + 2);
   return static_cast<int>(std::max<std::size_t>(n, 12));
 }
@@ -902,7 +923,11 @@ void Executor::seed(std::uint64_t seed) {
       TensorRec& s = recs_[static_cast<std::size_t>(p.partner)];
       std::uint8_t* pv = p.tier == PTier::Gpu ? where(p) : tmp;
       std::uint8_t* sdst = stage_[1];
-      TCB_CK(launch_init_state(reinterpret_cast<const std::uint16_t*>(pv), reinterpret_cast<float*>(sdst), n, nullptr));
+      s.split = s.split_ok;
+      if (s.split)  // master = float(param): low halves and round bits zero, moments zero
+        TCB_CK(cudaMemset(sdst, 0, s.bytes));
+      else
+        TCB_CK(launch_init_state(reinterpret_cast<const std::uint16_t*>(pv), reinterpret_cast<float*>(sdst), n, nullptr));
       TCB_CK(cudaDeviceSynchronize());
       if (s.tier == PTier::Nvme) {
         std::vector<std::uint8_t> hb(s.bytes);
@@ -911,8 +936,10 @@ void Executor::seed(std::uint64_t seed) {
         TCB_CK(cudaMemcpy(pin, sdst, s.bytes, cudaMemcpyDeviceToHost));
         nvme_write(s, pin);
         cudaFreeHost(pin);
+      } else if (s.tier == PTier::Gpu) {
+        TCB_CK(cudaMemcpy(where(s), sdst, s.bytes, cudaMemcpyDeviceToDevice));
       } else {
-        TCB_CK(cudaMemcpy(where(s), sdst, s.bytes, cudaMemcpyDeviceToHost));
+        TCB_CK(cudaMemcpy(where(s), sdst, state_xfer_bytes(s), cudaMemcpyDeviceToHost));
       }
     }
   }
@@ -922,23 +949,98 @@ void Executor::seed(std::uint64_t seed) {
   for (auto& r : recs_) r.issued_since_access = 0;
 }
 
+// A tensor's stored bytes from / to wherever it lives (states: as stored,
+// split or full).
+void Executor::load_state_host(TensorRec& r, void* dst) {
+  if (r.tier == PTier::Gpu) {
+    TCB_CK(cudaMemcpy(dst, where(r), r.bytes, cudaMemcpyDeviceToHost));
+  } else if (r.tier == PTier::Nvme) {
+    if (!r.nvme_valid) throw DeviceError(TC_EINTERNAL, "NVMe replica of tensor is stale");
+    std::uint8_t* tmp = nullptr;  // pinned and page-aligned (O_DIRECT tiers)
+    TCB_CK(cudaMallocHost(reinterpret_cast<void**>(&tmp), r.bytes));
+    const bool ok = nvme_->io(false, tmp, r.bytes, r.nvme_off);
+    if (ok) std::memcpy(dst, tmp, r.bytes);
+    cudaFreeHost(tmp);
+    if (!ok) throw DeviceError(TC_EIO, "read_tensor: NVMe read failed");
+  } else {
+    std::memcpy(dst, where(r), r.bytes);
+  }
+}
+
+void Executor::store_state_host(TensorRec& r, const void* src) {
+  if (r.tier == PTier::Gpu) {
+    TCB_CK(cudaMemcpy(where(r), src, r.bytes, cudaMemcpyHostToDevice));
+    r.nvme_valid = false;
+  } else if (r.tier == PTier::Nvme) {
+    std::uint8_t* tmp = nullptr;
+    TCB_CK(cudaMallocHost(reinterpret_cast<void**>(&tmp), r.bytes));
+    std::memcpy(tmp, src, r.bytes);
+    nvme_write(r, tmp);
+    cudaFreeHost(tmp);
+  } else {
+    std::memcpy(where(r), src, r.bytes);
+    r.nvme_valid = false;
+  }
+}
+
+// Split state -> full [p32|m|v] layout, on the GPU (stages 0/1 as scratch;
+// the caller has synced). The master's high half is the partner's bf16 value.
+void Executor::state_to_full(TensorRec& s, const void* stored_host, void* full_host) {
+  TensorRec& p = recs_[static_cast<std::size_t>(s.partner)];
+  drop_staged();
+  const std::uint16_t* B = param_bits_dev(p);
+  TCB_CK(cudaMemcpy(stage_[0], stored_host, state_xfer_bytes(s), cudaMemcpyHostToDevice));
+  TCB_CK(launch_state_expand(stage_[0], B, reinterpret_cast<float*>(stage_[1]), p.bytes / 2, nullptr));
+  TCB_CK(cudaMemcpy(full_host, stage_[1], s.bytes, cudaMemcpyDeviceToHost));
+}
+
+// Full layout -> split, on the GPU, into stage 1; false when some master does
+// not round to the parameter's bf16 value (not representable split).
+bool Executor::state_from_full(TensorRec& s, const void* full_host, std::uint8_t* stored_dev) {
+  TensorRec& p = recs_[static_cast<std::size_t>(s.partner)];
+  drop_staged();
+  const std::uint16_t* B = param_bits_dev(p);
+  TCB_CK(cudaMemcpy(stage_[0], full_host, s.bytes, cudaMemcpyHostToDevice));
+  TCB_CK(cudaMemset(codec_flag_, 0, sizeof(unsigned)));
+  TCB_CK(launch_state_compress(reinterpret_cast<const float*>(stage_[0]), B, stored_dev, p.bytes / 2, codec_flag_,
+                               nullptr));
+  unsigned flag = 1;
+  TCB_CK(cudaMemcpy(&flag, codec_flag_, sizeof(unsigned), cudaMemcpyDeviceToHost));
+  return flag == 0;
+}
+
+// The parameter's current bf16 bytes in HBM: its GPU slot, else a copy in its
+// first update scratch buffer (callers have synced: nothing uses it).
+const std::uint16_t* Executor::param_bits_dev(TensorRec& p) {
+  if (p.tier == PTier::Gpu) return reinterpret_cast<const std::uint16_t*>(where(p));
+  std::vector<std::uint8_t> hb(p.bytes);
+  load_state_host(p, hb.data());
+  std::uint8_t* d = pout_scratch_.at(p.bytes).front();
+  TCB_CK(cudaMemcpy(d, hb.data(), p.bytes, cudaMemcpyHostToDevice));
+  return reinterpret_cast<const std::uint16_t*>(d);
+}
+
+// Back to the full layout in place (its parameter is about to change).
+void Executor::unsplit(TensorRec& s) {
+  if (!s.split) return;
+  std::vector<std::uint8_t> stored(s.bytes), full(s.bytes);
+  load_state_host(s, stored.data());
+  state_to_full(s, stored.data(), full.data());
+  s.split = false;
+  store_state_host(s, full.data());
+}
+
 void Executor::read_tensor(TensorId id, void* dst, std::uint64_t bytes) {
   TCB_CK(cudaSetDevice(device_));
   sync();
   TensorRec& r = rec(id);
   if (bytes != r.bytes) throw std::invalid_argument("read_tensor: size mismatch");
-  if (r.tier == PTier::Gpu) {
-    TCB_CK(cudaMemcpy(dst, where(r), bytes, cudaMemcpyDeviceToHost));
-  } else if (r.tier == PTier::Nvme) {
-    if (!r.nvme_valid) throw DeviceError(TC_EINTERNAL, "NVMe replica of tensor is stale");
-    std::uint8_t* tmp = nullptr;  // pinned and page-aligned (O_DIRECT tiers)
-    TCB_CK(cudaMallocHost(reinterpret_cast<void**>(&tmp), bytes));
-    const bool ok = nvme_->io(false, tmp, bytes, r.nvme_off);
-    if (ok) std::memcpy(dst, tmp, bytes);
-    cudaFreeHost(tmp);
-    if (!ok) throw DeviceError(TC_EIO, "read_tensor: NVMe read failed");
+  if (r.is_state && r.split) {
+    std::vector<std::uint8_t> stored(r.bytes);
+    load_state_host(r, stored.data());
+    state_to_full(r, stored.data(), dst);
   } else {
-    std::memcpy(dst, where(r), bytes);
+    load_state_host(r, dst);
   }
 }
 
@@ -948,19 +1050,18 @@ void Executor::write_tensor(TensorId id, const void* src, std::uint64_t bytes) {
   TensorRec& r = rec(id);
   if (bytes != r.bytes) throw std::invalid_argument("write_tensor: size mismatch");
   if (r.is_state) drop_staged();
-  if (r.tier == PTier::Gpu) {
-    TCB_CK(cudaMemcpy(where(r), src, bytes, cudaMemcpyHostToDevice));
-    r.nvme_valid = false;
-  } else if (r.tier == PTier::Nvme) {
-    std::uint8_t* tmp = nullptr;
-    TCB_CK(cudaMallocHost(reinterpret_cast<void**>(&tmp), bytes));
-    std::memcpy(tmp, src, bytes);
-    nvme_write(r, tmp);
-    cudaFreeHost(tmp);
-  } else {
-    std::memcpy(where(r), src, bytes);
-    r.nvme_valid = false;
+  if (!r.is_state && r.partner >= 0) unsplit(recs_[static_cast<std::size_t>(r.partner)]);  // its high halves change
+  if (r.is_state && r.split_ok) {
+    if (state_from_full(r, src, stage_[1])) {
+      std::vector<std::uint8_t> stored(r.bytes, 0);
+      TCB_CK(cudaMemcpy(stored.data(), stage_[1], split_layout(r.bytes / 12).bytes, cudaMemcpyDeviceToHost));
+      r.split = true;
+      store_state_host(r, stored.data());
+      return;
+    }
+    r.split = false;
   }
+  store_state_host(r, src);
 }
 
 void* Executor::gpu_ptr(TensorId id) {

@@ -26,6 +26,7 @@
 #include <map>
 #include <memory>
 #include <optional>
+#include <set>
 #include <string>
 #include <fstream>
 #include <unordered_map>
@@ -135,6 +136,12 @@ struct TensorRec {
   bool has_home = false, home_valid = false;
   PTier home_tier = PTier::HostParam;
   std::uint32_t home_slot = 0;
+  // States: held split on the host (dataplane.cuh SplitLayout: the master's
+  // high half is the partner parameter's bf16 value, which only the update
+  // writes). split_ok (dry run of the policy's decisions): the partner never
+  // lives in NVMe (its bytes are in HBM or pinned memory at every update),
+  // the state never moves into HBM, and the chunk is whole AdamW tiles.
+  bool split = false, split_ok = false;
 };
 
 // ZeRO-3 exchange state of one rank. Chunk c of layer L holds
@@ -291,7 +298,20 @@ class Executor {
     std::size_t b = 0;            // stage index (host-resident states)
     std::uint8_t* pout = nullptr;  // bf16 result (the parameter's GPU slot or a scratch buffer)
     SlotSync* psync = nullptr;
+    bool split = false;            // stg holds [lo|rb|m|v] (SplitLayout); pout is also the master's high half
   };
+  // bytes of a host-resident state that cross PCIe (its split prefix or all of it)
+  std::uint64_t state_xfer_bytes(const TensorRec& s) const {
+    return s.split ? split_layout(s.bytes / 12).bytes : s.bytes;
+  }
+  // state bytes as stored (split or full) <-> the full [p32|m|v] layout, on the GPU
+  void state_to_full(TensorRec& s, const void* stored_host, void* full_host);
+  const std::uint16_t* param_bits_dev(TensorRec& p);  // the parameter's bf16 bytes in HBM (synchronous)
+  bool state_from_full(TensorRec& s, const void* full_host, std::uint8_t* stored_dev);
+  void unsplit(TensorRec& s);
+  void load_state_host(TensorRec& s, void* host_dst);          // the state's stored bytes, any host tier
+  void store_state_host(TensorRec& s, const void* host_src);   // ... written back
+  unsigned* codec_flag_ = nullptr;  // device word: compress mismatch
   UpdateJob prepare_update(TensorRec& s, TensorRec& p);
   void run_updates(std::vector<UpdateJob>& jobs);
   void finish_update(UpdateJob& j, cudaEvent_t a1);
@@ -404,7 +424,9 @@ class Executor {
   std::uint64_t barrier_io_ = 0;  // NVMe job a blocking request ended with
   // peak slots per (tier, class) over two iterations of decisions; also the
   // steady-state forward pass's non-instant H2D bytes (*fwd_h2d)
-  std::map<std::pair<int, std::uint64_t>, std::uint32_t> simulate_occupancy(double* fwd_h2d = nullptr) const;
+  std::map<std::pair<int, std::uint64_t>, std::uint32_t> simulate_occupancy(
+      double* fwd_h2d = nullptr, std::set<tencache::TensorId>* in_nvme = nullptr,
+      std::set<tencache::TensorId>* to_gpu = nullptr) const;
   int auto_stage_slots(double fwd_h2d) const;
   std::vector<Copy> copies_;
   std::vector<Stall> stalls_;                                      // (reach, go) on compute

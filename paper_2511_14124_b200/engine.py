@@ -18,10 +18,10 @@ from . import _native as N
 
 class Engine:
     def __init__(self, trace_path, machine_path="", config=None, device=0, nvme_dir="", gpu_spare_slots=16,
-                 host_spare_slots=1, opt_stage_slots=0, direct_io=False):
+                 host_spare_slots=1, opt_stage_slots=0, direct_io=False, full_master=False):
         import json
         o = N.tc_engine_options(device, N.b(nvme_dir), gpu_spare_slots, host_spare_slots, opt_stage_slots,
-                                1 if direct_io else 0, 1)
+                                1 if direct_io else 0, 1, 1 if full_master else 0)
         self._h = C.c_void_p()
         N.check(N.lib().tc_engine_create(N.b(trace_path), N.b(machine_path), N.b(json.dumps(config or {})),
                                          C.byref(o), C.byref(self._h)))

@@ -39,9 +39,9 @@ def load(tr):
     return tensors, steps
 
 
-def check_engine(tr, m, cfg, iters=2, nvme_dir="", hoist=True, prestage=True, stages=12):
+def check_engine(tr, m, cfg, iters=2, nvme_dir="", hoist=True, prestage=True, stages=12, full_master=False):
     tensors, steps = load(tr)
-    e = Engine(tr, m, cfg, nvme_dir=nvme_dir, opt_stage_slots=stages)
+    e = Engine(tr, m, cfg, nvme_dir=nvme_dir, opt_stage_slots=stages, full_master=full_master)
     e.seed(7)
     params = {i: e.read_tensor(i, t["size"]).view(np.uint16).copy() for i, t in tensors.items() if t["kind"] == "p16"}
     states = {i: e.read_tensor(i, t["size"]).view(np.float32).copy() for i, t in tensors.items() if t["kind"] == "o32"}
@@ -75,6 +75,17 @@ def check_engine(tr, m, cfg, iters=2, nvme_dir="", hoist=True, prestage=True, st
     return st
 
 
+def assert_state_traffic(st, iters, n, S):
+    """Every state crossed PCIe exactly once per direction per iteration, as
+    its split-master prefix (10.125 B/param; + the bf16 parameter H2D when
+    that is not in HBM at the update)."""
+    split_b = 10 * (S // 2) + S // 16
+    assert st["opt_logical_bytes"] == 2 * iters * n * 6 * S
+    assert st["split_updates"] == iters * n
+    assert st["opt_d2h_bytes"] == iters * n * split_b
+    assert iters * n * split_b <= st["opt_h2d_bytes"] <= iters * n * (split_b + S)
+
+
 def write_with_states(d, name, sizes, gpu, cpu, fwd_multi=False, iters=2, order=None):
     p = [(i + 1, s, "p16", i) for i, s in enumerate(sizes)]
     s, o = cases.with_states(p, order=order)
@@ -92,6 +103,31 @@ def test_fig8_shape(tmpd, pol, ro, hoist):
     st = check_engine(tr, m, cfg, hoist=hoist)
     rep = ref.run(tr, m, cfg)
     assert st["param_accesses"] == rep["param_accesses"] and st["param_hits"] == rep["param_hits"]
+
+
+@pytest.mark.parametrize("full_master", [False, True])
+@pytest.mark.parametrize("gpu_chunks", [6, 3])
+def test_split_master_states(tmpd, full_master, gpu_chunks):
+    """Optimizer states cross PCIe split (low half + round bit, 10.125 B/param
+    instead of 12); when the parameter is not in HBM at its update its bf16
+    bytes (the master's high half) come along. Either way every state,
+    parameter and access checksum is bit-exact with the oracle after every
+    iteration (check_engine)."""
+    S, n_p, iters = 8192, 6, 3
+    tr, m = write_with_states(tmpd, "sm", [S] * n_p, gpu_chunks * S, n_p * S + n_p * 6 * S, iters=iters)
+    st = check_engine(tr, m, {"policy": "tencache"}, iters=iters, full_master=full_master)
+    n = S // 2
+    split_b = 2 * n + n // 8 + 8 * n
+    assert st["opt_logical_bytes"] == 2 * iters * n_p * 6 * S
+    if full_master:
+        assert st["split_updates"] == 0
+        assert st["opt_h2d_bytes"] == iters * n_p * 6 * S
+    elif gpu_chunks == n_p:  # every parameter pinned in HBM: every state split, nothing else moves
+        assert st["split_updates"] == iters * n_p
+        assert st["opt_h2d_bytes"] == st["opt_d2h_bytes"] == iters * n_p * split_b
+    else:
+        assert st["split_updates"] == iters * n_p
+        assert iters * n_p * split_b <= st["opt_h2d_bytes"] <= iters * n_p * (split_b + S)
 
 
 @pytest.mark.parametrize("pol", ["tencache", "tencache+opt"])
@@ -175,8 +211,9 @@ def test_chunk_trace_c2_mini(tmpd):
     assert st["param_hits"] == rep["param_hits"]
     assert st["h2d_bytes"] > 0 and st["d2h_bytes"] > 0
     # every state crosses PCIe exactly once each way per iteration (the next
-    # iteration's prologue staging included, none re-staged or dropped)
-    assert st["opt_h2d_bytes"] == 3 * n * 6 * S and st["opt_d2h_bytes"] == 3 * n * 6 * S
+    # iteration's prologue staging included, none re-staged or dropped), as
+    # its split-master prefix (+ the bf16 parameter when that is not in HBM)
+    assert_state_traffic(st, 3, n, S)
 
 
 def test_zero3_exchange_world1(tmpd):
@@ -384,7 +421,7 @@ def test_back_to_back_iterations_with_prologue(tmpd):
         assert np.array_equal(e.read_tensor(i, S).view(np.uint16), params[i]), f"param {i}"
         assert np.array_equal(e.read_tensor(n + i, 6 * S).view(np.uint32), states[n + i].view(np.uint32)), f"state {n + i}"
     st = e.stats()
-    assert st["opt_h2d_bytes"] == iters * n * 6 * S and st["opt_d2h_bytes"] == iters * n * 6 * S
+    assert_state_traffic(st, iters, n, S)
     e.close()
 
 
@@ -425,7 +462,7 @@ def test_full_size_c2_bit_exact(tmpd):
             f"state {n + i}"
     st = e.stats()
     assert st["param_hits"] == ref.run(info["trace"], info["machine"], {"policy": "tencache"})["param_hits"]
-    assert st["opt_h2d_bytes"] == 2 * n * 6 * S and st["opt_d2h_bytes"] == 2 * n * 6 * S
+    assert_state_traffic(st, 2, n, S)
     e.close()
 
 

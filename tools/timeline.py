@@ -18,7 +18,9 @@ cfgname = os.environ.get("CFG", "c2")
 iters = int(os.environ.get("ITERS", "5"))
 stages = int(os.environ.get("STAGES", "12"))
 wd = tempfile.mkdtemp(dir="/dev/shm")
-if cfgname == "c5":
+if cfgname == "c3":
+    info = T.config_c3_rank(wd, world=1, rank=0)
+elif cfgname == "c5":
     info = T.config_c5_rank(wd)
 elif cfgname == "c4":
     info = T.config_c4_rank(wd)
@@ -26,13 +28,18 @@ else:
     info = T.config_c2(wd, iterations=1)
 pol = "tencache+opt" if cfgname == "c4" else "tencache"
 eng = Engine(info["trace"], info["machine"], {"policy": pol}, opt_stage_slots=stages, nvme_dir=wd)
+print("stages", stages)
 eng.seed(0)
+if cfgname == "c3":  # ZeRO-3 exchange at world 1, as bench.py runs it
+    from paper_2511_14124_b200 import zero3 as Z  # noqa: E402
+    Z.enable(eng, info["layout"], 0, 1, exchange="p2p")
+compute_mode = int(os.environ.get("COMPUTE", "1"))  # 1 spin, 2 GEMM stand-in
 os.makedirs("gpurun_out", exist_ok=True)
 log = f"gpurun_out/timeline_{cfgname}.jsonl"
 eng.event_log(log)
 stream = torch.cuda.current_stream()
 for _ in range(iters):
-    eng.iteration(lr=1e-4, compute_mode=1, spin_ctas=1, stream=stream.cuda_stream)
+    eng.iteration(lr=1e-4, compute_mode=compute_mode, spin_ctas=1, stream=stream.cuda_stream)
 eng.sync()
 phases = eng.phase_ms()
 eng.event_log("")
