@@ -291,7 +291,10 @@ int tc_engine_read_tensor(tc_engine* e, uint32_t tensor, void* host_dst, uint64_
 int tc_engine_write_tensor(tc_engine* e, uint32_t tensor, const void* host_src, uint64_t bytes);
 /* Host copy of a parameter's bf16 gradient (HBM). */
 int tc_engine_read_grad(tc_engine* e, uint32_t tensor, void* host_dst, uint64_t bytes);
-/* Device pointer of the tensor's current GPU slot (NULL if not GPU-resident). */
+/* Device pointer of the tensor's current GPU slot (NULL if not GPU-resident).
+ * Parameter bytes behind it are the high halves of split-master states
+ * (tc_engine_options.full_master): write them through tc_engine_write_tensor,
+ * or create the engine with full_master = 1 to write them in place. */
 void* tc_engine_gpu_ptr(tc_engine* e, uint32_t tensor);
 /* Gradient buffer (bf16, on GPU) of a parameter tensor. */
 void* tc_engine_grad_ptr(tc_engine* e, uint32_t tensor);

@@ -61,6 +61,7 @@ class GemmStandin {
   std::deque<std::pair<double, double>> window_;  // (flops, seconds) of completed steps
   double win_flops_ = 0, win_s_ = 0;
   double rate_tflops_ = 0;  // current estimate under load (starts at the alone rate)
+  bool open_loop_ = false;
   std::deque<cudaEvent_t> spare_events_;
   void poll(bool block_oldest);
   cudaEvent_t event();

@@ -68,3 +68,27 @@ def test_reference_arm_under_torchrun_world2():
     d = json.loads(lines[0])
     assert d["impl"] == "reference" and d["n_gpus"] == 2
     assert d["cpu_baseline"]["cores"] == len(os.sched_getaffinity(0))
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("world", [4, 8])
+def test_product_arm_torchrun_ranks_sharing_one_gpu(world):
+    """N>1 product arm (the driver's SCALE launch) with every rank on the one
+    GPU of the box (gloo plumbing, fused p2p exchange): one line from rank 0
+    carrying the N=1 line's measurement keys plus the exchange block."""
+    r = subprocess.run([sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", str(world),
+                        "--master-addr", "127.0.0.1", "--master-port", str(29660 + world), "bench.py",
+                        "--gpus", str(world), "--config", "c2", "--steps", "2", "--warmup", "3"],
+                       cwd=ROOT, capture_output=True, text=True, timeout=900)
+    assert r.returncode == 0, r.stderr[-3000:]
+    lines = [l for l in r.stdout.splitlines() if l.strip().startswith("{")]
+    assert len(lines) == 1, r.stdout
+    d = json.loads(lines[0])
+    assert BASE_KEYS <= d.keys() and d["n_gpus"] == world and "impl" not in d
+    for k in ("roofline", "pcie", "migration_hidden_frac", "ontime_rate", "hit_rate", "migrated_bytes_per_step",
+              "exchange", "gpu_launches", "clocks", "state_codec"):
+        assert k in d, k
+    assert set(d["pcie"]["per_rank_min_max"]) == {"h2d_GBps_step", "d2h_GBps_step", "h2d_GBps_busy", "d2h_GBps_busy"}
+    assert d["exchange"]["bytes_per_step_per_rank"] > 0
+    assert d["hit_rate"]["accesses"] > 0 and d["value"] > 0
+    assert "functional run" in d["config"]["workload"]

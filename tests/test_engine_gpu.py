@@ -497,3 +497,53 @@ def test_nvme_failure_surfaces(tmpd, monkeypatch):
     assert ei.value.code == N.TC_EIO
     monkeypatch.delenv("TC_NVME_FAIL_JOB")
     e.close()
+
+
+@pytest.mark.parametrize("gpu_chunks", [4, 2])
+def test_split_master_rewrites(tmpd, gpu_chunks):
+    """A parameter written through the API changes the master's high half, so
+    its split state goes back to the full layout first (the stored master is
+    kept, as the reference's state is); a state written with a master that
+    does not round to its parameter stays full; one that does is split again.
+    Every later update matches the oracle on those values."""
+    S, n_p = 4096, 4
+    tr, m = write_with_states(tmpd, "rw", [S] * n_p, gpu_chunks * S, n_p * S + n_p * 6 * S, iters=3)
+    tensors, steps = load(tr)
+    e = Engine(tr, m, {"policy": "tencache"})
+    e.seed(5)
+    e.iteration(**HP, last=True)
+    params = {i: e.read_tensor(i, S).view(np.uint16).copy() for i in range(1, n_p + 1)}
+    states = {n_p + i: e.read_tensor(n_p + i, 6 * S).view(np.float32).copy() for i in range(1, n_p + 1)}
+    grads = {i: e.read_grad(i, S).copy() for i in range(1, n_p + 1)}
+    rng = np.random.default_rng(0)
+    k = S // 2
+    # (1) new bf16 values for parameter 1: its state keeps its master
+    params[1] = (rng.standard_normal(k).astype(np.float32) * 0.02).view(np.uint32).__rshift__(16).astype(np.uint16)
+    e.write_tensor(1, params[1])
+    assert np.array_equal(e.read_tensor(n_p + 1, 6 * S).view(np.uint32), states[n_p + 1].view(np.uint32))
+    # (2) a state whose master is not the parameter's rounding: kept full
+    st2 = states[n_p + 2].copy()
+    st2[:k] += np.float32(0.5)
+    states[n_p + 2] = st2
+    e.write_tensor(n_p + 2, st2)
+    # (3) a consistent state (master = float(param), fresh moments): split again
+    st3 = np.concatenate([(params[3].astype(np.uint32) << 16).view(np.float32),
+                          rng.standard_normal(2 * k).astype(np.float32) * 1e-4])
+    st3[2 * k:] = np.abs(st3[2 * k:])
+    states[n_p + 3] = st3
+    e.write_tensor(n_p + 3, st3)
+    for sid in states:
+        assert np.array_equal(e.read_tensor(sid, 6 * S).view(np.uint32), states[sid].view(np.uint32)), sid
+    e.reset_stats()
+    for it in (2, 3):
+        e.iteration(**HP, last=it == 3)
+        for sid, pid in [s["ids"] for s in steps if s["phase"] == "o"]:
+            st = states[sid]
+            params[pid] = ref.adamw(st[:k], st[k:2 * k], st[2 * k:], grads[pid], HP["lr"], HP["beta1"],
+                                    HP["beta2"], HP["eps"], HP["weight_decay"], it)
+    for i in range(1, n_p + 1):
+        assert np.array_equal(e.read_tensor(i, S).view(np.uint16), params[i]), f"param {i}"
+        assert np.array_equal(e.read_tensor(n_p + i, 6 * S).view(np.uint32), states[n_p + i].view(np.uint32)), i
+    st = e.stats()
+    assert st["split_updates"] == 2 * 2  # states 3 and 4 split; 1 and 2 full
+    e.close()
