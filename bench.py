@@ -47,9 +47,9 @@ sys.path.insert(0, ROOT)
 
 METRIC = "step time & migrated GB/s per GPU vs PCIe roofline; GPU cache hit rate"
 ADAM_BYTES_PER_ELEM = 28  # read p32,m,v (12) + g bf16 (2); write p32,m,v (12) + p bf16 (2)
-# split-master states (tc_adamw_split_master): read lo (2) + round bit (1/8) + bf16 param (2) + m,v (8) + g (2);
-# write lo (2) + round bit (1/8) + param (2) + m,v (8)
-ADAM_SPLIT_BYTES_PER_ELEM = 26.25
+# packed split-master states (tc_adamw_split_master): read lo (2) + round bit (1/8) + bf16 param (2) + m, v planes
+# (7.25) + group bases (1/16) + g (2); write the same but g
+ADAM_SPLIT_BYTES_PER_ELEM = 24.875
 WORKLOADS = {
     "c2": "C2: OPT-1.3B offloaded training step, GPU->pinned-CPU tier, size-class buffer reuse (BASELINE.json "
           "configs[1])",
@@ -398,11 +398,12 @@ def run_ours(args, name, secondary=False):
                 "split_updates_per_step_rank0": st["split_updates"] // K,
                 "opt_bytes_per_step_rank0": {"logical_12B_per_param": st["opt_logical_bytes"] // K,
                                              "over_pcie": (st["opt_h2d_bytes"] + st["opt_d2h_bytes"]) // K},
-                "note": "optimizer states whose parameter never lives in NVMe cross PCIe as the fp32 master's low "
-                        "half + a round bit + m + v (10.125 B/param each way instead of 12): the high half is the "
-                        "bf16 parameter the update itself rounds from the master (lossless, bit-exact; "
-                        "tests/test_split_master_gpu.py). W (the value numerator) keeps the full 12 B/param, "
-                        "the PCIe fractions use the bytes that crossed the link"},
+                "note": "optimizer states whose parameter never lives in NVMe cross PCIe packed: the fp32 master's "
+                        "low half + a round bit (the high half is the bf16 parameter the update itself rounds "
+                        "from it), m and v with their top exponent byte coded per 32-element group (9.44 B/param "
+                        "each way instead of 12; lossless, bit-exact: tests/test_split_master_gpu.py). W (the "
+                        "value numerator) keeps the full 12 B/param, the PCIe fractions use the bytes that "
+                        "crossed the link"},
             "gpu_launches": int(launches_total),
             "setup_s": round(setup_s, 2),
             "setup_breakdown_s": {"engine_create_pin_and_carve": round(t_create, 2), "seed": round(t_seed, 2)},

@@ -157,23 +157,29 @@ typedef struct {
 } tc_adam_chunk;
 int tc_adamw_batch(const tc_adam_chunk* chunks, uint32_t count, double lr, double beta1, double beta2, double eps,
                    double weight_decay, int64_t step, float grad_scale, void* stream);
-/* Split-master optimizer state (what the engine keeps on the host for a
- * parameter that never leaves HBM): n % 2048 == 0 elements laid out as
- * [lo: u16 x n][rb: n/8 bytes][m: f32 x n][v: f32 x n] = tc_split_state_bytes(n)
- * = 10.125 n bytes instead of the full 12 n. The fp32 master is
- * (hi << 16) | lo with hi = the bf16 parameter B minus the round bit rb_i
- * (for a NaN B: B with its quiet bit cleared when rb_i is set) -- exact for
- * every fp32 value, because the update writes B = RNE(master) itself.
- * tc_adamw_split_master updates such a state in place, reading the current
- * `param` (bf16, n) and writing the new one; results are bit-identical to
- * tc_adamw on the expanded state (same arithmetic). */
+/* Packed split-master optimizer state (what the engine keeps on the host for
+ * a parameter that never lives in NVMe), n % 2048 == 0, in the state's own
+ * 12n-byte buffer: a prefix of tc_split_state_bytes(n) = 9.19 n bytes (what
+ * crosses PCIe) and a 2n-byte overflow area behind it.
+ *  - fp32 master: its low 16 bits + one round bit rb_i; the high half is the
+ *    bf16 parameter B minus rb_i (for a NaN B: B with its quiet bit cleared
+ *    when rb_i is set) -- exact for every fp32 value, because the update
+ *    writes B = RNE(master) itself;
+ *  - m, v: sign and 23 mantissa bits as stored; the 8-bit exponents coded
+ *    against the largest exponent of each 32-element group (m: 5-bit offset,
+ *    v: 4-bit offset, plus a code for exponent 0); a 2048-element tile with a
+ *    value outside those windows keeps its raw exponents in the overflow area.
+ * Lossless for every bit pattern. tc_adamw_split_master updates such a state
+ * in place, reading the current `param` (bf16, n) and writing the new one;
+ * results are bit-identical to tc_adamw on the expanded state. */
 uint64_t tc_split_state_bytes(uint64_t n);
 int tc_adamw_split_master(void* split_state, const void* grad, void* param, uint64_t n, double lr, double beta1,
                           double beta2, double eps, double weight_decay, int64_t step, float grad_scale,
                           void* stream);
-/* Codec between the split and the full [p32|m|v] layouts (device buffers,
- * out of place). compress sets *d_mismatch (a device u32, never cleared) to
- * nonzero when some p32 does not round to its bf16 param: not representable. */
+/* Codec between the packed split (12n bytes) and the full [p32|m|v] layouts
+ * (device buffers, out of place). compress sets *d_mismatch (a device u32,
+ * never cleared) to nonzero when some p32 does not round to its bf16 param:
+ * not representable split. */
 int tc_state_expand(const void* split_state, const void* param, float* full_state, uint64_t n, void* stream);
 int tc_state_compress(const float* full_state, const void* param, void* split_state, uint64_t n,
                       uint32_t* d_mismatch, void* stream);

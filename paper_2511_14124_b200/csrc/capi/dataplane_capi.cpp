@@ -125,7 +125,7 @@ int tc_adamw_batch(const tc_adam_chunk* chunks, uint32_t count, double lr, doubl
   return cuda_status(e, "tc_adamw_batch");
 }
 
-uint64_t tc_split_state_bytes(uint64_t n) { return split_layout(n).bytes; }
+uint64_t tc_split_state_bytes(uint64_t n) { return packed_layout(n).bytes; }
 
 int tc_adamw_split_master(void* split_state, const void* grad, void* param, uint64_t n, double lr, double beta1,
                           double beta2, double eps, double weight_decay, int64_t step, float grad_scale,
@@ -135,10 +135,8 @@ int tc_adamw_split_master(void* split_state, const void* grad, void* param, uint
   if (n == 0) return TC_OK;
   if (!split_state || !grad || !param) return set_error(TC_EARG, "tc_adamw_split_master: null buffer");
   auto* b = static_cast<std::uint8_t*>(split_state);
-  const SplitLayout L = split_layout(n);
-  AdamChunk c{nullptr, reinterpret_cast<float*>(b + L.m), reinterpret_cast<float*>(b + L.v),
-              static_cast<const std::uint16_t*>(grad), static_cast<std::uint16_t*>(param), n,
-              reinterpret_cast<std::uint16_t*>(b + L.lo), reinterpret_cast<std::uint32_t*>(b + L.rb)};
+  AdamChunk c{nullptr, nullptr, nullptr, static_cast<const std::uint16_t*>(grad), static_cast<std::uint16_t*>(param), n,
+              b, b + packed_layout(n).ovf};
   const cudaError_t e = launch_adamw_batch(&c, 1, adam_scalars(lr, beta1, beta2, eps, weight_decay, step), grad_scale,
                                            as_stream(stream));
   if (e == cudaErrorInvalidValue) {

@@ -20,13 +20,26 @@ AdamScalars adam_scalars(double lr, double b1, double b2, double eps, double wd,
 // One chunk of a batched AdamW launch: n elements (a multiple of 8) at
 // 16-byte aligned addresses; pout may be null.
 //
-// Split-master chunks (lo != null; n a multiple of kSplitTile): the fp32
-// master is not stored whole. Its high half is the bf16 parameter at `pout`
-// (the update's own RNE output, kept in HBM) up to one rounding step, so the
-// state carries only the low half `lo` (u16) and one round bit per element in
-// `rb` (bit i of word i/32): H = B - rb for a non-NaN B, H = rb ? B & ~0x40 : B
-// for a NaN B (the cast sets the quiet bit). Exact for every fp32 value; the
-// kernel reads (lo, rb, B) and writes (lo', rb', B'). p is unused.
+// Packed split-master chunks (packed != null; n a multiple of kSplitTile):
+// the state is not stored as [p32 | m | v] but in the PackedLayout below.
+//  * The fp32 master's high half is the bf16 parameter at `pout` (the update's
+//    own RNE output, kept in HBM) up to one rounding step: the state carries
+//    the low half `lo` and one round bit rb per element: hi = B - rb for a
+//    non-NaN B, hi = rb ? B & ~0x40 : B for a NaN B (the cast sets the quiet
+//    bit). Exact for every fp32 value.
+//  * m and v keep bits 0-23 (mantissa + the exponent's lowest bit) as they
+//    are; byte 3 (sign + the exponent's top 7 bits) is coded against the
+//    largest top-7 value of each 32-element group: m as a 4-bit offset (14 =
+//    top bits zero) with its sign, v as a 5-bit offset (30 = zero; v's sign
+//    is not stored). A tile (2048 elements) with any value outside those
+//    windows (or a negative v) is an overflow tile: byte 3 of its m's and v's
+//    lives in `ovf` (2 B/element), read and written by the kernel itself
+//    through a device-accessible pointer (the mapped tail of the state's
+//    pinned host slot), so the bytes that cross PCIe have a fixed size.
+//    Bytes are moved with byte permutes and SWAR arithmetic on 4 elements at
+//    a time.
+// The kernel reads (lo, rb, B, planes) and writes (lo', rb', B', planes').
+// p, m, v are unused for packed chunks.
 struct AdamChunk {
   float* p;
   float* m;
@@ -34,24 +47,46 @@ struct AdamChunk {
   const std::uint16_t* g;
   std::uint16_t* pout;
   std::uint64_t n;
-  std::uint16_t* lo = nullptr;
-  std::uint32_t* rb = nullptr;
+  std::uint8_t* packed = nullptr;  // PackedLayout prefix (HBM stage)
+  std::uint8_t* ovf = nullptr;     // 2n bytes: raw exponents of overflow tiles (device-accessible)
 };
-constexpr std::uint64_t kSplitTile = 2048;  // elements per AdamW tile; split chunks hold whole tiles
+constexpr std::uint64_t kSplitTile = 2048;  // elements per AdamW tile; packed chunks hold whole tiles
 
-// Layout of a split state chunk of n parameters (n % kSplitTile == 0) inside
-// the state's 12n-byte slot: [lo: 2n][rb: n/8][m: 4n][v: 4n] — 10.125n bytes,
-// the prefix that crosses PCIe.
-struct SplitLayout {
-  std::uint64_t n, lo, rb, m, v, bytes;
-};
 #ifdef __CUDACC__
 #define TCB_HD __host__ __device__
 #else
 #define TCB_HD
 #endif
-TCB_HD inline SplitLayout split_layout(std::uint64_t n) {
-  return SplitLayout{n, 0, 2 * n, 2 * n + n / 8, 2 * n + n / 8 + 4 * n, 2 * n + n / 8 + 8 * n};
+
+// Byte offsets of the planes of a packed state of n parameters (n %
+// kSplitTile == 0) inside its 12n-byte slot; [0, bytes) crosses PCIe
+// (9.44 B/param), [ovf, ovf + 2n) is the overflow area. Per element:
+// lo u16 | rb 1 bit | mlo u16 (m bits 0-15) | mb2 u8 (m bits 16-23) | vlo u16 |
+// vb2 u8 | code u8 (m sign << 7 | m code << 3 | v code bits 0-2) | x2 2 bits
+// (v code bits 3-4); per 32-element group: base u16 (m's largest top-7 |
+// v's << 8); per tile: flags u32 (1 = overflow tile). The windows (m: 13
+// steps of 2 binades, v: 29) cover the moments of a run whose gradient never
+// changes (v ~ g^2 spans twice g's binades); an EMA over changing gradients
+// is narrower.
+struct PackedLayout {
+  std::uint64_t n, lo, rb, mlo, mb2, vlo, vb2, code, x2, base, flags, bytes, ovf;
+};
+TCB_HD inline PackedLayout packed_layout(std::uint64_t n) {
+  PackedLayout L{};
+  L.n = n;
+  L.lo = 0;
+  L.rb = 2 * n;
+  L.mlo = L.rb + n / 8;
+  L.mb2 = L.mlo + 2 * n;
+  L.vlo = L.mb2 + n;
+  L.vb2 = L.vlo + 2 * n;
+  L.code = L.vb2 + n;
+  L.x2 = L.code + n;
+  L.base = L.x2 + n / 4;
+  L.flags = L.base + n / 16;
+  L.bytes = (L.flags + n / 512 + 15) / 16 * 16;
+  L.ovf = L.bytes;
+  return L;
 }
 constexpr int kMaxAdamChunks = 8;
 struct AdamBatch {  // kernel parameter: the chunks and their first tile in the launch's tile space
@@ -90,14 +125,15 @@ cudaError_t launch_fill_normal_bf16(std::uint16_t* out, std::uint64_t n, float s
                                     std::uint64_t stream_id, cudaStream_t st);
 // Optimizer-state init from bf16 params: p32 = float(param), m = v = 0.
 cudaError_t launch_init_state(const std::uint16_t* param, float* state, std::uint64_t n, cudaStream_t st);
-// Split-master codec (layout above), out of place, n % kSplitTile == 0:
-// expand: [lo|rb|m|v] + bf16 params -> full [p32|m|v];
-// compress: full + bf16 params -> [lo|rb|m|v]; *mismatch (device word, set
-// to nonzero, never cleared) when some p32 does not round to its bf16 param,
+// Packed split-master codec (layout above), out of place, n % kSplitTile == 0;
+// `packed` is a whole 12n-byte state (prefix + overflow area):
+// expand: packed + bf16 params -> full [p32|m|v];
+// compress: full + bf16 params -> packed; *mismatch (device word, set to
+// nonzero, never cleared) when some p32 does not round to its bf16 param,
 // i.e. the state is not representable split.
-cudaError_t launch_state_expand(const std::uint8_t* split, const std::uint16_t* param, float* full, std::uint64_t n,
+cudaError_t launch_state_expand(const std::uint8_t* packed, const std::uint16_t* param, float* full, std::uint64_t n,
                                 cudaStream_t st);
-cudaError_t launch_state_compress(const float* full, const std::uint16_t* param, std::uint8_t* split, std::uint64_t n,
+cudaError_t launch_state_compress(const float* full, const std::uint16_t* param, std::uint8_t* packed, std::uint64_t n,
                                   unsigned* mismatch, cudaStream_t st);
 
 int num_sms();

@@ -157,6 +157,11 @@ Executor::UpdateJob Executor::prepare_update(TensorRec& s, TensorRec& p) {
     k = (k + 1) % pout_scratch_[p.bytes].size();
   }
   if (j.state_on_gpu && s.split) throw DeviceError(TC_EINTERNAL, "split optimizer state moved into HBM");
+  if (j.split) {  // the kernel reads and writes the overflow area in the state's pinned slot directly
+    Slot& h = slot_of(s);
+    j.ovf = h.dptr + packed_layout(j.n).ovf;
+    wait_for_write(ost, h.sync);
+  }
   if (j.split && !j.on_gpu) {  // the master's high half: the parameter's bytes from its host slot into the scratch
     if (p.tier != PTier::HostParam)
       throw DeviceError(TC_EINTERNAL, "split optimizer state " + std::to_string(s.id) + ": parameter in NVMe");
@@ -193,10 +198,7 @@ void Executor::run_updates(std::vector<UpdateJob>& jobs) {
     const auto* g = reinterpret_cast<const std::uint16_t*>(j.p->grad);
     auto* pout = reinterpret_cast<std::uint16_t*>(j.pout);
     if (j.split) {
-      const SplitLayout L = split_layout(j.n);
-      chunks.push_back(AdamChunk{nullptr, reinterpret_cast<float*>(j.stg + L.m), reinterpret_cast<float*>(j.stg + L.v),
-                                 g, pout, j.n, reinterpret_cast<std::uint16_t*>(j.stg + L.lo),
-                                 reinterpret_cast<std::uint32_t*>(j.stg + L.rb)});
+      chunks.push_back(AdamChunk{nullptr, nullptr, nullptr, g, pout, j.n, j.stg, j.ovf});
       ++stats_.split_updates;
       stats_.split_elems += j.n;
     } else {

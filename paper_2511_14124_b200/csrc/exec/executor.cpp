@@ -77,7 +77,7 @@ static std::uint8_t* pin_region(std::uint64_t bytes, std::uint64_t* mapped_len) 
       std::memset(static_cast<char*>(p) + b, 0, e - b);
     });
   for (auto& t : th) t.join();
-  if (cudaHostRegister(p, bytes, cudaHostRegisterPortable) != cudaSuccess) {
+  if (cudaHostRegister(p, bytes, cudaHostRegisterPortable | cudaHostRegisterMapped) != cudaSuccess) {
     cudaGetLastError();
     munmap(p, bytes);
     return nullptr;
@@ -116,7 +116,18 @@ void SlotPool::allocate(bool device, int dev) {
     mapped_.assign(pieces.size(), 0);
     for (std::size_t r = 0; r < pieces.size(); ++r) {
       regions_[r] = pin_region(pieces[r], &mapped_[r]);
-      if (!regions_[r]) TCB_CK(cudaHostAlloc(reinterpret_cast<void**>(&regions_[r]), pieces[r], cudaHostAllocPortable));
+      if (!regions_[r])
+        TCB_CK(cudaHostAlloc(reinterpret_cast<void**>(&regions_[r]), pieces[r], cudaHostAllocPortable | cudaHostAllocMapped));
+    }
+  }
+  std::vector<std::uint8_t*> dev_base(pieces.size(), nullptr);  // host regions: device-side alias (kernels' zero-copy)
+  for (std::size_t r = 0; r < pieces.size(); ++r) {
+    if (device) {
+      dev_base[r] = regions_[r];
+    } else {
+      void* d = nullptr;
+      TCB_CK(cudaHostGetDevicePointer(&d, regions_[r], 0));
+      dev_base[r] = static_cast<std::uint8_t*>(d);
     }
   }
   for (std::size_t r = 0; r < pieces.size(); ++r) {
@@ -126,6 +137,7 @@ void SlotPool::allocate(bool device, int dev) {
       c.size = slots[k].first;
       Slot sl;
       sl.ptr = regions_[r] + off;
+      sl.dptr = dev_base[r] + off;
       off += slots[k].first;
       c.free_fifo.push_back(static_cast<std::uint32_t>(c.slots.size()));
       c.slots.push_back(sl);
@@ -518,7 +530,7 @@ int Executor::auto_stage_slots(double fwd_h2d) const {
     if (st.phase == Phase::Forward) fwd_us += st.compute_us * cfg_.batch_scale;
   for (const auto& r : recs_)
     if (r.is_state) {  // bytes a load moves (split-master prefix where eligible)
-      sbytes = std::max(sbytes, static_cast<double>(r.split_ok ? split_layout(r.bytes / 12).bytes : r.bytes));
+      sbytes = std::max(sbytes, static_cast<double>(r.split_ok ? packed_layout(r.bytes / 12).bytes : r.bytes));
       alloc = std::max(alloc, static_cast<double>(r.bytes));
       ++nstates;
     }
@@ -924,7 +936,7 @@ void Executor::seed(std::uint64_t seed) {
       std::uint8_t* pv = p.tier == PTier::Gpu ? where(p) : tmp;
       std::uint8_t* sdst = stage_[1];
       s.split = s.split_ok;
-      if (s.split)  // master = float(param): low halves and round bits zero, moments zero
+      if (s.split)  // master = float(param): low halves, round bits, moments, codes, flags all zero
         TCB_CK(cudaMemset(sdst, 0, s.bytes));
       else
         TCB_CK(launch_init_state(reinterpret_cast<const std::uint16_t*>(pv), reinterpret_cast<float*>(sdst), n, nullptr));
@@ -989,13 +1001,14 @@ void Executor::state_to_full(TensorRec& s, const void* stored_host, void* full_h
   TensorRec& p = recs_[static_cast<std::size_t>(s.partner)];
   drop_staged();
   const std::uint16_t* B = param_bits_dev(p);
-  TCB_CK(cudaMemcpy(stage_[0], stored_host, state_xfer_bytes(s), cudaMemcpyHostToDevice));
+  TCB_CK(cudaMemcpy(stage_[0], stored_host, s.bytes, cudaMemcpyHostToDevice));  // prefix + overflow area
   TCB_CK(launch_state_expand(stage_[0], B, reinterpret_cast<float*>(stage_[1]), p.bytes / 2, nullptr));
   TCB_CK(cudaMemcpy(full_host, stage_[1], s.bytes, cudaMemcpyDeviceToHost));
 }
 
-// Full layout -> split, on the GPU, into stage 1; false when some master does
-// not round to the parameter's bf16 value (not representable split).
+// Full layout -> packed split (prefix + overflow area), on the GPU, into
+// stage 1; false when some master does not round to the parameter's bf16
+// value (not representable split).
 bool Executor::state_from_full(TensorRec& s, const void* full_host, std::uint8_t* stored_dev) {
   TensorRec& p = recs_[static_cast<std::size_t>(s.partner)];
   drop_staged();
@@ -1054,7 +1067,7 @@ void Executor::write_tensor(TensorId id, const void* src, std::uint64_t bytes) {
   if (r.is_state && r.split_ok) {
     if (state_from_full(r, src, stage_[1])) {
       std::vector<std::uint8_t> stored(r.bytes, 0);
-      TCB_CK(cudaMemcpy(stored.data(), stage_[1], split_layout(r.bytes / 12).bytes, cudaMemcpyDeviceToHost));
+      TCB_CK(cudaMemcpy(stored.data(), stage_[1], r.bytes, cudaMemcpyDeviceToHost));  // prefix + overflow area
       r.split = true;
       store_state_host(r, stored.data());
       return;

@@ -86,6 +86,7 @@ enum class PTier : std::uint8_t { Gpu, HostParam, HostOpt, Nvme };
 
 struct Slot {
   std::uint8_t* ptr = nullptr;
+  std::uint8_t* dptr = nullptr;  // the same bytes as seen by kernels (host slots: mapped pinned memory)
   SlotSync sync;
   std::int32_t occupant = -1;  // tensor index
 };
@@ -136,9 +137,9 @@ struct TensorRec {
   bool has_home = false, home_valid = false;
   PTier home_tier = PTier::HostParam;
   std::uint32_t home_slot = 0;
-  // States: held split on the host (dataplane.cuh SplitLayout: the master's
+  // States: held split on the host (dataplane.cuh PackedLayout: the master's
   // high half is the partner parameter's bf16 value, which only the update
-  // writes). split_ok (dry run of the policy's decisions): the partner never
+  // writes; the moments' exponents coded per 32-element group). split_ok (dry run of the policy's decisions): the partner never
   // lives in NVMe (its bytes are in HBM or pinned memory at every update),
   // the state never moves into HBM, and the chunk is whole AdamW tiles.
   bool split = false, split_ok = false;
@@ -298,11 +299,12 @@ class Executor {
     std::size_t b = 0;            // stage index (host-resident states)
     std::uint8_t* pout = nullptr;  // bf16 result (the parameter's GPU slot or a scratch buffer)
     SlotSync* psync = nullptr;
-    bool split = false;            // stg holds [lo|rb|m|v] (SplitLayout); pout is also the master's high half
+    bool split = false;            // stg holds the PackedLayout prefix; pout is also the master's high half
+    std::uint8_t* ovf = nullptr;   // split: the overflow area (tail of the state's pinned slot, mapped)
   };
-  // bytes of a host-resident state that cross PCIe (its split prefix or all of it)
+  // bytes of a host-resident state that cross PCIe (its packed prefix or all of it)
   std::uint64_t state_xfer_bytes(const TensorRec& s) const {
-    return s.split ? split_layout(s.bytes / 12).bytes : s.bytes;
+    return s.split ? packed_layout(s.bytes / 12).bytes : s.bytes;
   }
   // state bytes as stored (split or full) <-> the full [p32|m|v] layout, on the GPU
   void state_to_full(TensorRec& s, const void* stored_host, void* full_host);

@@ -86,20 +86,21 @@ def adamw_batch(chunks, lr, beta1, beta2, eps, weight_decay, step, grad_scale=1.
 
 
 def split_state_bytes(n):
-    """Bytes of a split-master state of n parameters ([lo u16 | round bits | m | v])."""
+    """Bytes of a packed split-master state of n parameters that cross PCIe (the
+    prefix of its 12n-byte buffer; the rest is the overflow area)."""
     return int(N.lib().tc_split_state_bytes(n))
 
 
 def adamw_split_master(split_state, grad, param, lr, beta1, beta2, eps, weight_decay, step, grad_scale=1.0,
                        stream=None):
-    """In-place AdamW on a split-master state (uint8 [split_state_bytes(n)]); param (bf16 [n]) is the master's
-    high half on input and the updated bf16 parameter on output."""
+    """In-place AdamW on a packed split-master state (uint8 [12n]); param (bf16 [n]) is the master's high half on
+    input and the updated bf16 parameter on output."""
     N.check(N.lib().tc_adamw_split_master(_dev(split_state), _dev(grad), _dev(param), grad.numel(), lr, beta1, beta2,
                                           eps, weight_decay, step, grad_scale, _stream(stream)))
 
 
 def state_expand(split_state, param, out=None, stream=None):
-    """split-master state + bf16 params -> full fp32 [p32 | m | v]."""
+    """packed split-master state (uint8 [12n]) + bf16 params -> full fp32 [p32 | m | v]."""
     n = param.numel()
     out = out if out is not None else torch.empty(3 * n, dtype=torch.float32, device=param.device)
     N.check(N.lib().tc_state_expand(_dev(split_state), _dev(param), _dev(out), n, _stream(stream)))
@@ -107,9 +108,9 @@ def state_expand(split_state, param, out=None, stream=None):
 
 
 def state_compress(full_state, param, out=None, stream=None):
-    """full fp32 [p32 | m | v] + bf16 params -> (split-master state, representable: bool; syncs)."""
+    """full fp32 [p32 | m | v] + bf16 params -> (packed split-master state uint8 [12n], representable: bool; syncs)."""
     n = param.numel()
-    out = out if out is not None else torch.empty(split_state_bytes(n), dtype=torch.uint8, device=param.device)
+    out = out if out is not None else torch.zeros(12 * n, dtype=torch.uint8, device=param.device)
     flag = torch.zeros(1, dtype=torch.int32, device=param.device)
     N.check(N.lib().tc_state_compress(_dev(full_state), _dev(param), _dev(out), n, _dev(flag), _stream(stream)))
     return out, int(flag.item()) == 0

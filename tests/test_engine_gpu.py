@@ -75,11 +75,16 @@ def check_engine(tr, m, cfg, iters=2, nvme_dir="", hoist=True, prestage=True, st
     return st
 
 
+def packed_bytes(n):
+    """PCIe bytes of a packed split-master state of n parameters (dataplane.cuh PackedLayout)."""
+    return (9 * n + n // 8 + n // 4 + n // 16 + n // 512 + 15) // 16 * 16
+
+
 def assert_state_traffic(st, iters, n, S):
     """Every state crossed PCIe exactly once per direction per iteration, as
-    its split-master prefix (10.125 B/param; + the bf16 parameter H2D when
-    that is not in HBM at the update)."""
-    split_b = 10 * (S // 2) + S // 16
+    its packed split-master prefix (9.44 B/param; + the bf16 parameter H2D
+    when that is not in HBM at the update)."""
+    split_b = packed_bytes(S // 2)
     assert st["opt_logical_bytes"] == 2 * iters * n * 6 * S
     assert st["split_updates"] == iters * n
     assert st["opt_d2h_bytes"] == iters * n * split_b
@@ -108,16 +113,15 @@ def test_fig8_shape(tmpd, pol, ro, hoist):
 @pytest.mark.parametrize("full_master", [False, True])
 @pytest.mark.parametrize("gpu_chunks", [6, 3])
 def test_split_master_states(tmpd, full_master, gpu_chunks):
-    """Optimizer states cross PCIe split (low half + round bit, 10.125 B/param
-    instead of 12); when the parameter is not in HBM at its update its bf16
+    """Optimizer states cross PCIe packed split (master low half + round bit,
+    moments with group-coded exponents: 9.44 B/param instead of 12); when the parameter is not in HBM at its update its bf16
     bytes (the master's high half) come along. Either way every state,
     parameter and access checksum is bit-exact with the oracle after every
     iteration (check_engine)."""
     S, n_p, iters = 8192, 6, 3
     tr, m = write_with_states(tmpd, "sm", [S] * n_p, gpu_chunks * S, n_p * S + n_p * 6 * S, iters=iters)
     st = check_engine(tr, m, {"policy": "tencache"}, iters=iters, full_master=full_master)
-    n = S // 2
-    split_b = 2 * n + n // 8 + 8 * n
+    split_b = packed_bytes(S // 2)
     assert st["opt_logical_bytes"] == 2 * iters * n_p * 6 * S
     if full_master:
         assert st["split_updates"] == 0
@@ -532,6 +536,14 @@ def test_split_master_rewrites(tmpd, gpu_chunks):
     st3[2 * k:] = np.abs(st3[2 * k:])
     states[n_p + 3] = st3
     e.write_tensor(n_p + 3, st3)
+    # (4) consistent, with moments spread over ~100 binades: split, every tile
+    # an overflow tile (raw exponents in the pinned slot's tail, which the
+    # kernel reads and writes through the mapped pointer)
+    st4 = states[n_p + 4].copy()
+    st4[k:2 * k] = (rng.standard_normal(k) * np.exp2(rng.integers(-60, 40, k))).astype(np.float32)
+    st4[2 * k:] = np.abs(rng.standard_normal(k) * np.exp2(rng.integers(-90, 10, k))).astype(np.float32)
+    states[n_p + 4] = st4
+    e.write_tensor(n_p + 4, st4)
     for sid in states:
         assert np.array_equal(e.read_tensor(sid, 6 * S).view(np.uint32), states[sid].view(np.uint32)), sid
     e.reset_stats()

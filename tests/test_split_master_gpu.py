@@ -45,20 +45,75 @@ def special_masters(n, seed):
     return bits
 
 
+def layout(n):
+    """Byte offsets of the packed planes (dataplane.cuh PackedLayout)."""
+    rb = 2 * n
+    mlo = rb + n // 8
+    mb2 = mlo + 2 * n
+    vlo = mb2 + n
+    vb2 = vlo + 2 * n
+    code = vb2 + n
+    x2 = code + n
+    base = x2 + n // 4
+    flags = base + n // 16
+    return {"flags": flags, "bytes": (flags + n // 512 + 15) // 16 * 16}
+
+
+def overflow_tiles(packed, n):
+    f = packed[layout(n)["flags"]:layout(n)["flags"] + 4 * (n // 2048)].cpu().numpy().view(np.uint32)
+    return np.nonzero(f & 1)[0]
+
+
+def typical_moments(n, seed):
+    g = np.random.default_rng(seed).standard_normal((20, n)).astype(np.float32) * 1e-3
+    m = np.zeros(n, np.float32)
+    v = np.zeros(n, np.float32)
+    for t in range(20):
+        m = np.float32(0.9) * m + np.float32(0.1) * g[t]
+        v = np.float32(0.999) * v + np.float32(0.001) * g[t] * g[t]
+    return m, v
+
+
 @pytest.mark.parametrize("n", [2048, 2048 * 37])
 def test_codec_exact_for_every_pattern(n):
+    """Masters of every class, and moments from a typical run (no overflow
+    tile) to every bit pattern (wide exponent spreads, zeros, denormals,
+    NaN/Inf, negative v: overflow tiles) -- all round-trip bit for bit."""
     bits = special_masters(n, n)
     p32 = torch.from_numpy(bits.view(np.float32).copy()).to(DEV)
-    m = torch.randn(n, device=DEV) * 1e-4
-    v = torch.rand(n, device=DEV) * 1e-6
-    full = torch.cat([p32, m, v])
     param = K.cast_f32_to_bf16(p32)  # the engine's own rounding: B = RNE(master)
+    m, v = typical_moments(n, n)
+    full = torch.cat([p32, torch.from_numpy(m).to(DEV), torch.from_numpy(v).to(DEV)])
     split, ok = K.state_compress(full, param)
     assert ok
-    assert split.numel() == K.split_state_bytes(n) == 2 * n + n // 8 + 8 * n
-    back = K.state_expand(split, param)
+    assert split.numel() == 12 * n
+    assert K.split_state_bytes(n) == layout(n)["bytes"] == (9 * n + n // 8 + n // 4 + n // 16 + n // 512 + 15) // 16 * 16
+    assert len(overflow_tiles(split, n)) == 0  # typical moments fit the exponent windows
+    assert np.array_equal(u32(K.state_expand(split, param)), u32(full))
+    # the bench's moments (one gradient reused every step: v ~ g^2 spans twice g's binades)
+    g = (np.random.default_rng(n + 2).standard_normal(n).astype(np.float32) * 1e-3)
+    g = torch.from_numpy(g).to(torch.bfloat16).float().numpy()
+    mf, vf = np.float32(1 - 0.9 ** 3) * g, np.float32(1 - 0.999 ** 3) * g * g
+    full_f = torch.cat([p32, torch.from_numpy(mf).to(DEV), torch.from_numpy(vf).to(DEV)])
+    split_f, ok = K.state_compress(full_f, param)
+    assert ok and len(overflow_tiles(split_f, n)) <= max(1, n // 2048 // 100)
+    assert np.array_equal(u32(K.state_expand(split_f, param)), u32(full_f))
+    # arbitrary moments: every fp32 pattern, in a third of the tiles
+    rng = np.random.default_rng(n + 1)
+    mm, vv = m.copy().view(np.uint32), v.copy().view(np.uint32)
+    tiles = n // 2048
+    wild = rng.choice(tiles, max(1, tiles // 3), replace=False)
+    for t in wild:
+        sl = slice(2048 * t, 2048 * (t + 1))
+        mm[sl] = special_masters(2048, int(t) + 7)
+        vv[sl] = rng.integers(0, 1 << 32, 2048, dtype=np.uint64).astype(np.uint32)
+    full2 = torch.cat([p32, torch.from_numpy(mm.view(np.float32)).to(DEV), torch.from_numpy(vv.view(np.float32)).to(DEV)])
+    split2, ok = K.state_compress(full2, param)
+    assert ok
+    assert set(overflow_tiles(split2, n).tolist()) == set(int(t) for t in wild)
+    back = K.state_expand(split2, param)
     torch.cuda.synchronize()
-    assert np.array_equal(u32(back), u32(full))  # bit-exact, NaN payloads included
+    assert np.array_equal(u32(back), u32(full2))  # bit-exact, NaN payloads included
 
 
 def test_compress_reports_unrepresentable():

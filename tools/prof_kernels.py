@@ -60,15 +60,16 @@ timeit("adamw_batch_4xC2", lambda i: K.adamw_batch(chunks, 1e-4, 0.9, 0.999, 1e-
        "4 C2 chunks in one launch (the executor's batched hoisted updates)")
 timeit("adamw_1xC2", lambda i: K.adamw(chunks[0][0], chunks[0][1], chunks[0][2], 1e-4, 0.9, 0.999, 1e-8, 0.01, i + 1),
        28 * c2, "one C2 chunk (470 MB, L2-resident tail)")
-# split-master AdamW: 26.25 B/elem (lo + round bit + bf16 param + m + v in and out, g in)
+# packed split-master AdamW: 24.875 B/elem (lo 2 + round bit 1/8 + bf16 param 2 + m, v planes 7.25 + group
+# bases 1/16 in and out, g 2 in)
 sstate, ok = K.state_compress(state, K.cast_f32_to_bf16(state[:n]), stream=None)
 assert ok
 sparam = K.cast_f32_to_bf16(state[:n])
 timeit("adamw_split_master_64M", lambda i: K.adamw_split_master(sstate, grad, sparam, 1e-4, 0.9, 0.999, 1e-8, 0.01,
-                                                               i + 1), int(26.25 * n),
+                                                               i + 1), int(24.875 * n),
        "one chunk of 64 Mi elements, split-master state (the engine's host format)")
 full_out = torch.empty(3 * n, dtype=torch.float32, device=dev)
-timeit("state_expand_64M", lambda i: K.state_expand(sstate, sparam, out=full_out), int((2 + 0.125 + 2 + 8 + 12) * n),
+timeit("state_expand_64M", lambda i: K.state_expand(sstate, sparam, out=full_out), int((11.4375 + 2 + 12) * n),
        "split -> full layout (read/write tensor path)")
 del state, grad, pout, chunks, sstate, sparam, full_out
 # casts: 6 B/elem
