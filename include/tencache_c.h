@@ -159,16 +159,17 @@ int tc_adamw_batch(const tc_adam_chunk* chunks, uint32_t count, double lr, doubl
                    double weight_decay, int64_t step, float grad_scale, void* stream);
 /* Packed split-master optimizer state (what the engine keeps on the host for
  * a parameter that never lives in NVMe), n % 2048 == 0, in the state's own
- * 12n-byte buffer: a prefix of tc_split_state_bytes(n) = 9.19 n bytes (what
+ * 12n-byte buffer: a prefix of tc_split_state_bytes(n) = 9.44 n bytes (what
  * crosses PCIe) and a 2n-byte overflow area behind it.
  *  - fp32 master: its low 16 bits + one round bit rb_i; the high half is the
  *    bf16 parameter B minus rb_i (for a NaN B: B with its quiet bit cleared
  *    when rb_i is set) -- exact for every fp32 value, because the update
  *    writes B = RNE(master) itself;
- *  - m, v: sign and 23 mantissa bits as stored; the 8-bit exponents coded
- *    against the largest exponent of each 32-element group (m: 5-bit offset,
- *    v: 4-bit offset, plus a code for exponent 0); a 2048-element tile with a
- *    value outside those windows keeps its raw exponents in the overflow area.
+ *  - m, v: bytes 0-2 as stored; byte 3 (sign + top 7 exponent bits) coded
+ *    against the largest top-7 value of each 32-element group (m: sign +
+ *    4-bit offset, v: 5-bit offset, each with a code for zero); a
+ *    2048-element tile with a value outside those windows keeps byte 3 of
+ *    its moments in the overflow area.
  * Lossless for every bit pattern. tc_adamw_split_master updates such a state
  * in place, reading the current `param` (bf16, n) and writing the new one;
  * results are bit-identical to tc_adamw on the expanded state. */

@@ -521,8 +521,10 @@ std::map<std::pair<int, std::uint64_t>, std::uint32_t> Executor::simulate_occupa
 // own cache prefetches), plus the backward's lookahead; at least 12, at most
 // half the free HBM. Measured optima it reproduces: 12 on C2 at 16k tokens,
 // ~118 on C5 (profiles/r01_stage_sweep.json). Without forward prefetches the
-// forward's time is taken 1.5x the model's (it runs longer under load, and
-// the prologue then fills the ring: forward_prestage_budget).
+// forward's time is taken 2x the model's (it runs longer under load — at
+// 1.5x the C3 H2D link still idled ~35 ms per step before the backward freed
+// a stage, profiles/r02_timeline_c3.json — and the prologue then fills the
+// ring: forward_prestage_budget).
 int Executor::auto_stage_slots(double fwd_h2d) const {
   double fwd_us = 0, sbytes = 0, alloc = 0;
   std::size_t nstates = 0;
@@ -541,7 +543,7 @@ int Executor::auto_stage_slots(double fwd_h2d) const {
   } catch (...) {
     return 12;
   }
-  const double spare = std::max(0.0, (fwd_h2d == 0 ? 1.5 : 1.0) * fwd_us * bw - fwd_h2d);
+  const double spare = std::max(0.0, (fwd_h2d == 0 ? 2.0 : 1.0) * fwd_us * bw - fwd_h2d);
   std::size_t n = static_cast<std::size_t>(spare / sbytes) + 4;
   std::size_t free_b = 0, total_b = 0;
   if (cudaMemGetInfo(&free_b, &total_b) == cudaSuccess)

@@ -323,12 +323,14 @@ class Executor {
   std::vector<std::pair<std::int32_t, std::int32_t>> deferred_;  // hoisted updates waiting for a batch
   // Hoisted updates per fused AdamW launch. On its own stream (compute-bound
   // traces, ZeRO-3) each launch waits for SMs behind the concurrent layer
-  // compute and pays the front-end latency of a second stream: batches of 4
-  // amortise that (C3: event-timed 0.45 -> 0.71 of the HBM peak, step time
-  // unchanged). On the compute stream (migration-bound) single updates keep
-  // each state's write-back earliest (C2 steps 2-4 % shorter,
-  // profiles/r02_adam_batch_ab.json). TC_ADAM_BATCH overrides (1..8).
-  static constexpr std::size_t kAdamBatchConcurrent = 4;
+  // compute and pays the front-end latency of a second stream: batches of 8
+  // amortise that (C3, packed states: event-timed 0.34 / 0.42 / 0.49 / 0.54
+  // of the HBM peak at 1 / 2 / 4 / 8, step time unchanged,
+  // profiles/r02_adam_batch_packed.json). On the compute stream
+  // (migration-bound) single updates keep each state's write-back earliest
+  // (C2 steps 2-4 % shorter, profiles/r02_adam_batch_ab.json). TC_ADAM_BATCH
+  // overrides (1..8).
+  static constexpr std::size_t kAdamBatchConcurrent = 8;
   std::size_t adam_batch_env_ = 0;
   std::size_t adam_batch() const { return adam_batch_env_ ? adam_batch_env_ : adam_stream() == opt_ ? kAdamBatchConcurrent : 1; }
   std::size_t stage_state(TensorRec& s);

@@ -77,3 +77,14 @@ def test_policy_call_overflow_is_not_lost(tmpd):
     _, step, hook, reqs = calls[k + 1]
     assert L.tc_policy_call(h, code[hook], step, buf, 64, C.byref(n)) == N.TC_OK and n.value == len(reqs)
     L.tc_policy_destroy(h)
+
+
+def test_packed_state_layout_fits_its_slot():
+    """tc_split_state_bytes: the packed split-master prefix (9.44 B/param,
+    16-byte multiple) plus its 2 B/param overflow area fit the reference's
+    12 B/param state slot (no GPU needed)."""
+    from paper_2511_14124_b200 import _native as N
+    for n in (2048, 4096, 2048 * 37, 16865280):
+        b = N.lib().tc_split_state_bytes(n)
+        assert b == (9 * n + n // 8 + n // 4 + n // 16 + n // 512 + 15) // 16 * 16
+        assert b % 16 == 0 and b + 2 * n <= 12 * n
