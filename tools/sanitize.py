@@ -29,6 +29,17 @@ plan.pack(src, dst)
 plan.unpack(dst, src)
 K.checksum(src)
 K.spin(5.0)
+# packed split-master codec + update, with overflow tiles (wild moments in every other tile)
+n = 2048 * 5
+p32 = torch.randn(n, device="cuda") * 0.02
+mm = torch.randn(n, device="cuda") * 1e-4
+vv = torch.rand(n, device="cuda") * 1e-8
+mm[::4096] = 1e30
+vv[2048::4096] = -1.0
+param = K.cast_f32_to_bf16(p32)
+pk, ok = K.state_compress(torch.cat([p32, mm, vv]), param)
+K.adamw_split_master(pk, (torch.randn(n, device="cuda") * 1e-3).to(torch.bfloat16), param, 1e-3, 0.9, 0.999, 1e-8, 0.01, 1)
+K.state_expand(pk, param)
 torch.cuda.synchronize()
 
 d = tempfile.mkdtemp()
@@ -45,6 +56,16 @@ for pol in ("tencache", "tencache+opt"):
     e.iteration(lr=1e-3, last=True)
     e.step_result()
     e.sync()
+    if pol == "tencache":  # a packed state with overflow tiles: the kernel's mapped-memory path
+        import numpy as np
+        sid = n + 1
+        st = e.read_tensor(sid, 6 * S).view(np.float32).copy()
+        k = S // 2
+        st[k:2 * k:997] = 1e30
+        e.write_tensor(sid, st)
+        e.iteration(lr=1e-3, last=True)
+        e.sync()
+        e.read_tensor(sid, 6 * S)
     e.close()
 from paper_2511_14124_b200 import zero3 as Z  # noqa: E402
 lay = Z.shard_layout("gpt2-small", 1, chunks_per_layer=2)
