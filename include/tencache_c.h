@@ -444,6 +444,15 @@ int tc_engine_p2p_handles(tc_engine* e, uint8_t* out, size_t cap, size_t* n);
 int tc_engine_enable_p2p(tc_engine* e, const uint8_t* all_blobs);
 /* Bytes all-gathered + reduce-scattered (NCCL payload, all ranks' pieces) so far. */
 uint64_t tc_engine_exchanged_bytes(tc_engine* e);
+/* GPUDirect Storage for the NVMe tier: 1 when the
+ * nvidia-fs driver is present and cuFile opened (never probed otherwise: in
+ * its compatibility mode cuFile is a bounce-buffer copy, and on boxes without
+ * the driver cuFileDriverOpen may not return); `why` (may be NULL) gets the
+ * reason when 0. TC_GDS=0 disables it. An engine created with direct_io = 1
+ * moves NVMe tier bytes file <-> HBM with it when available
+ * (tc_engine_gds), else through the pinned bounce buffers. */
+int tc_gds_available(char* why, size_t cap);
+int tc_engine_gds(tc_engine* e);
 
 #ifdef __cplusplus
 }

@@ -185,6 +185,8 @@ _SIGS = {
     "tc_engine_enable_zero3": ([C.c_void_p, C.c_int, C.c_int, C.c_void_p, C.POINTER(C.c_uint64), C.POINTER(C.c_uint64),
                                 C.c_uint32], C.c_int),
     "tc_engine_exchanged_bytes": ([C.c_void_p], C.c_uint64),
+    "tc_gds_available": ([C.c_char_p, C.c_size_t], C.c_int),
+    "tc_engine_gds": ([C.c_void_p], C.c_int),
     "tc_engine_event_log": ([C.c_void_p, C.c_char_p], C.c_int),
     "tc_engine_p2p_handles": ([C.c_void_p, C.c_void_p, C.c_size_t, C.POINTER(C.c_size_t)], C.c_int),
     "tc_engine_enable_p2p": ([C.c_void_p, C.c_void_p], C.c_int),
@@ -223,3 +225,10 @@ def check(rc: int):
 
 def b(s) -> bytes:
     return (s or "").encode() if not isinstance(s, bytes) else s
+
+
+def gds_available():
+    """(available, reason): GPUDirect Storage for the NVMe tier (tc_gds_available)."""
+    buf = C.create_string_buffer(256)
+    ok = lib().tc_gds_available(buf, 256)
+    return bool(ok), buf.value.decode()

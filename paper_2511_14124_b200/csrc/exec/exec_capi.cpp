@@ -1,5 +1,9 @@
 // C-ABI of the migration executor (include/tencache_c.h, tc_engine_*).
 #include "executor.hpp"
+#include "gds.hpp"
+
+#include <algorithm>
+#include <string>
 
 #include <cstring>
 
@@ -196,6 +200,19 @@ int tc_engine_enable_zero3(tc_engine* e, int world, int rank, const uint8_t id[1
 }
 
 uint64_t tc_engine_exchanged_bytes(tc_engine* e) { return e ? e->ex->exchanged_bytes() : 0; }
+
+int tc_gds_available(char* why, size_t cap) {
+  std::string w;
+  const bool ok = tcb::Gds::available(&w);
+  if (why && cap) {
+    const size_t n = std::min(cap - 1, w.size());
+    std::memcpy(why, w.data(), n);
+    why[n] = 0;
+  }
+  return ok ? 1 : 0;
+}
+
+int tc_engine_gds(tc_engine* e) { return e && e->ex->gds() ? 1 : 0; }
 
 int tc_engine_p2p_handles(tc_engine* e, uint8_t* out, size_t cap, size_t* n) {
   TC_GUARD({

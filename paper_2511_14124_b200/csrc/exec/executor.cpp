@@ -1,5 +1,6 @@
 // Per-GPU migration executor (see executor.hpp for the physical layout).
 #include "executor.hpp"
+#include "gds.hpp"
 
 #include <nvtx3/nvToolsExt.h>
 
@@ -312,6 +313,9 @@ Executor::Executor(const std::string& trace_path, const std::string& machine_pat
     }
   }
 
+  // GPUDirect Storage for the NVMe tier when O_DIRECT was asked for and the
+  // nvidia-fs driver is present (never probed otherwise: gds.hpp)
+  gds_ = io_ != nullptr && nvme_->direct() && Gds::available();
   lap("NVMe tier files + I/O pool");
   for (const auto& [size, _] : pclass) {
     void* p = nullptr;
@@ -627,13 +631,14 @@ std::vector<cudaEvent_t> Executor::io_deps(std::vector<cudaEvent_t> deps) {
 
 // NVMe -> host buffer once every GPU op touching `target` is done; returns the
 // job (GPU consumers wait on it through target.io_write).
-std::uint64_t Executor::nvme_read_async(TensorRec& r, void* dst, SlotSync& target) {
+std::uint64_t Executor::nvme_read_async(TensorRec& r, void* dst, SlotSync& target, bool device) {
   std::vector<cudaEvent_t> waits(target.readers.begin(), target.readers.end());
   if (target.writer) waits.push_back(target.writer);
   // after: the buffer's previous job and the extent's previous job (a pending
   // write of the same tensor must land before it is read back)
-  const std::uint64_t k = io_->submit_read(dst, r.bytes, r.nvme_off, io_deps(std::move(waits)),
-                                           {target.io_read, target.io_write, r.nvme_job});
+  std::vector<std::uint64_t> after{target.io_read, target.io_write, r.nvme_job};
+  const std::uint64_t k = device ? io_->submit_read_device(dst, r.bytes, r.nvme_off, io_deps(std::move(waits)), after)
+                                 : io_->submit_read(dst, r.bytes, r.nvme_off, io_deps(std::move(waits)), after);
   r.nvme_job = k;
   target = SlotSync{};
   target.io_write = k;
@@ -643,14 +648,14 @@ std::uint64_t Executor::nvme_read_async(TensorRec& r, void* dst, SlotSync& targe
 
 // host buffer -> NVMe once the copy that filled `source` is done; later writers
 // of the buffer wait on source.io_read.
-std::uint64_t Executor::nvme_write_async(TensorRec& r, const void* src, SlotSync& source) {
+std::uint64_t Executor::nvme_write_async(TensorRec& r, const void* src, SlotSync& source, bool device) {
   std::vector<cudaEvent_t> waits;
   if (source.writer) waits.push_back(source.writer);
-  const std::uint64_t k =
-      io_->submit_write(src, r.bytes, r.nvme_off, io_deps(std::move(waits)),
-                        // the buffer's previous reader too: source.io_read must keep naming a job
-                        // whose completion implies every earlier read of the buffer finished
-                        {source.io_write, source.io_read, r.nvme_job});
+  // the buffer's previous reader too: source.io_read must keep naming a job
+  // whose completion implies every earlier read of the buffer finished
+  std::vector<std::uint64_t> after{source.io_write, source.io_read, r.nvme_job};
+  const std::uint64_t k = device ? io_->submit_write_device(src, r.bytes, r.nvme_off, io_deps(std::move(waits)), after)
+                                 : io_->submit_write(src, r.bytes, r.nvme_off, io_deps(std::move(waits)), after);
   r.nvme_job = k;
   source.io_read = k;
   r.nvme_valid = true;
@@ -692,7 +697,10 @@ void Executor::nvme_write(TensorRec& r, const void* src) {
 void Executor::ensure_nvme_fresh(TensorRec& r) {
   if (r.nvme_valid) return;
   tag_ = CopyTag{"writeback", r.id, 0, 2};
-  if (r.tier == PTier::Gpu) {
+  if (r.tier == PTier::Gpu && gds_) {  // HBM -> file directly (GPUDirect Storage)
+    Slot& g = slot_of(r);
+    nvme_write_async(r, g.ptr, g.sync, true);
+  } else if (r.tier == PTier::Gpu) {
     Slot& g = slot_of(r);
     std::uint8_t* b = bounce_.at(r.bytes);
     SlotSync& bs = bounce_sync_[r.bytes];
@@ -809,6 +817,19 @@ void Executor::apply(const Req& r) {
     } else {
       free_slot(x.tier, x.bytes, x.slot);
     }
+    x.tier = PTier::Gpu;
+    x.slot = gs;
+    x.arrival = done;
+    stats_.h2d_bytes += x.bytes;
+  } else if (r.src == Tier::Nvme && r.dst == Tier::Gpu && gds_) {  // GPUDirect Storage: file -> HBM, one leg
+    const std::uint32_t gs = take_slot(PTier::Gpu, x.bytes, xi);
+    Slot& g = gpu_.cls(x.bytes).slots[gs];
+    const std::uint64_t k = nvme_read_async(x, g.ptr, g.sync, true);
+    io_->stream_wait(h2d_, k);
+    done = events_.get(true);
+    TCB_CK(cudaEventRecord(done, h2d_));
+    g.sync = SlotSync{done, {}};
+    if (!r.src_retains) x.nvme_valid = false;
     x.tier = PTier::Gpu;
     x.slot = gs;
     x.arrival = done;

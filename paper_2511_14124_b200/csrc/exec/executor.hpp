@@ -412,8 +412,12 @@ class Executor {
   std::unique_ptr<NvmeQueue> io_;  // async NVMe tier I/O (null: synchronous fallback)
   cudaStream_t io_join_ = nullptr;  // joins a job's dependencies into one event of the submitting generation
   std::vector<cudaEvent_t> io_deps(std::vector<cudaEvent_t> deps);
-  std::uint64_t nvme_read_async(TensorRec& r, void* dst, SlotSync& target);
-  std::uint64_t nvme_write_async(TensorRec& r, const void* src, SlotSync& source);
+  std::uint64_t nvme_read_async(TensorRec& r, void* dst, SlotSync& target, bool device = false);
+  std::uint64_t nvme_write_async(TensorRec& r, const void* src, SlotSync& source, bool device = false);
+  bool gds_ = false;  // NVMe <-> HBM through GPUDirect Storage (direct_io, nvidia-fs present: gds.hpp)
+ public:
+  bool gds() const { return gds_; }
+ private:
 
   // h2d_/d2h_: cache decisions (prefetch, evict, restore); h2d_opt_/d2h_opt_:
   // optimizer-state staging and write-back, so evictions never queue behind

@@ -10,6 +10,7 @@
 #include <cstdlib>
 
 #include "capi_common.hpp"
+#include "gds.hpp"
 
 namespace tcb {
 
@@ -32,7 +33,7 @@ void stream_wait_value32(cudaStream_t s, const unsigned* dev_addr, unsigned valu
     throw DeviceError(TC_ECUDA, "cuStreamWaitValue32 failed");
 }
 
-StripedFile::StripedFile(const std::string& dir, std::uint64_t bytes, int files, bool direct) {
+StripedFile::StripedFile(const std::string& dir, std::uint64_t bytes, int files, bool direct) : direct_(direct) {
   files = std::max(1, files);
   const std::uint64_t stripes = (bytes + kStripe - 1) / kStripe;
   const std::uint64_t per_file = ((stripes + files - 1) / files) * kStripe;
@@ -67,6 +68,22 @@ bool StripedFile::io(bool write, std::uint8_t* buf, std::uint64_t bytes, std::ui
       done += static_cast<std::uint64_t>(r);
     }
     buf += len;
+    off += len;
+    bytes -= len;
+  }
+  return true;
+}
+
+bool StripedFile::io_device(bool write, std::uint8_t* dev, std::uint64_t bytes, std::uint64_t off) const {
+  Gds& g = Gds::get();
+  const std::uint64_t k = fds_.size();
+  while (bytes) {
+    const std::uint64_t stripe = off / kStripe, in = off % kStripe;
+    const std::uint64_t len = std::min(bytes, kStripe - in);
+    void* fh = g.handle(fds_[stripe % k]);
+    const std::uint64_t foff = (stripe / k) * kStripe + in;
+    if (!(write ? g.write(fh, dev, len, foff) : g.read(fh, dev, len, foff))) return false;
+    dev += len;
     off += len;
     bytes -= len;
   }
@@ -154,12 +171,22 @@ std::uint64_t NvmeQueue::submit(Job j) {
 
 std::uint64_t NvmeQueue::submit_read(void* dst, std::uint64_t bytes, std::uint64_t off, std::vector<cudaEvent_t> w,
                                      std::vector<std::uint64_t> after) {
-  return submit(Job{false, dst, bytes, off, 0, std::move(w), std::move(after)});
+  return submit(Job{false, false, dst, bytes, off, 0, std::move(w), std::move(after)});
+}
+
+std::uint64_t NvmeQueue::submit_read_device(void* dst, std::uint64_t bytes, std::uint64_t off,
+                                            std::vector<cudaEvent_t> w, std::vector<std::uint64_t> after) {
+  return submit(Job{false, true, dst, bytes, off, 0, std::move(w), std::move(after)});
+}
+
+std::uint64_t NvmeQueue::submit_write_device(const void* src, std::uint64_t bytes, std::uint64_t off,
+                                             std::vector<cudaEvent_t> w, std::vector<std::uint64_t> after) {
+  return submit(Job{true, true, const_cast<void*>(src), bytes, off, 0, std::move(w), std::move(after)});
 }
 
 std::uint64_t NvmeQueue::submit_write(const void* src, std::uint64_t bytes, std::uint64_t off,
                                       std::vector<cudaEvent_t> w, std::vector<std::uint64_t> after) {
-  return submit(Job{true, const_cast<void*>(src), bytes, off, 0, std::move(w), std::move(after)});
+  return submit(Job{true, false, const_cast<void*>(src), bytes, off, 0, std::move(w), std::move(after)});
 }
 
 std::uint64_t NvmeQueue::done() const {
@@ -288,8 +315,8 @@ void NvmeQueue::dispatch() {
     remaining_[j.seq] = static_cast<std::uint32_t>(n);
     for (std::uint64_t k = 0; k < n; ++k) {
       const std::uint64_t o = k * kPiece;
-      pieces_.push_back(Piece{j.write, static_cast<std::uint8_t*>(j.buf) + o, std::min(kPiece, j.bytes - o),
-                              j.off + o, j.seq});
+      pieces_.push_back(Piece{j.write, j.device, static_cast<std::uint8_t*>(j.buf) + o,
+                              std::min(kPiece, j.bytes - o), j.off + o, j.seq});
     }
     piece_cv_.notify_all();
   }
@@ -308,7 +335,15 @@ void NvmeQueue::work() {
     // fault injection for tests: TC_NVME_FAIL_JOB=k fails job k's I/O
     const char* fe = std::getenv("TC_NVME_FAIL_JOB");
     const std::uint64_t fail_job = fe ? std::strtoull(fe, nullptr, 10) : 0ull;
-    piece_done(p.seq, p.seq != fail_job && file_->io(p.write, p.buf, p.bytes, p.off));
+    bool ok = p.seq != fail_job;
+    if (ok) {
+      try {
+        ok = p.device ? file_->io_device(p.write, p.buf, p.bytes, p.off) : file_->io(p.write, p.buf, p.bytes, p.off);
+      } catch (const std::exception&) {
+        ok = false;  // surfaces as the queue's I/O error
+      }
+    }
+    piece_done(p.seq, ok);
   }
 }
 

@@ -40,10 +40,15 @@ class StripedFile {
   StripedFile& operator=(const StripedFile&) = delete;
   // Full transfer at logical offset `off`; false on an I/O error.
   bool io(bool write, std::uint8_t* buf, std::uint64_t bytes, std::uint64_t off) const;
+  // The same between the file and HBM through GPUDirect Storage (gds.hpp);
+  // the files must be O_DIRECT.
+  bool io_device(bool write, std::uint8_t* dev, std::uint64_t bytes, std::uint64_t off) const;
+  bool direct() const { return direct_; }
   int files() const { return static_cast<int>(fds_.size()); }
 
  private:
   std::vector<int> fds_;
+  bool direct_ = false;
 };
 
 class NvmeQueue {
@@ -59,6 +64,11 @@ class NvmeQueue {
                             std::vector<std::uint64_t> after = {});
   std::uint64_t submit_write(const void* src, std::uint64_t bytes, std::uint64_t file_off,
                              std::vector<cudaEvent_t> waits, std::vector<std::uint64_t> after = {});
+  // dst/src in HBM: the worker moves the bytes with GPUDirect Storage
+  std::uint64_t submit_read_device(void* dst, std::uint64_t bytes, std::uint64_t file_off,
+                                   std::vector<cudaEvent_t> waits, std::vector<std::uint64_t> after = {});
+  std::uint64_t submit_write_device(const void* src, std::uint64_t bytes, std::uint64_t file_off,
+                                    std::vector<cudaEvent_t> waits, std::vector<std::uint64_t> after = {});
   void stream_wait(cudaStream_t s, std::uint64_t seq);       // GPU-side wait for job `seq` alone
   void stream_wait_upto(cudaStream_t s, std::uint64_t seq);  // GPU-side wait for every job <= seq
   void wait(std::uint64_t seq);                              // host-side wait for job `seq`
@@ -78,6 +88,7 @@ class NvmeQueue {
   static constexpr std::uint32_t kRing = 1u << 16;  // per-job completion words (seq % kRing)
   struct Job {
     bool write;
+    bool device = false;  // buf is HBM (GPUDirect Storage)
     void* buf;
     std::uint64_t bytes, off, seq;
     std::vector<cudaEvent_t> waits;
@@ -86,6 +97,7 @@ class NvmeQueue {
   };
   struct Piece {
     bool write;
+    bool device;
     std::uint8_t* buf;
     std::uint64_t bytes, off, seq;
   };

@@ -144,6 +144,11 @@ class Engine:
         N.check(N.lib().tc_engine_step_result(self._h, out, n.value, C.byref(n)))
         return np.array(out[: n.value], dtype=np.uint64)
 
+    @property
+    def gds(self):
+        """True when the NVMe tier moves file <-> HBM through GPUDirect Storage."""
+        return bool(N.lib().tc_engine_gds(self._h))
+
     def close(self):
         if self._h:
             N.lib().tc_engine_destroy(self._h)

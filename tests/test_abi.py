@@ -88,3 +88,16 @@ def test_packed_state_layout_fits_its_slot():
         b = N.lib().tc_split_state_bytes(n)
         assert b == (9 * n + n // 8 + n // 4 + n // 16 + n // 512 + 15) // 16 * 16
         assert b % 16 == 0 and b + 2 * n <= 12 * n
+
+
+def test_gds_availability_probe():
+    """GPUDirect Storage is probed only where the nvidia-fs driver is loaded
+    (cuFile's compatibility mode is the bounce-buffer path the engine already
+    has, and its driver open may not return without nvidia-fs)."""
+    import os
+    from paper_2511_14124_b200 import _native as N
+    ok, why = N.gds_available()
+    if not os.path.exists("/proc/driver/nvidia-fs"):
+        assert not ok and "nvidia-fs" in why
+    else:
+        assert ok or why

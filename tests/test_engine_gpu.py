@@ -39,9 +39,12 @@ def load(tr):
     return tensors, steps
 
 
-def check_engine(tr, m, cfg, iters=2, nvme_dir="", hoist=True, prestage=True, stages=12, full_master=False):
+def check_engine(tr, m, cfg, iters=2, nvme_dir="", hoist=True, prestage=True, stages=12, full_master=False,
+                 direct_io=False, want_gds=None):
     tensors, steps = load(tr)
-    e = Engine(tr, m, cfg, nvme_dir=nvme_dir, opt_stage_slots=stages, full_master=full_master)
+    e = Engine(tr, m, cfg, nvme_dir=nvme_dir, opt_stage_slots=stages, full_master=full_master, direct_io=direct_io)
+    if want_gds is not None:
+        assert e.gds == want_gds
     e.seed(7)
     params = {i: e.read_tensor(i, t["size"]).view(np.uint16).copy() for i, t in tensors.items() if t["kind"] == "p16"}
     states = {i: e.read_tensor(i, t["size"]).view(np.float32).copy() for i, t in tensors.items() if t["kind"] == "o32"}
@@ -137,15 +140,27 @@ def test_split_master_states(tmpd, full_master, gpu_chunks, hoist):
 
 
 @pytest.mark.parametrize("pol", ["tencache", "tencache+opt"])
-@pytest.mark.parametrize("io", ["async", "sync"])
+@pytest.mark.parametrize("io", ["async", "sync", "direct", "gds"])
 def test_nvme_tiers(tmpd, pol, io, monkeypatch):
+    """io: the async queue, synchronous I/O, O_DIRECT files (GPUDirect
+    Storage off), GPUDirect Storage (file <-> HBM; only where nvidia-fs is
+    loaded)."""
+    from paper_2511_14124_b200 import _native as N
+    gds_ok, why = N.gds_available()
     if io == "sync":
         monkeypatch.setenv("TC_SYNC_NVME", "1")
+    if io == "direct":
+        monkeypatch.setenv("TC_GDS", "0")  # read in a fresh process only; the probe is per process
+        if gds_ok:
+            pytest.skip("GPUDirect Storage already active in this process")
+    if io == "gds" and not gds_ok:
+        pytest.skip("GPUDirect Storage unavailable: " + why)
     # fig9 shape: tensor 7 placed in NVMe, CPU victim spilled, staged fetches;
     # optimizer states partly (or, base posture, all) in NVMe.
     tr, m = write_with_states(tmpd, "f9", [4096] * 7, 3 * 4096, 3 * 4096 + 2 * 6 * 4096, iters=3)
     cfg = {"policy": pol}
-    st = check_engine(tr, m, cfg, iters=3, nvme_dir=tmpd)
+    st = check_engine(tr, m, cfg, iters=3, nvme_dir=tmpd, direct_io=io in ("direct", "gds"),
+                      want_gds=io == "gds" if io in ("direct", "gds") else None)
     rep = ref.run(tr, m, cfg)
     assert st["param_hits"] == rep["param_hits"]
     assert st["nvme_read_bytes"] > 0 and st["nvme_write_bytes"] > 0
