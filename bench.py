@@ -25,8 +25,8 @@ value = W / step time, W = the config's migrated bytes per step (whole job):
 
 --impl reference runs the reference's own CPU path on the box's host cores,
 with the oracle only (oracle/_ref = the unmodified reference compiled here,
-oracle/numerics.c): reference IPolicy decisions, host memcpy migrations, the
-gradient copy to host, OpenMP CPU-Adam and the bf16 parameter copy (the
+oracle/numerics.c): reference IPolicy decisions, host memcpy migrations (the
+NVMe tier as files, like the engine's), the gradient copy to host, OpenMP CPU-Adam and the bf16 parameter copy (the
 paper's CPU-Adam architecture), with the trace's compute time
 either overlapped with that host work (max(compute, host): the reported
 value, the most favourable CPU number) or serial (reported beside it).
@@ -478,33 +478,72 @@ def dram_traffic(elems_per_launch, bytes_per_elem=ADAM_BYTES_PER_ELEM):
 class HostTiers:
     """Tier buffers of the CPU path for the sampled tensors: per (tier, size)
     FIFO free lists, allocated on first use (the warm-up iteration); a move
-    is a host memcpy on every host thread (the reference's transfer)."""
+    between host tiers is a host memcpy on every host thread (the
+    reference's transfer). The NVMe tier (2) is files in `nvme_dir`, as the
+    engine's: a move into or out of it is pwrite/pread in 16 MiB pieces on a
+    pool of host threads (the engine's NVMe tier, like DeepSpeed's aio, keeps
+    16 in flight), through the page cache like the engine's default tier."""
 
-    def __init__(self, np, ref, sizes, initial):
+    NVME, PIECE = 2, 16 << 20
+
+    def __init__(self, np, ref, sizes, initial, nvme_dir=None, threads=16):
+        import concurrent.futures as cf
         self.np, self.ref = np, ref
         self.slots, self.free, self.loc, self.size = {}, {}, {}, sizes
+        self.nvme_dir, self.fds = nvme_dir or tempfile.gettempdir(), {}
+        self.pool = cf.ThreadPoolExecutor(max_workers=threads)
         for tid, tier in initial.items():
             self.loc[tid] = (tier, self.take(tier, sizes[tid]))
 
     def take(self, tier, size):
         fl = self.free.setdefault((tier, size), [])
         if not fl:
-            self.slots.setdefault((tier, size), []).append(self.np.empty(size, self.np.uint8))
-            return len(self.slots[(tier, size)]) - 1
+            lst = self.slots.setdefault((tier, size), [])
+            lst.append(None if tier == self.NVME else self.np.empty(size, self.np.uint8))
+            return len(lst) - 1
         return fl.pop(0)
 
     def buf(self, tid):
         tier, s = self.loc[tid]
         return self.slots[(tier, self.size[tid])][s]
 
+    def _fd(self, size):
+        if size not in self.fds:
+            fd, path = tempfile.mkstemp(dir=self.nvme_dir, prefix="tencache_ref_nvme_")
+            os.unlink(path)
+            self.fds[size] = fd
+        return self.fds[size]
+
+    def _file_io(self, write, buf, size, slot):
+        fd, base = self._fd(size), slot * size
+        mv = memoryview(buf).cast("B")
+
+        def piece(o):
+            n = min(self.PIECE, size - o)
+            if write:
+                os.pwrite(fd, mv[o:o + n], base + o)
+            else:
+                os.preadv(fd, [mv[o:o + n]], base + o)
+        list(self.pool.map(piece, range(0, size, self.PIECE)))
+
     def move(self, tid, dst, copy=True):
         tier, s = self.loc[tid]
         size = self.size[tid]
         ns = self.take(dst, size)
         if copy:
-            self.ref.memcpy(self.slots[(dst, size)][ns], self.slots[(tier, size)][s], size)
+            if dst == self.NVME and tier != self.NVME:
+                self._file_io(True, self.slots[(tier, size)][s], size, ns)
+            elif tier == self.NVME and dst != self.NVME:
+                self._file_io(False, self.slots[(dst, size)][ns], size, s)
+            elif tier != self.NVME:
+                self.ref.memcpy(self.slots[(dst, size)][ns], self.slots[(tier, size)][s], size)
         self.free.setdefault((tier, size), []).append(s)
         self.loc[tid] = (dst, ns)
+
+    def close(self):
+        self.pool.shutdown()
+        for fd in self.fds.values():
+            os.close(fd)
 
 
 def _sleep_until(t_end):
@@ -521,7 +560,8 @@ def cpu_reference(args, name, steps, warmup):
 
     Per trace step in the reference's call order (engine.cpp:119-178): the
     reference IPolicy decides (oracle/_ref Replay); every non-instant request
-    of a sampled tensor is a host memcpy between tier buffers; each optimizer
+    of a sampled tensor is a host memcpy between tier buffers (to or from the
+    NVMe tier: pwrite/pread of files on a thread pool); each optimizer
     step of a sampled state copies the chunk's bf16 gradient to host memory,
     runs OpenMP AdamW (oracle/numerics.c) and writes the bf16 parameter back
     into the parameter's buffer (CPU-Adam); the trace's compute
@@ -552,17 +592,19 @@ def cpu_reference(args, name, steps, warmup):
     place = dec["init"]["placement"]
     tiers_of = {int(k): v for k, v in place["params"].items()}
     tiers_of.update({int(k): v for k, v in place["opt"].items()})
-    tiers = HostTiers(np, ref, sizes, {t: tiers_of[t] for t in sampled})
+    tiers = HostTiers(np, ref, sizes, {t: tiers_of[t] for t in sampled}, nvme_dir=args.nvme_dir,
+                      threads=max(1, min(16, ref.threads())))
     rng = np.random.default_rng(0)
     S = info["chunk_bytes"]
     blk = (rng.standard_normal(S // 2) * 0.02).astype(np.float32)
     grads = {}
     for pid in sorted(sampled_p):
-        tiers.buf(pid)[:] = 0
+        if tiers.buf(pid) is not None:  # (an NVMe-resident chunk starts as the file's zeros)
+            tiers.buf(pid)[:] = 0
         g = ((rng.standard_normal(S // 2) * 1e-3).astype(np.float32).view(np.uint32) >> 16).astype(np.uint16)
         grads[pid] = g  # the parameter's bf16 gradient where the device left it
     for sid, pid in partner.items():
-        if sid in sampled:
+        if sid in sampled and tiers.buf(sid) is not None:
             st = tiers.buf(sid).view(np.float32)
             st[: S // 2] = blk
             st[S // 2:] = 0
@@ -636,12 +678,14 @@ def cpu_reference(args, name, steps, warmup):
         wall = (time.perf_counter() - t0) / k
         out[mode] = (d + max(0.0, wall - d) / frac_eff) * 1e3
     rp.close()
+    tiers.close()
     ms = out["overlapped"]
     sample = (f"{'all' if frac_eff == 1 else f'{len(sampled_p)} of {len(params)}'} parameter chunks (every "
               f"{every}th) and their state chunks: data work and compute time of those, timed and scaled by "
               f"{len(params)}/{len(sampled_p)}; decisions for the whole trace ({d * 1e3:.1f} ms/step, unscaled); "
-              f"reference IPolicy decisions (oracle/_ref), host memcpy migrations, gradient copy, OpenMP AdamW + "
-              f"bf16 parameter write (oracle/numerics.c), trace compute overlapped (value) / serial")
+              f"reference IPolicy decisions (oracle/_ref), host memcpy migrations (NVMe tier: pwrite/pread of "
+              f"files, 16 threads), gradient copy, OpenMP AdamW + bf16 parameter write (oracle/numerics.c), "
+              f"trace compute overlapped (value) / serial")
     return {"value": round(W["total"] / (ms * 1e-3) / 1e9, 4), "ms_per_step": round(ms, 3),
             "serial_ms_per_step": round(out["serial"], 3), "cores": threads, "sample": sample, "W": W, "rep": rep,
             "info": info, "frac": frac_eff, "decisions_ms": round(d * 1e3, 3)}
@@ -671,8 +715,8 @@ def run_reference_arm(args, name):
                        "tokens_per_step": args.tokens, "compute": "trace compute time (sleep), overlapped with the "
                        "host work (value) and serial (serial_ms_per_step)", "compute_model_tflops": args.tflops,
                        "parallelism": "host cores (%d threads)" % r["cores"],
-                       "path": "reference IPolicy decisions (oracle/_ref), host memcpy migrations, CPU-Adam "
-                               "(oracle/numerics.c)"},
+                       "path": "reference IPolicy decisions (oracle/_ref), host memcpy migrations (NVMe tier: "
+                               "file pwrite/pread), CPU-Adam (oracle/numerics.c)"},
             "hit_rate": {"exact": r["rep"]["hit_rate"], "hits": r["rep"]["param_hits"],
                          "accesses": r["rep"]["param_accesses"]},
             "migrated_bytes_per_step": {"W_job": r["W"]["total"], **r["W"]},
