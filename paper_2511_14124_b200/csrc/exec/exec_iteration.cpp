@@ -376,10 +376,15 @@ std::vector<std::size_t> Executor::plan_hoisting(const std::vector<Hook>& hooks)
     const std::size_t a = la->second;
     const Tier home = policy_->initial_tier(sid).value_or(Tier::Nvme);
     if (home != Tier::Cpu && home != Tier::Gpu) continue;
-    bool moved = false;  // any decision moving the state before its update's end
+    // any decision moving the state before its update has run; its own end
+    // hook's moves (the +Opt rotation evicts the updated state to NVMe there,
+    // scheduler.cpp:338-370) come after the hoisted update anyway: requests
+    // touching a deferred update's tensors flush it first (flush_if_touched)
+    // and wait on its write-back through the slot's events
+    bool moved = false;
     auto t = touched.find(sid);
     if (t != touched.end())
-      for (std::size_t k : t->second) moved = moved || k <= end_pos[j];
+      for (std::size_t k : t->second) moved = moved || k < end_pos[j];
     if (moved) continue;
     at[j] = a;
   }
@@ -475,6 +480,8 @@ void Executor::iteration_begin(const StepOptions& so, cudaStream_t compute, bool
   // (no decision touches them before their update, plan_hoisting). States
   // staged by the prologue are skipped by refill_stages.
   set_prestage_order(it.hooks, it.hoist);
+  set_early_order(it.hooks);
+  refill_early();
   // states the prologue staged come first in the order: continue after them
   while (prestage_next_ < prestage_order_.size() && staged_.count(prestage_order_[prestage_next_])) ++prestage_next_;
   if (so_.prestage) {
@@ -611,6 +618,47 @@ void Executor::set_prestage_order(const std::vector<Hook>& hooks, const std::vec
 void Executor::drop_staged() {
   for (auto& [idx, b] : staged_) stage_free_.push_back(b);
   staged_.clear();
+  drop_early();
+}
+
+// The iteration's NVMe -> pinned state fetches, in decision order.
+void Executor::set_early_order(const std::vector<Hook>& hooks) {
+  drop_early();  // (empty here: every read-ahead of an iteration is bound by its own decision)
+  if (nvme_ahead_ == 0 || !io_) return;
+  for (const Hook& h : hooks)
+    for (const Req& r : h.reqs)
+      if (r.src == Tier::Nvme && r.dst == Tier::Cpu && !r.instant && rec(r.tensor_id).is_state)
+        early_order_.push_back(index_of(r.tensor_id));
+}
+
+// Keep up to nvme_ahead_ of the upcoming fetches read into spare pinned
+// slots. An entry whose state is not in the NVMe tier now (an earlier fetch
+// of the same state in this iteration comes first) is left to its decision.
+void Executor::refill_early() {
+  while (early_.size() < nvme_ahead_ && early_next_ < early_order_.size()) {
+    const std::int32_t xi = early_order_[early_next_];
+    TensorRec& x = recs_[static_cast<std::size_t>(xi)];
+    if (x.tier != PTier::Nvme || !x.nvme_valid || early_.count(xi)) {
+      ++early_next_;
+      continue;
+    }
+    if (!host_opt_.has_free(x.bytes)) return;  // every spare slot holds a read-ahead: wait for a bind
+    ++early_next_;
+    const std::uint32_t hs = take_slot(PTier::HostOpt, x.bytes, xi);
+    Slot& h = host_opt_.cls(x.bytes).slots[hs];
+    tag_ = CopyTag{"nvme_ahead", x.id, 2, 1};
+    nvme_read_async(x, h.ptr, h.sync);
+    early_[xi] = EarlyFetch{hs};
+  }
+}
+
+// Give read-ahead slots back (their pending reads stay ordered before any
+// later writer of the slot through its SlotSync).
+void Executor::drop_early() {
+  for (auto& [xi, ef] : early_) free_slot(PTier::HostOpt, recs_[static_cast<std::size_t>(xi)].bytes, ef.slot);
+  early_.clear();
+  early_order_.clear();
+  early_next_ = 0;
 }
 
 // Prologue of iteration t+1, run at the end of iteration t's enqueue: its

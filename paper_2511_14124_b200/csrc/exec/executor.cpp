@@ -233,6 +233,12 @@ Executor::Executor(const std::string& trace_path, const std::string& machine_pat
   double fwd_h2d = 0;
   std::set<TensorId> in_nvme, to_gpu;
   std::map<std::pair<int, std::uint64_t>, std::uint32_t> need = simulate_occupancy(&fwd_h2d, &in_nvme, &to_gpu);
+  {  // NVMe lookahead window: only when optimizer states live in the NVMe tier
+    bool states_in_nvme = false;
+    for (const auto& r : recs_) states_in_nvme = states_in_nvme || (r.is_state && in_nvme.count(r.id));
+    const char* na = std::getenv("TC_NVME_AHEAD");
+    nvme_ahead_ = states_in_nvme ? (na ? static_cast<std::size_t>(std::max(0, std::atoi(na))) : 16) : 0;
+  }
   lap("occupancy dry run");
   {  // split-master eligibility (TensorRec::split_ok)
     const char* fm = std::getenv("TC_FULL_MASTER");
@@ -259,7 +265,7 @@ Executor::Executor(const std::string& trace_path, const std::string& machine_pat
   }
   for (const auto& [size, _] : sclass) {
     if (need[{0, size}]) gpu_.plan(size, need[{0, size}] + 1);  // GPU-resident states (no offload)
-    host_opt_.plan(size, need[{2, size}] + hspare + 1);          // +1 transient
+    host_opt_.plan(size, need[{2, size}] + hspare + 1 + nvme_ahead_);  // +1 transient, + NVMe lookahead
   }
   gpu_.allocate(true, device_);
   lap("HBM pool");
@@ -731,7 +737,9 @@ void Executor::ensure_nvme_fresh(TensorRec& r) {
 
 bool Executor::dest_available(const Req& r) const {
   if (r.instant || r.dst == Tier::Nvme) return true;
-  const TensorRec& x = recs_[static_cast<std::size_t>(index_of(r.tensor_id))];
+  const std::int32_t xi = index_of(r.tensor_id);
+  if (r.src == Tier::Nvme && early_.count(xi)) return true;  // its slot is already taken (read ahead)
+  const TensorRec& x = recs_[static_cast<std::size_t>(xi)];
   if (r.dst == Tier::Gpu) return gpu_.has_free(x.bytes);
   return (x.is_state ? host_opt_ : host_param_).has_free(x.bytes);
 }
@@ -857,6 +865,12 @@ void Executor::apply(const Req& r) {
     x.slot = gs;
     x.arrival = done;
     stats_.h2d_bytes += x.bytes;
+  } else if (r.src == Tier::Nvme && r.dst == Tier::Cpu && early_.count(xi)) {  // read ahead: bind its slot
+    x.slot = early_.at(xi).slot;
+    early_.erase(xi);
+    if (!r.src_retains) x.nvme_valid = false;
+    x.tier = host_tier(x);
+    refill_early();
   } else if (r.src == Tier::Nvme && r.dst == Tier::Cpu) {  // state (or param) read into host memory
     const PTier ht = host_tier(x);
     const std::uint32_t hs = take_slot(ht, x.bytes, xi);

@@ -335,6 +335,21 @@ class Executor {
   std::size_t adam_batch() const { return adam_batch_env_ ? adam_batch_env_ : adam_stream() == opt_ ? kAdamBatchConcurrent : 1; }
   std::size_t stage_state(TensorRec& s);
   void refill_stages(std::size_t want_staged);
+  // NVMe lookahead: the iteration's NVMe -> pinned fetches of optimizer states
+  // (the +Opt rotation, scheduler.cpp:320-370) are known when it is decided;
+  // up to nvme_ahead_ of them are read into spare pinned slots early, and the
+  // decision's fetch then binds the slot instead of starting the read. The
+  // state's NVMe bytes cannot change in between (only its fetch moves it), and
+  // the read is ordered after the extent's last write (nvme_read_async).
+  struct EarlyFetch {
+    std::uint32_t slot = 0;  // physical slot in the state's pinned class
+  };
+  std::unordered_map<std::int32_t, EarlyFetch> early_;
+  std::vector<std::int32_t> early_order_;  // state fetches NVMe -> CPU in decision order
+  std::size_t early_next_ = 0, nvme_ahead_ = 0;
+  void set_early_order(const std::vector<Hook>& hooks);
+  void refill_early();
+  void drop_early();
   std::size_t forward_prestage_budget(const std::vector<Hook>& hooks) const;
   void set_prestage_order(const std::vector<Hook>& hooks, const std::vector<std::size_t>& hoist);
   void drop_staged();
