@@ -104,6 +104,16 @@ void* Gds::handle(int fd) {
   return h;
 }
 
+void Gds::release(int fd) {
+  State& s = state();
+  if (!s.ok) return;
+  std::lock_guard<std::mutex> g(s.mu);
+  auto it = s.handles.find(fd);
+  if (it == s.handles.end()) return;
+  if (s.f.HandleDeregister) s.f.HandleDeregister(it->second);
+  s.handles.erase(it);
+}
+
 bool Gds::read(void* fh, void* dev, std::uint64_t bytes, std::uint64_t file_off) {
   for (std::uint64_t done = 0; done < bytes;) {
     const ssize_t r = state().f.Read(static_cast<CUfileHandle_t>(fh), dev, bytes - done,

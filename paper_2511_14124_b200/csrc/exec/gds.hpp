@@ -25,6 +25,9 @@ class Gds {
 
   // A registered handle for an O_DIRECT file descriptor (idempotent per fd).
   void* handle(int fd);
+  // Deregister the handle of `fd` before the descriptor is closed (a later
+  // file may reuse the number). No-op when GDS never ran or fd has none.
+  static void release(int fd);
   // Whole transfer between HBM and a registered file; false on an I/O error.
   bool read(void* fh, void* dev, std::uint64_t bytes, std::uint64_t file_off);
   bool write(void* fh, const void* dev, std::uint64_t bytes, std::uint64_t file_off);

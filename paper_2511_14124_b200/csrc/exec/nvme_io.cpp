@@ -51,7 +51,10 @@ StripedFile::StripedFile(const std::string& dir, std::uint64_t bytes, int files,
 }
 
 StripedFile::~StripedFile() {
-  for (int fd : fds_) close(fd);
+  for (int fd : fds_) {
+    Gds::release(fd);
+    close(fd);
+  }
 }
 
 bool StripedFile::io(bool write, std::uint8_t* buf, std::uint64_t bytes, std::uint64_t off) const {

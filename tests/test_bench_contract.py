@@ -92,3 +92,20 @@ def test_product_arm_torchrun_ranks_sharing_one_gpu(world):
     assert d["exchange"]["bytes_per_step_per_rank"] > 0
     assert d["hit_rate"]["accesses"] > 0 and d["value"] > 0
     assert "functional run" in d["config"]["workload"]
+
+
+def test_reference_arm_nvme_tier_is_files(tmp_path):
+    """The CPU path's NVMe tier (bench.HostTiers, tier 2) round-trips bytes
+    through files, like the engine's tier: CPU -> NVMe -> CPU returns them."""
+    import numpy as np
+    import bench
+    from oracle import ref
+    size = (16 << 20) * 2 + 4096
+    tiers = bench.HostTiers(np, ref, {7: size}, {7: 1}, nvme_dir=str(tmp_path), threads=4)
+    data = np.random.default_rng(0).integers(0, 255, size, dtype=np.uint8)
+    tiers.buf(7)[:] = data
+    tiers.move(7, 2)
+    assert tiers.buf(7) is None and tiers.loc[7][0] == 2
+    tiers.move(7, 1)
+    assert np.array_equal(tiers.buf(7), data)
+    tiers.close()
