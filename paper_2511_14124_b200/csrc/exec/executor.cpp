@@ -643,8 +643,9 @@ std::uint64_t Executor::nvme_read_async(TensorRec& r, void* dst, SlotSync& targe
   // after: the buffer's previous job and the extent's previous job (a pending
   // write of the same tensor must land before it is read back)
   std::vector<std::uint64_t> after{target.io_read, target.io_write, r.nvme_job};
+  const std::uint64_t pn = r.is_state && r.split ? r.bytes / 12 : 0;  // packed: what the last write moved
   const std::uint64_t k = device ? io_->submit_read_device(dst, r.bytes, r.nvme_off, io_deps(std::move(waits)), after)
-                                 : io_->submit_read(dst, r.bytes, r.nvme_off, io_deps(std::move(waits)), after);
+                                 : io_->submit_read(dst, r.bytes, r.nvme_off, io_deps(std::move(waits)), after, pn);
   r.nvme_job = k;
   target = SlotSync{};
   target.io_write = k;
@@ -660,8 +661,9 @@ std::uint64_t Executor::nvme_write_async(TensorRec& r, const void* src, SlotSync
   // the buffer's previous reader too: source.io_read must keep naming a job
   // whose completion implies every earlier read of the buffer finished
   std::vector<std::uint64_t> after{source.io_write, source.io_read, r.nvme_job};
+  const std::uint64_t pn = r.is_state && r.split ? r.bytes / 12 : 0;  // packed: prefix (+ overflow area)
   const std::uint64_t k = device ? io_->submit_write_device(src, r.bytes, r.nvme_off, io_deps(std::move(waits)), after)
-                                 : io_->submit_write(src, r.bytes, r.nvme_off, io_deps(std::move(waits)), after);
+                                 : io_->submit_write(src, r.bytes, r.nvme_off, io_deps(std::move(waits)), after, pn);
   r.nvme_job = k;
   source.io_read = k;
   r.nvme_valid = true;
@@ -691,6 +693,7 @@ void Executor::nvme_read(const TensorRec& r, void* dst) {
 }
 
 void Executor::nvme_write(TensorRec& r, const void* src) {
+  if (io_) io_->forget_extent(r.nvme_off);  // the whole slot lands outside the queue
   if (!nvme_->io(true, const_cast<std::uint8_t*>(static_cast<const std::uint8_t*>(src)), r.bytes, r.nvme_off))
     throw DeviceError(TC_EIO, "NVMe tier write failed for tensor " + std::to_string(r.id));
   r.nvme_valid = true;

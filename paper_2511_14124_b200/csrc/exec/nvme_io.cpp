@@ -10,6 +10,7 @@
 #include <cstdlib>
 
 #include "capi_common.hpp"
+#include "dataplane.cuh"
 #include "gds.hpp"
 
 namespace tcb {
@@ -173,8 +174,41 @@ std::uint64_t NvmeQueue::submit(Job j) {
 }
 
 std::uint64_t NvmeQueue::submit_read(void* dst, std::uint64_t bytes, std::uint64_t off, std::vector<cudaEvent_t> w,
-                                     std::vector<std::uint64_t> after) {
-  return submit(Job{false, false, dst, bytes, off, 0, std::move(w), std::move(after)});
+                                     std::vector<std::uint64_t> after, std::uint64_t packed_n) {
+  Job j{false, false, dst, bytes, off, 0, std::move(w), std::move(after)};
+  j.packed_n = packed_n;
+  return submit(std::move(j));
+}
+
+void NvmeQueue::forget_extent(std::uint64_t off) {
+  std::lock_guard<std::mutex> g(mu_);
+  extent_len_.erase(off);
+}
+
+// A packed state's write moves its prefix, plus the overflow area when a
+// tile uses it; a read of the extent moves what its last write moved. (O_DIRECT
+// files: whole 4 KiB blocks.)
+std::uint64_t NvmeQueue::effective_bytes(Job& j) {
+  std::uint64_t bytes = j.bytes;
+  if (j.packed_n && !j.device) {
+    const PackedLayout L = packed_layout(j.packed_n);
+    if (j.write) {
+      const auto* fl = reinterpret_cast<const std::uint32_t*>(static_cast<const std::uint8_t*>(j.buf) + L.flags);
+      bool ovf = false;
+      for (std::uint64_t t = 0; t < j.packed_n / kSplitTile && !ovf; ++t) ovf = (fl[t] & 1u) != 0;
+      bytes = ovf ? L.ovf + 2 * j.packed_n : L.bytes;
+      if (file_->direct()) bytes = (bytes + 4095) / 4096 * 4096;
+      bytes = std::min(bytes, j.bytes);
+      extent_len_[j.off] = bytes;
+    } else {
+      auto e = extent_len_.find(j.off);
+      if (e != extent_len_.end()) bytes = std::min(bytes, e->second);
+    }
+  } else if (j.write) {
+    extent_len_.erase(j.off);
+  }
+  (j.write ? bytes_written_ : bytes_read_) -= j.bytes - bytes;
+  return bytes;
 }
 
 std::uint64_t NvmeQueue::submit_read_device(void* dst, std::uint64_t bytes, std::uint64_t off,
@@ -188,8 +222,11 @@ std::uint64_t NvmeQueue::submit_write_device(const void* src, std::uint64_t byte
 }
 
 std::uint64_t NvmeQueue::submit_write(const void* src, std::uint64_t bytes, std::uint64_t off,
-                                      std::vector<cudaEvent_t> w, std::vector<std::uint64_t> after) {
-  return submit(Job{true, false, const_cast<void*>(src), bytes, off, 0, std::move(w), std::move(after)});
+                                      std::vector<cudaEvent_t> w, std::vector<std::uint64_t> after,
+                                      std::uint64_t packed_n) {
+  Job j{true, false, const_cast<void*>(src), bytes, off, 0, std::move(w), std::move(after)};
+  j.packed_n = packed_n;
+  return submit(std::move(j));
 }
 
 std::uint64_t NvmeQueue::done() const {
@@ -314,6 +351,7 @@ void NvmeQueue::dispatch() {
     }
     (j.write ? wait_w_ : wait_r_) += now_s() - j.t_submit;
     ++(j.write ? jobs_w_ : jobs_r_);
+    j.bytes = effective_bytes(j);
     const std::uint64_t n = std::max<std::uint64_t>(1, (j.bytes + kPiece - 1) / kPiece);
     remaining_[j.seq] = static_cast<std::uint32_t>(n);
     for (std::uint64_t k = 0; k < n; ++k) {

@@ -60,10 +60,17 @@ class NvmeQueue {
   // `after`: earlier jobs that must be complete before this one starts (the
   // buffer's previous jobs, the file extent's previous job). Jobs otherwise
   // start out of order, as soon as their events and `after` jobs are done.
+  // packed_n != 0: the buffer holds a packed split-master state of packed_n
+  // parameters (dataplane.cuh PackedLayout): a write moves only its prefix
+  // (+ the overflow area when a tile uses it: the flags are read from the
+  // buffer once its producer is done) and records that length for the
+  // extent; a later read of the extent moves that many bytes.
   std::uint64_t submit_read(void* dst, std::uint64_t bytes, std::uint64_t file_off, std::vector<cudaEvent_t> waits,
-                            std::vector<std::uint64_t> after = {});
+                            std::vector<std::uint64_t> after = {}, std::uint64_t packed_n = 0);
   std::uint64_t submit_write(const void* src, std::uint64_t bytes, std::uint64_t file_off,
-                             std::vector<cudaEvent_t> waits, std::vector<std::uint64_t> after = {});
+                             std::vector<cudaEvent_t> waits, std::vector<std::uint64_t> after = {},
+                             std::uint64_t packed_n = 0);
+  void forget_extent(std::uint64_t file_off);  // written outside the queue: whole length again
   // dst/src in HBM: the worker moves the bytes with GPUDirect Storage
   std::uint64_t submit_read_device(void* dst, std::uint64_t bytes, std::uint64_t file_off,
                                    std::vector<cudaEvent_t> waits, std::vector<std::uint64_t> after = {});
@@ -94,7 +101,10 @@ class NvmeQueue {
     std::vector<cudaEvent_t> waits;
     std::vector<std::uint64_t> after;
     double t_submit = 0;  // steady-clock seconds (TC_NVME_STATS)
+    std::uint64_t packed_n = 0;
   };
+  std::uint64_t effective_bytes(Job& j);  // mu_ held, at dispatch
+  std::map<std::uint64_t, std::uint64_t> extent_len_;  // file offset -> bytes the last packed write moved
   struct Piece {
     bool write;
     bool device;
