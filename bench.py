@@ -19,15 +19,19 @@ run), c4/c5 (one rank's shard of the 8-GPU configs on one GPU).
 value = W / step time, W = the config's migrated bytes per step (whole job):
         the reference's cache-decision bytes over the host link (its
         transfer_bytes on GPU-touching links) + the optimizer-state round
-        trip (every host-resident state chunk once H2D and once D2H). W is a
-        function of the trace and the decisions alone, identical in both arms,
-        so value ratios are step-time ratios.
+        trip (every host-resident state chunk once H2D and once D2H, in the
+        reference's 12 B/param layout). W is a function of the trace and the
+        decisions alone, identical in both arms, so value ratios are
+        step-time ratios. The engine moves fewer physical bytes (packed
+        split-master states, 9.44 B/param): the PCIe fractions and
+        `state_codec` report what crossed the link.
 
 --impl reference runs the reference's own CPU path on the box's host cores,
 with the oracle only (oracle/_ref = the unmodified reference compiled here,
 oracle/numerics.c): reference IPolicy decisions, host memcpy migrations (the
-NVMe tier as files, like the engine's), the gradient copy to host, OpenMP CPU-Adam and the bf16 parameter copy (the
-paper's CPU-Adam architecture), with the trace's compute time
+NVMe tier as files, like the engine's), the gradient copy to host, OpenMP
+CPU-Adam and the bf16 parameter copy (the paper's CPU-Adam architecture,
+PAPER.md:599), with the trace's compute time
 either overlapped with that host work (max(compute, host): the reported
 value, the most favourable CPU number) or serial (reported beside it).
 """
