@@ -37,9 +37,10 @@ def _sources():
     return cpp, cu
 
 
-def _headers():
-    return (glob.glob(os.path.join(ROOT, "include", "**", "*.h*"), recursive=True)
-            + glob.glob(os.path.join(CSRC, "**", "*.h*"), recursive=True))
+def _headers():  # .h, .hpp and .cuh (a header change rebuilds every object)
+    pats = ("*.h", "*.hpp", "*.cuh")
+    return [f for d in (os.path.join(ROOT, "include"), CSRC) for pat in pats
+            for f in glob.glob(os.path.join(d, "**", pat), recursive=True)]
 
 
 def _stale(src, obj, hdr_mtime):

@@ -30,14 +30,14 @@ AdamScalars adam_scalars(double lr, double b1, double b2, double eps, double wd,
 //  * m and v keep bits 0-23 (mantissa + the exponent's lowest bit) as they
 //    are; byte 3 (sign + the exponent's top 7 bits) is coded against the
 //    largest top-7 value of each 32-element group: m as a 4-bit offset (14 =
-//    top bits zero) with its sign, v as a 5-bit offset (30 = zero; v's sign
-//    is not stored). A tile (2048 elements) with any value outside those
-//    windows (or a negative v) is an overflow tile: byte 3 of its m's and v's
-//    lives in `ovf` (2 B/element), read and written by the kernel itself
-//    through a device-accessible pointer (the mapped tail of the state's
-//    pinned host slot), so the bytes that cross PCIe have a fixed size.
-//    Bytes are moved with byte permutes and SWAR arithmetic on 4 elements at
-//    a time.
+//    top bits zero, 15 = escape) with its sign, v as a 5-bit offset (30 =
+//    zero, 31 = escape; v's sign is not stored). An element outside those
+//    windows (or a negative v) is escaped: byte 3 of its m and v lives in
+//    `ovf` (2 B/element), which the kernel reads and writes itself through a
+//    device-accessible pointer (the mapped tail of the state's pinned host
+//    slot), so the bytes that cross PCIe have a fixed size; one flag byte per
+//    warp and tile says whether any element of its 256 used it. Bytes are
+//    moved with byte permutes and SWAR arithmetic on 4 elements at a time.
 // The kernel reads (lo, rb, B, planes) and writes (lo', rb', B', planes').
 // p, m, v are unused for packed chunks.
 struct AdamChunk {
@@ -64,7 +64,8 @@ constexpr std::uint64_t kSplitTile = 2048;  // elements per AdamW tile; packed c
 // lo u16 | rb 1 bit | mlo u16 (m bits 0-15) | mb2 u8 (m bits 16-23) | vlo u16 |
 // vb2 u8 | code u8 (m sign << 7 | m code << 3 | v code bits 0-2) | x2 2 bits
 // (v code bits 3-4); per 32-element group: base u16 (m's largest top-7 |
-// v's << 8); per tile: flags u32 (1 = overflow tile). The windows (m: 13
+// v's << 8); per tile: 8 flag bytes (one per 256 elements: an escape used the
+// overflow area). The windows (m: 13
 // steps of 2 binades, v: 29) cover the moments of a run whose gradient never
 // changes (v ~ g^2 spans twice g's binades); an EMA over changing gradients
 // is narrower.
@@ -84,7 +85,7 @@ TCB_HD inline PackedLayout packed_layout(std::uint64_t n) {
   L.x2 = L.code + n;
   L.base = L.x2 + n / 4;
   L.flags = L.base + n / 16;
-  L.bytes = (L.flags + n / 512 + 15) / 16 * 16;
+  L.bytes = (L.flags + n / 256 + 15) / 16 * 16;
   L.ovf = L.bytes;
   return L;
 }

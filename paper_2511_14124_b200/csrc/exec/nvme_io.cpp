@@ -193,9 +193,9 @@ std::uint64_t NvmeQueue::effective_bytes(Job& j) {
   if (j.packed_n && !j.device) {
     const PackedLayout L = packed_layout(j.packed_n);
     if (j.write) {
-      const auto* fl = reinterpret_cast<const std::uint32_t*>(static_cast<const std::uint8_t*>(j.buf) + L.flags);
+      const std::uint8_t* fl = static_cast<const std::uint8_t*>(j.buf) + L.flags;  // a byte per 256 elements
       bool ovf = false;
-      for (std::uint64_t t = 0; t < j.packed_n / kSplitTile && !ovf; ++t) ovf = (fl[t] & 1u) != 0;
+      for (std::uint64_t t = 0; t < j.packed_n / 256 && !ovf; ++t) ovf = fl[t] != 0;
       bytes = ovf ? L.ovf + 2 * j.packed_n : L.bytes;
       if (file_->direct()) bytes = (bytes + 4095) / 4096 * 4096;
       bytes = std::min(bytes, j.bytes);

@@ -86,7 +86,7 @@ def test_packed_state_layout_fits_its_slot():
     from paper_2511_14124_b200 import _native as N
     for n in (2048, 4096, 2048 * 37, 16865280):
         b = N.lib().tc_split_state_bytes(n)
-        assert b == (9 * n + n // 8 + n // 4 + n // 16 + n // 512 + 15) // 16 * 16
+        assert b == (9 * n + n // 8 + n // 4 + n // 16 + n // 256 + 15) // 16 * 16
         assert b % 16 == 0 and b + 2 * n <= 12 * n
 
 

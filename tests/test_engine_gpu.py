@@ -80,7 +80,7 @@ def check_engine(tr, m, cfg, iters=2, nvme_dir="", hoist=True, prestage=True, st
 
 def packed_bytes(n):
     """PCIe bytes of a packed split-master state of n parameters (dataplane.cuh PackedLayout)."""
-    return (9 * n + n // 8 + n // 4 + n // 16 + n // 512 + 15) // 16 * 16
+    return (9 * n + n // 8 + n // 4 + n // 16 + n // 256 + 15) // 16 * 16
 
 
 def assert_state_traffic(st, iters, n, S):
