@@ -167,9 +167,8 @@ int tc_adamw_batch(const tc_adam_chunk* chunks, uint32_t count, double lr, doubl
  *    writes B = RNE(master) itself;
  *  - m, v: bytes 0-2 as stored; byte 3 (sign + top 7 exponent bits) coded
  *    against the largest top-7 value of each 32-element group (m: sign +
- *    4-bit offset, v: 5-bit offset, each with a code for zero); a
- *    2048-element tile with a value outside those windows keeps byte 3 of
- *    its moments in the overflow area.
+ *    4-bit offset, v: 5-bit offset, each with a code for zero and one for
+ *    an escape); an escaped element's byte 3 lives in the overflow area.
  * Lossless for every bit pattern. tc_adamw_split_master updates such a state
  * in place, reading the current `param` (bf16, n) and writing the new one;
  * results are bit-identical to tc_adamw on the expanded state. */

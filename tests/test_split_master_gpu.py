@@ -79,7 +79,8 @@ def typical_moments(n, seed):
 def test_codec_exact_for_every_pattern(n):
     """Masters of every class, and moments from a typical run (no overflow
     tile) to every bit pattern (wide exponent spreads, zeros, denormals,
-    NaN/Inf, negative v: overflow tiles) -- all round-trip bit for bit."""
+    NaN/Inf, negative v: escapes to the overflow area) -- all round-trip bit
+    for bit."""
     bits = special_masters(n, n)
     p32 = torch.from_numpy(bits.view(np.float32).copy()).to(DEV)
     param = K.cast_f32_to_bf16(p32)  # the engine's own rounding: B = RNE(master)

@@ -29,7 +29,7 @@ plan.pack(src, dst)
 plan.unpack(dst, src)
 K.checksum(src)
 K.spin(5.0)
-# packed split-master codec + update, with overflow tiles (wild moments in every other tile)
+# packed split-master codec + update, with escapes to the overflow area (wild moments)
 n = 2048 * 5
 p32 = torch.randn(n, device="cuda") * 0.02
 mm = torch.randn(n, device="cuda") * 1e-4
@@ -56,7 +56,7 @@ for pol in ("tencache", "tencache+opt"):
     e.iteration(lr=1e-3, last=True)
     e.step_result()
     e.sync()
-    if pol == "tencache":  # a packed state with overflow tiles: the kernel's mapped-memory path
+    if pol == "tencache":  # a packed state with escapes: the kernel's mapped-memory path
         import numpy as np
         sid = n + 1
         st = e.read_tensor(sid, 6 * S).view(np.float32).copy()
