@@ -61,7 +61,7 @@ for what in "$@"; do
       python bench.py --steps 1 --warmup 3 --secondary "" --no-cpu-baseline > gpurun_out/${T}_launches_bench.log 2>&1
     echo "launch list rc $?" ;;
   ncu)
-    timeout 1200 ncu --set full --clock-control none --import-source on -k regex:adamw_tma -s 400 -c 1 \
+    timeout 1200 ncu --set full --clock-control none --import-source on -k regex:adamw_tma -s 120 -c 1 \
       -o gpurun_out/${T}_adamw_c3 python bench.py --config c3 --steps 1 --warmup 3 --secondary "" --no-cpu-baseline \
       > gpurun_out/${T}_ncu.log 2>&1; echo "ncu rc $?" ;;
   kernels)
