@@ -134,7 +134,7 @@ NvmeQueue::NvmeQueue(int device, const StripedFile* file) : device_(device), fil
   }
   dispatcher_ = std::thread([this] { dispatch(); });
   const char* env = std::getenv("TC_NVME_THREADS");
-  const int nw = env ? std::max(1, std::atoi(env)) : 16;
+  const int nw = env ? std::max(1, std::atoi(env)) : 32;
   for (int i = 0; i < nw; ++i) workers_.emplace_back([this] { work(); });
 }
 
