@@ -362,7 +362,11 @@ int tc_engine_sync(tc_engine* e);
  * so->compute_mode 0 also checksums every accessed chunk (tc_engine_step_result);
  * 3 = the caller's compute only. The engine's own stand-ins (modes 1, 2) do
  * not run. A backward step's gradient writes are ordered after the previous
- * update that read them. Not available with a ZeRO-3 exchange (TC_ECONFIG).
+ * update that read them. With a ZeRO-3 exchange every forward/backward step
+ * accesses one layer's chunks: step_begin all-gathers the layer into a flat
+ * view (tc_engine_zero3_views), a backward step's caller writes the
+ * full-layer gradient into the gradient view, and step_end sums it over the
+ * ranks into this rank's gradient chunks before their updates.
  * tc_engine_step_begin with too small a `ptrs` returns TC_ERANGE with the step
  * open (*n = its tensor count; read the addresses with tc_engine_gpu_ptr). */
 int tc_engine_iteration_begin(tc_engine* e, const tc_step_options* so, void* compute_stream);
@@ -440,6 +444,15 @@ int tc_engine_event_log(tc_engine* e, const char* path);
  * maps the peers. Accesses then run one gather+unpack kernel and, backward,
  * one pull-reduce kernel that read the peers' HBM directly. */
 int tc_engine_p2p_handles(tc_engine* e, uint8_t* out, size_t cap, size_t* n);
+/* ZeRO-3 per-step execution, between tc_engine_step_begin and step_end of a
+ * forward/backward step: the gathered layer (flat bf16, the layer table's
+ * elements, *layer_bytes = 2 x elements; read-only) and the gradient view of
+ * the same layout the caller writes in a backward step (its contents are
+ * undefined at step_begin: zero it before accumulating). Both are device
+ * memory, valid until step_end; write/read them on the compute stream.
+ * TC_EARG outside such a step, TC_ECONFIG without a ZeRO-3 exchange. The
+ * ranks run the same steps in the same order (the exchange pairs them). */
+int tc_engine_zero3_views(tc_engine* e, void** params, void** grads, uint64_t* layer_bytes);
 int tc_engine_enable_p2p(tc_engine* e, const uint8_t* all_blobs);
 /* Bytes all-gathered + reduce-scattered (NCCL payload, all ranks' pieces) so far. */
 uint64_t tc_engine_exchanged_bytes(tc_engine* e);

@@ -174,6 +174,8 @@ _SIGS = {
     "tc_engine_step_end": ([C.c_void_p, C.c_uint32], C.c_int),
     "tc_engine_regions": ([C.c_void_p, C.POINTER(C.c_void_p), C.POINTER(C.c_uint64), C.POINTER(C.c_void_p),
                            C.POINTER(C.c_uint64)], C.c_int),
+    "tc_engine_zero3_views": ([C.c_void_p, C.POINTER(C.c_void_p), C.POINTER(C.c_void_p), C.POINTER(C.c_uint64)],
+                              C.c_int),
     "tc_engine_iteration_end": ([C.c_void_p], C.c_int),
     "tc_engine_iteration_abort": ([C.c_void_p], C.c_int),
     "tc_engine_sync": ([C.c_void_p], C.c_int),

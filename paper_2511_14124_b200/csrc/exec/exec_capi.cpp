@@ -172,6 +172,20 @@ int tc_engine_regions(tc_engine* e, void** hbm_pool, uint64_t* hbm_pool_bytes, v
   })
 }
 
+int tc_engine_zero3_views(tc_engine* e, void** params, void** grads, uint64_t* layer_bytes) {
+  TC_GUARD({
+    if (!e) return set_error(TC_EARG, "null engine");
+    void* pb = nullptr;
+    void* gb = nullptr;
+    std::uint64_t n = 0;
+    e->ex->zero3_views(&pb, &gb, &n);
+    if (params) *params = pb;
+    if (grads) *grads = gb;
+    if (layer_bytes) *layer_bytes = n;
+    return TC_OK;
+  })
+}
+
 int tc_engine_sync(tc_engine* e) {
   TC_GUARD({
     e->ex->sync();

@@ -31,6 +31,14 @@ void Executor::param_enter(const TraceStep& step, cudaStream_t cs, bool external
     // update that read them is done
     if (external && step.phase == Phase::Backward && x.grad_reader) TCB_CK(cudaStreamWaitEvent(cs, x.grad_reader, 0));
   }
+  if (z3_ && external) {  // the caller reads the gathered layer (and, backward, writes its gradient view)
+    const std::uint32_t layer = z3_->plans.at(index_of(step.tensor_ids.front())).layer;
+    for (TensorId id : step.tensor_ids)
+      if (z3_->plans.at(index_of(id)).layer != layer)
+        throw DeviceError(TC_ECONFIG, "ZeRO-3 per-step execution needs every step to access one layer's chunks");
+    z3_->open_layer = layer;
+    if (step.phase == Phase::Backward) zero3_grad_fence(cs);
+  }
   wait_barriers(cs);
   TCB_CK(cudaEventRecord(go, cs));
   stalls_.push_back(Stall{reach, go, step.tensor_ids.front()});
@@ -42,7 +50,9 @@ void Executor::param_enter(const TraceStep& step, cudaStream_t cs, bool external
     else if (x.arrival)
       ontime_.emplace_back(reach, x.arrival);
     x.issued_since_access = 0;
-    if (z3_) {
+    if (z3_ && external) {
+      zero3_gather(x, cs);
+    } else if (z3_) {
       zero3_access(x, step.phase == Phase::Backward, cs);
     } else if (access_cursor_ < n_accesses_) {
       if (so_.compute_mode == 0 || !external)
@@ -77,6 +87,11 @@ void Executor::param_compute(const TraceStep& step, cudaStream_t cs) {
 // Everything the step computes is enqueued: its slots are read until here,
 // and a caller-computed backward step's gradients are final here.
 void Executor::param_exit(const TraceStep& step, cudaStream_t cs, bool external) {
+  if (z3_ && external) {  // the caller's full-layer gradient is summed into this rank's chunks
+    if (step.phase == Phase::Backward)
+      for (TensorId id : step.tensor_ids) zero3_reduce(rec(id), cs, false);
+    z3_->open_layer = -1;
+  }
   cudaEvent_t done = events_.get(false);
   TCB_CK(cudaEventRecord(done, cs));
   for (TensorId id : step.tensor_ids) {
@@ -439,7 +454,6 @@ void Executor::iteration(const StepOptions& so, cudaStream_t compute) {
 void Executor::iteration_begin(const StepOptions& so, cudaStream_t compute, bool external) {
   TCB_CK(cudaSetDevice(device_));
   if (open_) throw DeviceError(TC_EARG, "iteration_begin: an iteration is already open");
-  if (external && z3_) throw DeviceError(TC_ECONFIG, "per-step execution with a ZeRO-3 exchange is not supported");
   if (compute == nullptr) {
     if (!compute_owned_) TCB_CK(cudaStreamCreateWithFlags(&compute_owned_, cudaStreamNonBlocking));
     compute = compute_owned_;

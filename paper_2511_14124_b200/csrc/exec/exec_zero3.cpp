@@ -93,6 +93,13 @@ void Executor::enable_zero3(int world, int rank, const ncclUniqueId& id, const s
 // full-layer gradient of those pieces (stand-in: seeded per rank), packs it
 // rank-major and reduce-scatters it (sum) into this rank's gradient chunk.
 void Executor::zero3_access(TensorRec& x, bool backward, cudaStream_t cs) {
+  zero3_gather(x, cs);
+  if (backward) zero3_reduce(x, cs, true);
+}
+
+// The gather half of an access: chunk x's pieces of the layer from every rank
+// into the flat layer view (and their checksums).
+void Executor::zero3_gather(TensorRec& x, cudaStream_t cs) {
   Zero3& z = *z3_;
   const Zero3::ChunkPlan& cp = z.plans.at(index_of(x.id));
   const unsigned peers_n = static_cast<unsigned>(z.world - 1);
@@ -123,17 +130,33 @@ void Executor::zero3_access(TensorRec& x, bool backward, cudaStream_t cs) {
     }
     ++access_cursor_;
   }
-  if (!backward) return;
-  if (z.p2p) {  // my gradient view is refilled only after every peer pulled the previous one
-    const std::uint32_t g = ++z.grad_epoch;
-    if (peers_n && g > 1) stream_wait_value32(cs, &z.ctl->gcnt, (g - 1) * peers_n);
+}
+
+// Gradient view writes from here on: every peer pulled the view's previous
+// contents (p2p; NCCL reads it synchronously on this stream).
+void Executor::zero3_grad_fence(cudaStream_t cs) {
+  Zero3& z = *z3_;
+  const unsigned peers_n = static_cast<unsigned>(z.world - 1);
+  if (z.p2p && peers_n && z.grad_epoch > 0) stream_wait_value32(cs, &z.ctl->gcnt, z.grad_epoch * peers_n);
+}
+
+// The reduce half of a backward access: the full-layer gradient of chunk x's
+// pieces in the gradient view (stand_in: seeded per rank, written here; else
+// the caller's, written since zero3_grad_fence) is summed over the ranks into
+// this rank's gradient chunk.
+void Executor::zero3_reduce(TensorRec& x, cudaStream_t cs, bool stand_in) {
+  Zero3& z = *z3_;
+  const Zero3::ChunkPlan& cp = z.plans.at(index_of(x.id));
+  if (stand_in) {
+    zero3_grad_fence(cs);
+    for (const auto& [off, nb] : cp.pieces) {
+      TCB_CK(launch_fill_normal_bf16(reinterpret_cast<std::uint16_t*>(z.gview + off), nb / 2, 1e-3f,
+                                     static_cast<std::uint64_t>(adam_step_) * 1000003ull + static_cast<std::uint64_t>(z.rank),
+                                     (static_cast<std::uint64_t>(cp.layer) << 40) + off / 2, cs));
+      ++stats_.kernel_launches;
+    }
   }
-  for (const auto& [off, nb] : cp.pieces) {
-    TCB_CK(launch_fill_normal_bf16(reinterpret_cast<std::uint16_t*>(z.gview + off), nb / 2, 1e-3f,
-                                   static_cast<std::uint64_t>(adam_step_) * 1000003ull + static_cast<std::uint64_t>(z.rank),
-                                   (static_cast<std::uint64_t>(cp.layer) << 40) + off / 2, cs));
-    ++stats_.kernel_launches;
-  }
+  if (z.p2p) ++z.grad_epoch;
   if (z.p2p) {  // fused pack + reduce-scatter: pull my piece from every rank's view and sum
     TCB_CK(launch_p2p_publish_grad(z.ctl, z.grad_epoch, cs));
     TCB_CK(launch_p2p_pull_reduce(z.peers, z.grad_epoch, cp.rank_view_off[z.rank], cp.rank_bytes[z.rank], z.S,
@@ -151,6 +174,19 @@ void Executor::zero3_access(TensorRec& x, bool backward, cudaStream_t cs) {
   cudaEvent_t e = events_.get(false);
   TCB_CK(cudaEventRecord(e, cs));
   x.grad_ready = e;
+}
+
+// Between step_begin and step_end of a caller-computed step: the flat layer
+// view the step gathered (read it on the compute stream) and the gradient
+// view the caller fills for a backward step (same layout; summed over the
+// ranks into this rank's chunks at step_end).
+void Executor::zero3_views(void** params, void** grads, std::uint64_t* layer_bytes) {
+  if (!z3_) throw ConfigError("zero3_views: no ZeRO-3 exchange (tc_engine_enable_zero3)");
+  if (!open_ || !open_->in_step || !open_->external || z3_->open_layer < 0)
+    throw DeviceError(TC_EARG, "zero3_views: no caller-computed forward/backward step open");
+  *params = z3_->view;
+  *grads = z3_->gview;
+  *layer_bytes = 2 * z3_->layer_elems.at(static_cast<std::size_t>(z3_->open_layer));
 }
 
 // This rank's IPC handles: HBM parameter pool, control block, gradient view.

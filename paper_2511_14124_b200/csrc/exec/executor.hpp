@@ -176,6 +176,7 @@ struct Zero3 {
   std::vector<void*> opened;               // IPC mappings to close
   std::vector<std::uint32_t> access_epoch;  // per chunk
   std::uint32_t grad_epoch = 0;
+  std::int64_t open_layer = -1;  // layer in the views during a caller-computed step
 };
 
 struct StepOptions {
@@ -209,6 +210,8 @@ class Executor {
   void* gpu_ptr(tencache::TensorId id);
   void* grad_ptr(tencache::TensorId id);
   void regions(void** pool, std::uint64_t* pool_bytes, void** grads, std::uint64_t* grad_bytes);
+  // ZeRO-3, inside a caller-computed step: the gathered layer and its gradient view
+  void zero3_views(void** params, void** grads, std::uint64_t* layer_bytes);
   std::uint64_t tensor_bytes(tencache::TensorId id) { return rec(id).bytes; }
   void enable_zero3(int world, int rank, const ncclUniqueId& id, const std::uint64_t* layer_elems,
                     const std::uint64_t* layer_per, std::uint32_t n_layers);
@@ -289,6 +292,9 @@ class Executor {
   };
   std::optional<OpenIter> open_;
   void zero3_access(TensorRec& x, bool backward, cudaStream_t cs);
+  void zero3_gather(TensorRec& x, cudaStream_t cs);
+  void zero3_grad_fence(cudaStream_t cs);
+  void zero3_reduce(TensorRec& x, cudaStream_t cs, bool stand_in);
   void optimizer_work(TensorRec& s, TensorRec& p);
   struct UpdateJob {
     TensorRec* s = nullptr;

@@ -58,6 +58,13 @@ class Engine:
         N.check(N.lib().tc_engine_regions(self._h, C.byref(pb), C.byref(pn), C.byref(gb), C.byref(gn)))
         return pb.value, pn.value, gb.value, gn.value
 
+    def zero3_views(self):
+        """(layer_ptr, grad_view_ptr, layer_bytes) of the open ZeRO-3 step --
+        tc_engine_zero3_views."""
+        pb, gb, n = C.c_void_p(), C.c_void_p(), C.c_uint64()
+        N.check(N.lib().tc_engine_zero3_views(self._h, C.byref(pb), C.byref(gb), C.byref(n)))
+        return pb.value, gb.value, n.value
+
     # -- execution --------------------------------------------------------
     def iteration(self, lr=1e-4, beta1=0.9, beta2=0.999, eps=1e-8, weight_decay=0.01, grad_scale=1.0,
                   compute_mode=0, spin_ctas=1, stream=None, hoist=True, prestage=True, last=False):

@@ -218,7 +218,8 @@ class OffloadedTrainer:
                         gu8[fr.src:fr.src + fr.nbytes])
 
     def _release(self, L: LayerLayout):
-        for _, p, _, _ in L.params:
+        for entry in L.params:
+            p = entry[1]
             p.grad = None
             p.data = self._empty
 
@@ -329,3 +330,135 @@ def _alias(ptr, nbytes, device):
     if not ptr or not nbytes:
         return torch.empty(0, dtype=torch.uint8, device=device)
     return torch.as_tensor(_CAI(ptr, nbytes), device=device)
+
+
+# -- ZeRO-3 data-parallel training ------------------------------------------
+
+
+@dataclass
+class ShardedLayer:
+    chunk_ids: list     # trace tensor ids of this rank's chunks of the layer
+    params: list        # [(name, param, byte offset in the flat layer, bytes, shape)]
+    elems: int          # flat layer elements (16-byte aligned)
+    per: int            # elements per rank (the exchange's layer table)
+    lo: int             # this rank's elements [lo, hi)
+    hi: int
+
+
+def plan_zero3(layers, world: int, rank: int, chunk_bytes: int):
+    """Flat layer layout of `layers` and rank `rank`'s shard of each layer, cut
+    into chunks of S bytes (the zero3.py partitioning: rank r owns elements
+    [r*per, (r+1)*per); per rounded up to 8 elements so that every piece is
+    16-byte aligned; the same chunk count per layer on every rank)."""
+    S = chunk_bytes
+    out, cid = [], 1
+    for li, mod in enumerate(layers):
+        off, plist = 0, []
+        for name, p in mod.named_parameters():
+            if p.dtype != torch.bfloat16:
+                raise TypeError(f"layer {li} parameter {name}: the engine's chunks hold bf16 parameters, got {p.dtype}")
+            off = -(-off // ALIGN) * ALIGN
+            plist.append((name, p, off, 2 * p.numel(), tuple(p.shape)))
+            off += 2 * p.numel()
+        E = -(-off // ALIGN) * ALIGN // 2
+        per = -(-(-(-E // world)) // 8) * 8
+        k = max(1, -(-2 * per // S))
+        lo = min(rank * per, E)
+        out.append(ShardedLayer(list(range(cid, cid + k)), plist, E, per, lo, min(lo + per, E)))
+        cid += k
+    return out
+
+
+def flat_layer_bytes(L: ShardedLayer):
+    """The layer's parameters laid out flat (padding zero), as host bytes."""
+    buf = np.zeros(2 * L.elems, np.uint8)
+    for _, p, off, nb, _ in L.params:
+        buf[off:off + nb] = p.detach().contiguous().view(-1).view(torch.int16).cpu().numpy().view(np.uint8)
+    return buf
+
+
+class Zero3Trainer(OffloadedTrainer):
+    """Data-parallel ZeRO-3 training through one engine per rank (SURVEY.md
+    §8e with the §8(b) per-step caller): rank `rank` of `world` holds only its
+    shard of every layer's parameters and optimizer states, in its engine's
+    chunks (GPU tier `gpu_chunks` chunks, the rest in pinned host memory).
+
+    Per forward/backward step the engine all-gathers the layer from every
+    rank into a flat view (``tc_engine_zero3_views``; the fused peer-memory
+    kernels with exchange="p2p", NCCL all-gather + unpack with "nccl"); the
+    layer's parameters become views of it, so nothing is assembled on the
+    Python side. A backward step's parameters' ``.grad`` are views of the
+    engine's full-layer gradient view (zeroed first, autograd accumulates into
+    it); step_end sums that view over the ranks into this rank's gradient
+    chunks and runs the fused AdamW of the chunks hoisted behind the step.
+    Gradients are SUMMED over ranks: scale the loss by 1/world for the mean.
+    Every rank must run the same steps (the exchange pairs them); `layers`
+    must hold the same initial parameters on every rank."""
+
+    def __init__(self, layers, loss_fn, workdir, world: int, rank: int, chunk_bytes: int, gpu_chunks: int,
+                 iterations: int = 1, exchange: str = "p2p", group=None, policy: str = "tencache", device: int = 0,
+                 lr=1e-3, betas=(0.9, 0.999), eps=1e-8, weight_decay=0.01, fwd_us=None, bwd_us=None,
+                 opt_stage_slots: int = 4):
+        from types import SimpleNamespace
+
+        from . import zero3 as Z
+        self.layers, self.loss_fn = list(layers), loss_fn
+        self.world, self.rank = world, rank
+        self.S = S = chunk_bytes
+        self.layout = plan_zero3(self.layers, world, rank, chunk_bytes)
+        self.n_chunks = n = sum(len(L.chunk_ids) for L in self.layout)
+        os.makedirs(workdir, exist_ok=True)
+        self.trace_path = write_layer_trace(self.layout, S, os.path.join(workdir, f"zero3_r{rank}.jsonl"),
+                                            iterations, fwd_us, bwd_us)
+        self.machine_path = T.write_machine(os.path.join(workdir, f"machine_r{rank}.json"), gpu_chunks * S,
+                                            (n - gpu_chunks) * S + n * 6 * S)
+        self.config = {"policy": policy}
+        self.hyper = dict(lr=lr, beta1=betas[0], beta2=betas[1], eps=eps, weight_decay=weight_decay)
+        self.device = torch.device("cuda", device)
+        self.engine = Engine(self.trace_path, self.machine_path, self.config, device=device,
+                             opt_stage_slots=opt_stage_slots)
+        for L in self.layout:  # this rank's shard, chunked (tail zero)
+            shard = np.zeros(len(L.chunk_ids) * S, np.uint8)
+            shard[:2 * (L.hi - L.lo)] = flat_layer_bytes(L)[2 * L.lo:2 * L.hi]
+            for k, cid in enumerate(L.chunk_ids):
+                chunk = shard[k * S:(k + 1) * S]
+                self.engine.write_tensor(cid, chunk)
+                self.engine.write_tensor(n + cid, init_state_bytes(chunk))
+        Z.enable(self.engine, SimpleNamespace(layers=self.layout), rank, world, group=group, exchange=exchange)
+        self._max_layer = max(2 * L.elems for L in self.layout)
+        self._views = None
+        self._gview = None
+        self._empty = torch.empty(0, dtype=torch.bfloat16, device=self.device)
+        for L in self.layout:
+            self._release(L)
+        self.stream = torch.cuda.Stream(device=self.device)
+        self.n_steps = sum(1 for l in open(self.trace_path) if '"s"' in l)
+        self.n_layers = len(self.layout)
+
+    def _materialize(self, L: ShardedLayer, ptrs):
+        """Point every parameter of L at its bytes in the gathered layer view."""
+        pv, gv, nb = self.engine.zero3_views()
+        if nb != 2 * L.elems:
+            raise RuntimeError(f"engine's layer view holds {nb} bytes, layer has {2 * L.elems}")
+        if self._views is None or self._views[0] != (pv, gv):
+            self._views = ((pv, gv), _alias(pv, self._max_layer, self.device), _alias(gv, self._max_layer, self.device))
+        view = self._views[1]
+        self._gview = self._views[2]
+        for _, p, off, nbytes, shape in L.params:
+            p.data = view[off:off + nbytes].view(torch.bfloat16).view(shape)
+
+    def _attach_grads(self, L: ShardedLayer):
+        self._gview[:2 * L.elems].zero_()  # padding stays zero
+        for _, p, off, nbytes, shape in L.params:
+            p.grad = self._gview[off:off + nbytes].view(torch.bfloat16).view(shape)
+
+    def _flush_grads(self, L):
+        pass  # the gradients are already in the engine's view
+
+    def read_params(self):
+        """Per layer: this rank's shard of the flat layer (bf16 bits, uint16)."""
+        out = []
+        for L in self.layout:
+            raw = np.concatenate([self.engine.read_tensor(c, self.S) for c in L.chunk_ids])
+            out.append(raw[:2 * (L.hi - L.lo)].view(np.uint16).copy())
+        return out

@@ -75,3 +75,36 @@ def test_layer_trace_decisions_match_reference(tmpd, policy):
     assert ra == rb
     assert ra["param_accesses"] == 3 * 2 * n
     assert ra["transfer_bytes"].get("cpu->gpu", 0) > 0  # the tier is too small: chunks migrate
+
+
+@pytest.mark.parametrize("world", [1, 2, 3, 8])
+def test_zero3_layout_partitions_every_layer(tmpd, world):
+    """Zero3Trainer's layout: the ranks' shards tile each flat layer exactly,
+    every piece is 16-byte aligned, every rank has the same chunk count per
+    layer (the exchange pairs the ranks' chunks), every parameter lies inside
+    the flat layer once; each rank's trace gets the reference's decisions."""
+    from paper_2511_14124_b200.training import flat_layer_bytes, plan_zero3
+    ls = layers()
+    S = 4096
+    per_rank = [plan_zero3(ls, world, r, S) for r in range(world)]
+    for li in range(len(ls)):
+        Ls = [lay[li] for lay in per_rank]
+        assert len({len(L.chunk_ids) for L in Ls}) == 1
+        assert len({(L.elems, L.per) for L in Ls}) == 1
+        L0 = Ls[0]
+        assert L0.per % 8 == 0 and L0.per * world >= L0.elems and 2 * L0.per <= len(L0.chunk_ids) * S
+        assert Ls[0].lo == 0 and Ls[-1].hi == L0.elems
+        assert all(a.hi == b.lo for a, b in zip(Ls, Ls[1:]))
+        spans = sorted((off, off + nb) for _, _, off, nb, _ in L0.params)
+        assert spans[0][0] == 0 and spans[-1][1] <= 2 * L0.elems and L0.elems * 2 % 16 == 0
+        assert all(a[1] <= b[0] and b[0] % 16 == 0 for a, b in zip(spans, spans[1:]))
+        flat = flat_layer_bytes(L0)
+        for _, p, off, nb, _ in L0.params:
+            assert np.array_equal(flat[off:off + nb], p.detach().reshape(-1).view(torch.int16).numpy().view(np.uint8))
+    ids = [c for L in per_rank[-1] for c in L.chunk_ids]
+    assert ids == list(range(1, len(ids) + 1))
+    n = len(ids)
+    tp = write_layer_trace(per_rank[-1], S, os.path.join(tmpd, "z.jsonl"), iterations=2)
+    mp = T.write_machine(os.path.join(tmpd, "zm.json"), max(4, n // 3) * S, n * 7 * S)
+    cfg = {"policy": "tencache"}
+    assert ref.decisions(tp, mp, cfg, with_pools=True) == P.decisions(tp, mp, cfg, with_pools=True)
