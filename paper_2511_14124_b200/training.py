@@ -241,6 +241,93 @@ class OffloadedTrainer:
         cur.wait_stream(self.stream)
         return loss
 
+    # -- the same steps driven by module hooks -------------------------------
+    def register_hooks(self):
+        """Drive the engine from the layers' own forward pre/post hooks (the
+        paper's call points) instead of step():
+
+            model = trainer.register_hooks()          # nn.Sequential of the layers
+            with trainer.iteration(last=...):
+                loss = loss_fn(model(x), y)
+                loss.backward()
+            # optimizer steps + iteration end ran on leaving the block
+
+        pre-hook: step_begin of the layer's forward step, parameters become
+        views of the engine's memory, the layer runs without autograd (its
+        slots are handed back at the post-hook); post-hook: step_end, and the
+        output is tied into the autograd graph by a boundary node that saves
+        the layer input. Backward reaches the boundaries in reverse layer
+        order (the trace's backward order); each one opens the layer's
+        backward step, recomputes the layer from its input with autograd,
+        back-propagates into the engine's gradient buffers and ends the
+        step. Returns the layers as one nn.Sequential."""
+        if getattr(self, "_hooks", None):
+            return self._model
+        self._hooks, self._it = [], None
+        for li, mod in enumerate(self.layers):
+            self._hooks.append(mod.register_forward_pre_hook(lambda m, args, li=li: self._pre_hook(li)))
+            self._hooks.append(mod.register_forward_hook(lambda m, args, out, li=li: self._post_hook(li, args, out)))
+        self._model = torch.nn.Sequential(*self.layers)
+        return self._model
+
+    def remove_hooks(self):
+        for h in getattr(self, "_hooks", None) or []:
+            h.remove()
+        self._hooks = []
+
+    def iteration(self, last=False):
+        """Context of one hooked training iteration (see register_hooks):
+        iteration_begin and the engine's stream on entry; on exit the
+        optimizer steps (the engine's fused AdamW) and iteration_end, or
+        iteration_abort if the block raised."""
+        return _HookedIteration(self, last)
+
+    def _pre_hook(self, li):
+        it = self._it
+        if it is None or it["recompute"]:
+            if it is None:
+                raise RuntimeError("hooked layer called outside trainer.iteration()")
+            return
+        if it["step"] != li:
+            raise RuntimeError(f"layer {li} called as forward step {it['step']}: layers must run once each, in order")
+        self._materialize(self.layout[li], self.engine.step_begin(it["step"]))
+        it["grad_mode"] = torch.is_grad_enabled()
+        torch.set_grad_enabled(False)
+
+    def _post_hook(self, li, args, out):
+        it = self._it
+        if it["recompute"]:
+            return None
+        torch.set_grad_enabled(it["grad_mode"])
+        self._release(self.layout[li])
+        self.engine.step_end(it["step"])
+        it["step"] += 1
+        if not it["grad_mode"]:
+            return None
+        return _LayerBoundary.apply(self, li, args[0], it["token"], out)
+
+    def _backward_step(self, li, xin, gy):
+        """Layer li's backward step, from its boundary node."""
+        it = self._it
+        L = self.layout[li]
+        self._materialize(L, self.engine.step_begin(it["step"]))
+        self._attach_grads(L)
+        if xin.is_floating_point():
+            xin = xin.detach().requires_grad_(True)
+        it["recompute"] = True
+        try:
+            with torch.enable_grad():
+                y = self.layers[li](xin)
+            torch.autograd.backward(y, gy)
+        finally:
+            it["recompute"] = False
+        gx = xin.grad if xin.requires_grad else None
+        self._flush_grads(L)
+        self._release(L)
+        self.engine.step_end(it["step"])
+        it["step"] += 1
+        return gx
+
     def _abort(self):
         for L in self.layout:
             self._release(L)
@@ -317,6 +404,69 @@ class OffloadedTrainer:
 
     def close(self):
         self.engine.close()
+
+
+class _LayerBoundary(torch.autograd.Function):
+    """Ties a layer's (autograd-free) output into the graph; its backward is
+    the layer's backward step (OffloadedTrainer._backward_step). `token`
+    requires grad so that the first layer's boundary is reached even when
+    the model input (token ids) does not."""
+
+    @staticmethod
+    def forward(ctx, trainer, li, x, token, y):
+        ctx.trainer, ctx.li = trainer, li
+        ctx.x = x.detach()
+        return y.detach()
+
+    @staticmethod
+    def backward(ctx, gy):
+        gx = ctx.trainer._backward_step(ctx.li, ctx.x, gy)
+        ctx.x = None
+        return None, None, gx, None, None
+
+
+class _HookedIteration:
+    def __init__(self, trainer, last):
+        self.tr, self.last = trainer, last
+
+    def __enter__(self):
+        tr = self.tr
+        if not getattr(tr, "_hooks", None):
+            raise RuntimeError("call register_hooks() first")
+        self.grad_mode = torch.is_grad_enabled()
+        self.cur = torch.cuda.current_stream(tr.device)
+        tr.stream.wait_stream(self.cur)
+        self.ctx = torch.cuda.stream(tr.stream)
+        self.ctx.__enter__()
+        tr.engine.iteration_begin(stream=tr.stream.cuda_stream, last=self.last, **tr.hyper)
+        tr._it = {"step": 0, "recompute": False, "grad_mode": True,
+                  "token": torch.empty(0, device=tr.device, requires_grad=True)}
+        return tr
+
+    def __exit__(self, et, ev, tb):
+        tr = self.tr
+        try:
+            if et is None:
+                n_fb = 2 * tr.n_layers
+                if tr._it["step"] != n_fb:
+                    raise RuntimeError(f"iteration left after {tr._it['step']} of {n_fb} forward/backward steps "
+                                       "(run the model forward and loss.backward() inside the block)")
+                for i in range(n_fb, tr.n_steps):  # optimizer steps: the engine's fused AdamW
+                    tr.engine.step_begin(i)
+                    tr.engine.step_end(i)
+                tr.engine.iteration_end()
+            else:
+                tr._abort()
+        except BaseException:
+            if et is None:
+                tr._abort()
+            raise
+        finally:
+            tr._it = None
+            torch.set_grad_enabled(self.grad_mode)
+            self.ctx.__exit__(None, None, None)
+            self.cur.wait_stream(tr.stream)
+        return False
 
 
 class _CAI:

@@ -128,7 +128,7 @@ def plain_torch_losses(layers, data):
         with torch.no_grad():
             for p, mp in zip(params, master):
                 p.copy_(mp.to(torch.bfloat16))
-        losses.append(float(loss))
+        losses.append(float(loss.detach()))
     return losses
 
 
@@ -211,3 +211,44 @@ def test_step_api_order_is_enforced(tmp_path):
     e.iteration(lr=1e-3)
     e.sync()
     tr.close()
+
+
+def test_module_hooks_drive_the_same_steps(tmp_path):
+    """The engine driven by the layers' forward pre/post hooks and autograd
+    boundary nodes (OffloadedTrainer.register_hooks: the user writes a plain
+    `loss_fn(model(x), y).backward()`) runs exactly the explicit loop's steps:
+    losses, every [p32 | m | v] state and every bf16 parameter are
+    bit-identical to OffloadedTrainer.step's after each step."""
+    from paper_2511_14124_b200.training import OffloadedTrainer
+
+    steps = 3
+    block_bytes = sum(2 * p.numel() for p in make_layers()[1].parameters())
+    S = -(-(block_bytes // 2 + 4096) // 4096) * 4096
+    kw = dict(chunk_bytes=S, gpu_chunks=6, iterations=steps, **HP)
+    explicit = OffloadedTrainer(make_layers(), loss_fn, str(tmp_path / "a"), **kw)
+    hooked = OffloadedTrainer(make_layers(), loss_fn, str(tmp_path / "b"), **kw)
+    model = hooked.register_hooks()
+    for t, (x, y) in enumerate(batches(steps), start=1):
+        want = float(explicit.step(x, y, last=t == steps))
+        with hooked.iteration(last=t == steps):
+            loss = loss_fn(model(x), y)
+            loss.backward()
+        assert float(loss.detach()) == want, (t, float(loss), want)
+        a, b = explicit.read_states(), hooked.read_states()
+        for c in a:
+            for u, w in zip(a[c], b[c]):
+                assert np.array_equal(u.view(np.uint32), w.view(np.uint32)), f"step {t}: state {c} differs"
+        for da, db in zip(explicit.read_params(), hooked.read_params()):
+            for k in da:
+                assert torch.equal(da[k].view(torch.int16), db[k].view(torch.int16)), f"step {t}: {k} differs"
+    assert hooked.engine.stats()["param_hits"] == explicit.engine.stats()["param_hits"]
+    # a failing step aborts the iteration; the next one runs
+    with pytest.raises(ZeroDivisionError):
+        with hooked.iteration():
+            model(batches(1)[0][0])
+            1 / 0
+    with hooked.iteration(last=True):
+        loss_fn(model(x), y).backward()
+    assert torch.is_grad_enabled()
+    explicit.close()
+    hooked.close()

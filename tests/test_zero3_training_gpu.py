@@ -191,3 +191,25 @@ def test_zero3_training_two_ranks_one_gpu():
         for t, (a, w) in enumerate(zip(losses, want)):
             assert abs(a - w[r]) <= 2e-2 * abs(w[r]), (r, t, losses, want)
     print(f"\nrank losses {[res[r][0] for r in range(world)]}\ntorch {want}")
+
+
+def test_zero3_module_hooks_match_the_explicit_loop(tmp_path):
+    """Zero3Trainer driven by module hooks (register_hooks) == its explicit
+    loop, bit for bit (world 1, fused exchange)."""
+    from paper_2511_14124_b200.training import Zero3Trainer
+    steps = 2
+    kw = dict(world=1, rank=0, chunk_bytes=S, gpu_chunks=8, iterations=steps, exchange="p2p", **HP)
+    a = Zero3Trainer(make_layers(), loss_fn, str(tmp_path / "a"), **kw)
+    b = Zero3Trainer(make_layers(), loss_fn, str(tmp_path / "b"), **kw)
+    model = b.register_hooks()
+    for t, (x, y) in enumerate(batches(steps), start=1):
+        want = float(a.step(x, y, last=t == steps))
+        with b.iteration(last=t == steps):
+            loss = loss_fn(model(x), y)
+            loss.backward()
+        assert float(loss.detach()) == want
+        sa, sb = a.read_states(), b.read_states()
+        assert all(np.array_equal(u.view(np.uint32), w.view(np.uint32)) for c in sa for u, w in zip(sa[c], sb[c]))
+        assert all(np.array_equal(u, w) for u, w in zip(a.read_params(), b.read_params()))
+    a.close()
+    b.close()
