@@ -76,6 +76,18 @@ for what in "$@"; do
         > gpurun_out/${T}_sanitize_$tool.log 2>&1
       echo "$tool rc $?"; tail -2 gpurun_out/${T}_sanitize_$tool.log
     done ;;
+  contention)
+    timeout 600 python tools/adamw_contention_r2.py > gpurun_out/${T}_contention.log 2>&1; echo "contention rc $?"
+    cp gpurun_out/adamw_contention_r2.json gpurun_out/${T}_adamw_contention_r2.json ;;
+  adamstream)
+    # C3 AdamW placement A/B, interleaved: compute stream (world-1 default) vs the opt stream, batch sizes
+    for r in 1 2; do for v in "ON=1" "ON=1 B=8" "ON=0"; do
+      on=${v#ON=}; on=${on%% *}; b=""; [[ $v == *B=* ]] && b=${v##*B=}
+      tag=c3_on${on}_b${b:-d}_r$r
+      ( export TC_ADAM_ON_COMPUTE=$on; [ -n "$b" ] && export TC_ADAM_BATCH=$b
+        bench --config c3 --secondary "" --no-cpu-baseline > gpurun_out/${T}_$tag.json 2> gpurun_out/${T}_$tag.err )
+      echo "$tag rc $?"
+    done; done ;;
   *) echo "unknown recipe $what"; exit 2 ;;
   esac
 done
