@@ -334,11 +334,15 @@ class Executor {
   // of the HBM peak at 1 / 2 / 4 / 8, step time unchanged,
   // profiles/r02_adam_batch_packed.json). On the compute stream
   // (migration-bound) single updates keep each state's write-back earliest
-  // (C2 steps 2-4 % shorter, profiles/r02_adam_batch_ab.json). TC_ADAM_BATCH
-  // overrides (1..8).
+  // (C2 steps 2-4 % shorter, profiles/r02_adam_batch_ab.json); a ZeRO-3
+  // rank at world 1 keeps batches of 8 there too (C3: event-timed 0.44 at 1
+  // vs 0.59 at 8, step within 0.3 %, profiles/r02_adam_placement_c3.json).
+  // TC_ADAM_BATCH overrides (1..8).
   static constexpr std::size_t kAdamBatchConcurrent = 8;
   std::size_t adam_batch_env_ = 0;
-  std::size_t adam_batch() const { return adam_batch_env_ ? adam_batch_env_ : adam_stream() == opt_ ? kAdamBatchConcurrent : 1; }
+  std::size_t adam_batch() const {
+    return adam_batch_env_ ? adam_batch_env_ : adam_stream() == opt_ || z3_ ? kAdamBatchConcurrent : 1;
+  }
   std::size_t stage_state(TensorRec& s);
   void refill_stages(std::size_t want_staged);
   // NVMe lookahead: the iteration's NVMe -> pinned fetches of optimizer states
@@ -404,9 +408,15 @@ class Executor {
   // cross-stream scheduling latency); on the opt stream when compute-bound, to
   // overlap. TC_ADAM_ON_COMPUTE=0/1 overrides.
   bool adam_on_compute_ = false;
-  // never with a ZeRO-3 exchange: an in-place update may wait for peers'
-  // reads of its slot, which must not stall this rank's compute stream
-  cudaStream_t adam_stream() const { return adam_on_compute_ && compute_ && !z3_ ? compute_ : opt_; }
+  // never with a ZeRO-3 exchange between ranks: an in-place update may wait
+  // for peers' reads of its slot, which must not stall this rank's compute
+  // stream. World 1 has no peers: C3 at N=1 (migration-bound) runs its
+  // updates between the layers' GEMMs, on the whole GPU instead of beside
+  // them (event-timed 0.55 -> 0.59 of the HBM peak, migration hidden 0.95 ->
+  // 0.99, profiles/r02_adam_placement_c3.json)
+  cudaStream_t adam_stream() const {
+    return adam_on_compute_ && compute_ && (!z3_ || z3_->world == 1) ? compute_ : opt_;
+  }
   double stamp_pre_ns_ = 0, stamp_post_ns_ = 0, stamps_ = 0;
   bool lookahead_ = true;           // TC_LOOKAHEAD: decide + pre-stage iteration t+1 at the end of t
   std::optional<std::vector<Hook>> ahead_;

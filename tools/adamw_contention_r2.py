@@ -12,6 +12,8 @@ host's submission latency is not in it.
 import json
 import os
 import sys
+import threading
+import time
 
 import torch
 
@@ -49,6 +51,39 @@ X = torch.randn(16384, 4096, device="cuda").to(torch.bfloat16)
 W = torch.randn(4096, 11008, device="cuda").to(torch.bfloat16)
 Y = torch.empty(16384, 11008, device="cuda", dtype=torch.bfloat16)
 GEMM_FLOP = 2 * 16384 * 4096 * 11008
+try:
+    import pynvml
+    pynvml.nvmlInit()
+    _h = pynvml.nvmlDeviceGetHandleByIndex(torch.cuda.current_device())
+except Exception:
+    _h = None
+
+
+class Clocks:
+    """SM clock samples (NVML, 2 ms) while a condition runs: the packed update is ALU-bound, so its
+    time follows the SM clock, which the GEMMs' power draw pulls below max (sw_power_cap)."""
+
+    def __enter__(self):
+        self.s, self.stop = [], False
+        self.t = threading.Thread(target=self._run, daemon=True)
+        if _h is not None:
+            self.t.start()
+        return self
+
+    def _run(self):
+        while not self.stop:
+            self.s.append(pynvml.nvmlDeviceGetClockInfo(_h, pynvml.NVML_CLOCK_SM))
+            time.sleep(0.002)
+
+    def __exit__(self, *a):
+        self.stop = True
+        if _h is not None:
+            self.t.join()
+
+    def median(self):
+        return sorted(self.s)[len(self.s) // 2] if self.s else None
+
+
 res = {"elems": n, "algorithmic_bytes": int(BPE * n), "peak_hbm_gbs": peak,
        "gemm_shape": "bf16 [16384x4096] x [4096x11008] (Llama-2 7B MLP up-projection at 16k tokens)"}
 step = [0]
@@ -74,26 +109,28 @@ def gemms(k=12, stream=comp):
             torch.matmul(X, W, out=Y)
 
 
-def timed_adam(name, background=(), stream=hi, serial_after_gemm=False):
+def timed_adam(name, background=(), stream=hi, serial_after_gemm=False, burst=0):
     times = []
+    clk = Clocks().__enter__()
     for _ in range(reps):
         torch.cuda.synchronize()
         for b in background:
             b()
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         if serial_after_gemm:  # the compute-stream posture: the update queued behind the layer's GEMMs
-            gemms(4, stream=stream)
+            gemms(4 + burst, stream=stream)
         K.spin(300.0, 1, stream=stream)
         e0.record(stream)
         adam(stream)
         e1.record(stream)
         torch.cuda.synchronize()
         times.append(e0.elapsed_time(e1) * 1e3)
+    clk.__exit__()
     times.sort()
     med = times[len(times) // 2]
     gbs = BPE * n / (med * 1e-6) / 1e9
     res[name] = {"median_us": round(med, 1), "min_us": round(times[0], 1), "max_us": round(times[-1], 1),
-                 "GBps": round(gbs, 1), "frac": round(gbs / peak, 3) if peak else None}
+                 "GBps": round(gbs, 1), "frac": round(gbs / peak, 3) if peak else None, "sm_mhz_median": clk.median()}
 
 
 def timed_gemms(name, with_adam=False, with_copies=False, k=12):
@@ -118,21 +155,25 @@ def timed_gemms(name, with_adam=False, with_copies=False, k=12):
     res[name] = {"median_us": round(med, 1), "TFLOPs": round(k * GEMM_FLOP / (med * 1e-6) / 1e12, 1)}
 
 
-def timed_copy(name, background=()):
-    """torch D2D copy of the same algorithmic bytes: what HBM gives a plain copy under the same background."""
+def timed_copy(name, background=(), burst=0):
+    """torch D2D copy of the same algorithmic bytes: what HBM gives a plain copy under the same background
+    (burst: that many GEMMs ahead of it on its stream, as for the update after a long GEMM burst)."""
     a = torch.empty(int(BPE * n) // 2, dtype=torch.uint8, device="cuda")
     b = torch.empty_like(a)
     times = []
+    st = comp if burst else hi
     for _ in range(reps):
         torch.cuda.synchronize()
         for bg in background:
             bg()
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        K.spin(300.0, 1, stream=hi)
-        e0.record(hi)
-        with torch.cuda.stream(hi):
+        if burst:
+            gemms(burst, stream=st)
+        K.spin(300.0, 1, stream=st)
+        e0.record(st)
+        with torch.cuda.stream(st):
             b.copy_(a)
-        e1.record(hi)
+        e1.record(st)
         torch.cuda.synchronize()
         times.append(e0.elapsed_time(e1) * 1e3)
     times.sort()
@@ -153,6 +194,10 @@ timed_adam("adam_with_gemm_hi_priority", [gemms])
 timed_adam("adam_with_gemm_normal_priority", [gemms], stream=lo)
 timed_adam("adam_with_gemm_and_pcie", [gemms, copies])
 timed_adam("adam_serial_after_gemm_same_stream_with_pcie", [copies], stream=comp, serial_after_gemm=True)
+# ~150 ms of GEMMs ahead of each update: long enough for the power cap to pull the SM clock down, as in the step
+timed_adam("adam_serial_after_150ms_gemm_burst_with_pcie", [lambda: copies(64)], stream=comp, serial_after_gemm=True,
+           burst=140)
+timed_copy("copy_after_150ms_gemm_burst_with_pcie", [lambda: copies(64)], burst=144)
 timed_gemms("gemm_alone")
 timed_gemms("gemm_with_pcie_duplex", with_copies=True)
 timed_gemms("gemm_with_adam_concurrent", with_adam=True)
