@@ -88,6 +88,18 @@ for what in "$@"; do
         bench --config c3 --secondary "" --no-cpu-baseline > gpurun_out/${T}_$tag.json 2> gpurun_out/${T}_$tag.err )
       echo "$tag rc $?"
     done; done ;;
+  packedab)
+    # packed-only AdamW launches (4 CTAs/SM) vs the general kernel (3 CTAs/SM), interleaved on C3
+    for r in ${ROUNDS:-1 2 3}; do for v in packed general; do
+      ( [ $v = general ] && export TC_ADAM_GENERAL=1
+        bench --config c3 --secondary "" --no-cpu-baseline > gpurun_out/${T}_c3_${v}_r$r.json 2> gpurun_out/${T}_c3_${v}_r$r.err )
+      echo "c3 $v r$r rc $?"
+    done; done ;;
+  ncupacked)
+    # ncu --set full of the packed-only AdamW alone (64 Mi elements, tools/prof_kernels.py's split-master case)
+    timeout 900 ncu --set full --clock-control none --import-source on --kernel-name-base mangled -k regex:adamw_tma_kernelILi256ELi2ELb1 -c 1 \
+      -o gpurun_out/${T}_adamw_packed_alone python tools/prof_kernels.py --reps 1 --out /tmp/k.json \
+      > gpurun_out/${T}_ncupacked.log 2>&1; echo "ncu packed rc $?" ;;
   *) echo "unknown recipe $what"; exit 2 ;;
   esac
 done
