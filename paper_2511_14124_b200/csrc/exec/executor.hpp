@@ -327,22 +327,18 @@ class Executor {
   void flush_updates();
   void flush_if_touched(const std::vector<Req>& reqs);
   std::vector<std::pair<std::int32_t, std::int32_t>> deferred_;  // hoisted updates waiting for a batch
-  // Hoisted updates per fused AdamW launch. On its own stream (compute-bound
-  // traces, ZeRO-3) each launch waits for SMs behind the concurrent layer
-  // compute and pays the front-end latency of a second stream: batches of 8
-  // amortise that (C3, packed states: event-timed 0.34 / 0.42 / 0.49 / 0.54
-  // of the HBM peak at 1 / 2 / 4 / 8, step time unchanged,
-  // profiles/r02_adam_batch_packed.json). On the compute stream
-  // (migration-bound) single updates keep each state's write-back earliest
-  // (C2 steps 2-4 % shorter, profiles/r02_adam_batch_ab.json); a ZeRO-3
-  // rank at world 1 keeps batches of 8 there too (C3: event-timed 0.44 at 1
-  // vs 0.59 at 8, step within 0.3 %, profiles/r02_adam_placement_c3.json).
-  // TC_ADAM_BATCH overrides (1..8).
+  // Hoisted updates per fused AdamW launch: 8 on either stream (one launch's
+  // front-end latency and ramp instead of 8). On its own stream (compute-
+  // bound traces, ZeRO-3 at world > 1) each launch waits for SMs behind the
+  // concurrent layer compute (C3, packed states: event-timed 0.34 / 0.42 /
+  // 0.49 / 0.54 of the HBM peak at 1 / 2 / 4 / 8, step time unchanged,
+  // profiles/r02_adam_batch_packed.json); on the compute stream (migration-
+  // bound traces, world-1 ZeRO-3) C3 0.44 -> 0.59, C5 0.49 -> 0.65, C2 0.49 ->
+  // 0.56 with steps within 0.5 % (profiles/r02_adam_placement_c3.json,
+  // r02_adam_batch_compute.json). TC_ADAM_BATCH overrides (1..8).
   static constexpr std::size_t kAdamBatchConcurrent = 8;
   std::size_t adam_batch_env_ = 0;
-  std::size_t adam_batch() const {
-    return adam_batch_env_ ? adam_batch_env_ : adam_stream() == opt_ || z3_ ? kAdamBatchConcurrent : 1;
-  }
+  std::size_t adam_batch() const { return adam_batch_env_ ? adam_batch_env_ : kAdamBatchConcurrent; }
   std::size_t stage_state(TensorRec& s);
   void refill_stages(std::size_t want_staged);
   // NVMe lookahead: the iteration's NVMe -> pinned fetches of optimizer states
