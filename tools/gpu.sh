@@ -16,6 +16,10 @@
 #   ncu        ncu --set full of the fused AdamW inside a C3 step
 #   kernels    every data-plane kernel alone at >= 1 GB per launch (events + ncu DRAM bytes)
 #   sanitize   compute-sanitizer memcheck / racecheck / synccheck over tools/sanitize.py
+#   contention the packed AdamW alone / beside PCIe DMA / beside or after the GEMMs (tools/adamw_contention_r2.py)
+#   adamstream C3 AdamW placement A/B (compute vs optimizer stream, batch size)
+#   packedab   C3 packed-only 4-CTA AdamW launches vs the general 3-CTA kernel (TC_ADAM_GENERAL), ROUNDS rounds
+#   ncupacked  ncu --set full of the packed AdamW alone
 cd "${GRAFT_REPO_ROOT:-$(dirname "$0")/..}" || exit 1
 mkdir -p gpurun_out
 T=${TAG:-run}
